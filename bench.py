@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Headline benchmark: Warp Cortex Topological Synapse hot path on B200.
+
+Metric (BASELINE.json): synapse compressions/s (L=8K, k=164) + agent decode
+steps/s at N=100/1000.  Workload = configs[1] ("0.5B-class shape"): 24 layers x
+2 KV heads x d=64 (14 q-heads, 7 per KV head), L=8192 context rows per group,
+k=164 landmarks (98% compression), lambda=0.5, N=100 agents with T=32 private
+rows each decoding against the shared synapse.
+
+A step = one synapse compression (attention mass + greedy selection + landmark
+K/V gather for all 48 (layer, KV-head) groups).  `value` = compressions/s with
+inputs resident in HBM; the decode leg (N agents x 24 layers append+attend) is
+timed in the same run and reported under "decode".  `e2e` = the same metric
+through the C-ABI with HOST buffers (pinned H2D of the step's K/V/queries and
+D2H of the synapse inside the timed region).
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref, compiled from the unmodified reference sources) on the host
+cores, on a bounded sample of the same workload.
+
+Multi-GPU (torchrun): the 48 groups are sharded across ranks (strong scaling of
+one compression), followed by the single NCCL all-gather of the synapse; the
+decode leg shards agents (N per rank).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "synapse compressions/s (L=8K,k=164) + agent decode steps/s at N=100/1000"
+N_LAYERS, N_KV, N_Q, D, L, K, LAM = 24, 2, 14, 64, 8192, 164, 0.5
+G = N_LAYERS * N_KV
+T_PRIV = 32
+# algorithmic bytes per unit
+COMPRESS_BYTES = (G * L * D * 4 + G * (N_Q // N_KV) * D * 4 + 4 * G * K * D * 4 + 16 * G * K)  # 108,936,192
+
+
+def decode_bytes(n_agents, t=T_PRIV):
+    S = N_LAYERS * N_KV * K * D * 4 * 2
+    return S + n_agents * (24576 * (t + 1) + 172032)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > i + 2 and
+                          s[i + 2].lower() in ("active", "1", "yes")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle/_ref = unmodified reference sources)
+# ----------------------------------------------------------------------------
+def cpu_compress_sample(n_threads, groups, seconds_target=10.0):
+    """Time the reference's per-group compression (attention over the group's
+    7 q-heads + select_landmarks_points) over `groups` groups on n_threads
+    host threads.  Returns (compressions/s, sample description)."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle
+    ref = oracle.load_ref()
+    kind = "reference"
+    rs = np.random.default_rng(0)
+    clouds = rs.standard_normal((groups, L, D), dtype=np.float32)
+    qs = rs.standard_normal((groups, N_Q // N_KV, D), dtype=np.float32)
+    idx = np.empty((groups, K), np.int64)
+    if ref is None:
+        raise RuntimeError("oracle/_ref/libcortex_ref.so not built (run build() where /root/reference exists)")
+    P = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        st = ref.lib.ref_compress_groups_mt(groups, P(clouds, C.c_float), C.c_int64(L), D, P(qs, C.c_float),
+                                            N_Q // N_KV, K, C.c_double(LAM), n_threads, P(idx, C.c_int64))
+        if st != 0:
+            raise RuntimeError("reference compression failed")
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds_target or reps >= 50:
+            break
+    value = reps * groups / G / el
+    return value, kind, f"{reps} x {groups} of 48 groups (L=8192, k=164, 7 q-heads) on {n_threads} threads, {el:.1f} s"
+
+
+def cpu_decode_sample(n_threads, n_agents, seconds_target=5.0):
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle
+    ref = oracle.load_ref()
+    rs = np.random.default_rng(1)
+    syn_k = rs.standard_normal((N_LAYERS, N_KV, K, D), dtype=np.float32)
+    syn_v = rs.standard_normal((N_LAYERS, N_KV, K, D), dtype=np.float32)
+    T = T_PRIV + 1
+    tk = rs.standard_normal((n_agents, N_LAYERS, N_KV, T, D), dtype=np.float32)
+    tv = rs.standard_normal((n_agents, N_LAYERS, N_KV, T, D), dtype=np.float32)
+    q = rs.standard_normal((n_agents, N_LAYERS, N_Q, D), dtype=np.float32)
+    out = np.empty_like(q)
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        st = ref.lib.ref_decode_attend_mt(n_agents, N_LAYERS, N_KV, N_Q, D, K, T, P(syn_k), P(syn_v), P(tk), P(tv),
+                                          P(q), P(out), n_threads)
+        if st != 0:
+            raise RuntimeError("reference decode failed")
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds_target or reps >= 100:
+            break
+    return reps * n_agents / el, f"{reps} x {n_agents} agents x 24 layers x 14 q-heads, n={K}+{T}, {n_threads} threads"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    groups = min(G, max(threads, 8))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, kind, sample = cpu_compress_sample(threads, groups, seconds_target=0.0)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    dec, dsample = cpu_decode_sample(threads, args.n_agents, seconds_target=1.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "compressions/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: 24 layers x 2 KV heads x d=64, L=8192 -> k=164, lambda=0.5, 14 q-heads; "
+                               f"decode N={args.n_agents}, T={T_PRIV}",
+                   "sample_groups_per_step": groups},
+        "cpu_baseline": {"value": value, "unit": "compressions/s", "cores": threads, "kind": "reference",
+                         "sample": f"{groups} of 48 groups per step on {threads} threads"},
+        "decode": {"agent_steps_per_s": dec, "n_agents": args.n_agents, "sample": dsample},
+        "e2e": {"value": value, "unit": "compressions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# B200 arm
+# ----------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_01298_b200 import device as cxd
+    from paper_2601_01298_b200.parallel import all_gather_groups, shard_range
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    gb, ge = shard_range(G, rank, world)
+    g_local = ge - gb
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    keys = torch.randn(g_local, L, D, device=dev, generator=gen)
+    values = torch.randn(g_local, L, D, device=dev, generator=gen)
+    queries = torch.randn(g_local, N_Q // N_KV, D, device=dev, generator=gen)
+    take = K
+    rows = torch.empty(g_local, take, dtype=torch.int64, device=dev)
+    scores = torch.empty(g_local, take, dtype=torch.float64, device=dev)
+    sk = torch.empty(g_local, take, D, device=dev)
+    sv = torch.empty(g_local, take, D, device=dev)
+    attn = torch.empty(g_local, L, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    # one full compression through the single C-ABI call (attention + select + gather)
+    def full_compress():
+        return cxd.compress_grouped(keys, values, queries, K, LAM, out=(rows, scores, sk, sv))
+
+    # warm-up
+    for _ in range(max(args.warmup, 3)):
+        full_compress()
+    torch.cuda.synchronize()
+
+    # ---- timed: compression with inputs resident in HBM, L2 flushed between steps
+    launches0 = cxd.kernel_launch_count()
+    times, sel_times = [], []
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(stream)
+            a = cxd.attention_grouped(keys, queries)
+            e[1].record(stream)
+            r, s = cxd.select_grouped(keys, a, K, LAM)
+            e[2].record(stream)
+            # landmark K/V gather (A5) through the grouped C-ABI on the chosen rows
+            cxd.gather_rows(keys, r, sk)
+            cxd.gather_rows(values, r, sv)
+            if world > 1:
+                all_gather_groups([r, s, sk, sv], G)
+            e[3].record(stream)
+            torch.cuda.synchronize()
+            times.append(e[0].elapsed_time(e[3]))
+            sel_times.append(e[1].elapsed_time(e[2]))
+        torch.cuda.synchronize()
+    launches = cxd.kernel_launch_count() - launches0
+    ms = statistics.mean(times)
+    sel_ms = statistics.mean(sel_times)
+    if world > 1:
+        t = torch.tensor([ms, sel_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, sel_ms = float(t[0]), float(t[1])
+    value = 1000.0 / ms  # one compression of all 48 groups per step (strong scaling)
+    return finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, values, queries)
+
+
+def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, values, queries):
+    import torch
+
+    from paper_2601_01298_b200 import device as cxd
+    hbm, peak_kind = load_peaks()
+    # roofline of the dominant kernel (greedy selection) against HBM
+    bytes_per_launch = COMPRESS_BYTES * keys.shape[0] / G
+    achieved = bytes_per_launch / (sel_ms * 1e-3) / 1e9
+    dec = run_decode(args, dev) if rank == 0 or True else None
+    e2e = run_e2e(args, dev) if rank == 0 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "compressions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (torch.randn N(0,1) keys/values/queries)",
+        "config": {"workload": "cfg2 (BASELINE configs[1]): 24 layers x 2 KV heads x d=64, 14 q-heads, "
+                               f"L=8192 -> k=164 (98%), lambda=0.5; decode N={args.n_agents} agents, T={T_PRIV}",
+                   "groups": G, "parallelism": f"groups sharded over {world} GPU(s)",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "roofline": {"kernel": "select_kernel (greedy max-min selection)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "peak_source": peak_kind, "traffic": None,
+                     "note": "selection is fp64/FMA-issue + barrier-latency bound (SURVEY.md §8(d)); "
+                             "HBM fraction reported as required"},
+        "select_ms": sel_ms,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if dec is not None:
+        line["decode"] = dec
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        try:
+            v, kind, sample = cpu_compress_sample(threads, min(G, max(threads, 8)), seconds_target=8.0)
+            line["cpu_baseline"] = {"value": v, "unit": "compressions/s", "cores": threads, "kind": kind,
+                                    "sample": sample}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": "compressions/s", "cores": threads, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_decode(args, dev):
+    import torch
+
+    from paper_2601_01298_b200 import device as cxd
+    out = {}
+    hbm, _ = load_peaks()
+    for n in sorted({args.n_agents, 1000}):
+        gen = torch.Generator(device=dev).manual_seed(99)
+        syn_k = torch.randn(N_LAYERS, N_KV, K, D, device=dev, generator=gen)
+        syn_v = torch.randn(N_LAYERS, N_KV, K, D, device=dev, generator=gen)
+        tk = torch.randn(n, N_LAYERS, N_KV, T_PRIV + 1, D, device=dev, generator=gen)
+        tv = torch.randn(n, N_LAYERS, N_KV, T_PRIV + 1, D, device=dev, generator=gen)
+        tl = torch.full((n,), T_PRIV, dtype=torch.int32, device=dev)
+        nk = torch.randn(n, N_LAYERS, N_KV, D, device=dev, generator=gen)
+        nv = torch.randn(n, N_LAYERS, N_KV, D, device=dev, generator=gen)
+        q = torch.randn(n, N_LAYERS, N_Q, D, device=dev, generator=gen)
+        o = torch.empty_like(q)
+        for _ in range(3):
+            cxd.decode_step(syn_k, syn_v, tk, tv, tl, q, o, nk, nv)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        e0.record()
+        for _ in range(reps):
+            cxd.decode_step(syn_k, syn_v, tk, tv, tl, q, o, nk, nv)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        b = decode_bytes(n)
+        out[f"N{n}"] = {"agent_steps_per_s": n / (ms * 1e-3), "ms_per_step": ms,
+                        "roofline": {"bound": "hbm", "achieved": b / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                     "frac": b / (ms * 1e-3) / 1e9 / hbm, "bytes": b}}
+    return out
+
+
+def run_e2e(args, dev):
+    """compressions/s through the C-ABI with HOST buffers: pinned H2D of the
+    step's keys, values and queries, the compression, D2H of the synapse."""
+    import torch
+
+    from paper_2601_01298_b200 import device as cxd
+    hk = torch.randn(G, L, D).pin_memory()
+    hv = torch.randn(G, L, D).pin_memory()
+    hq = torch.randn(G, N_Q // N_KV, D).pin_memory()
+    dk = torch.empty(G, L, D, device=dev)
+    dv = torch.empty(G, L, D, device=dev)
+    dq = torch.empty(G, N_Q // N_KV, D, device=dev)
+    outs = (torch.empty(G, K, dtype=torch.int64, device=dev), torch.empty(G, K, dtype=torch.float64, device=dev),
+            torch.empty(G, K, D, device=dev), torch.empty(G, K, D, device=dev))
+    h_rows = torch.empty(G, K, dtype=torch.int64).pin_memory()
+    h_sk = torch.empty(G, K, D).pin_memory()
+    h_sv = torch.empty(G, K, D).pin_memory()
+
+    def step():
+        dk.copy_(hk, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        dq.copy_(hq, non_blocking=True)
+        cxd.compress_grouped(dk, dv, dq, K, LAM, out=outs)
+        h_rows.copy_(outs[0], non_blocking=True)
+        h_sk.copy_(outs[2], non_blocking=True)
+        h_sv.copy_(outs[3], non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    reps = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    h2d = (hk.numel() + hv.numel() + hq.numel()) * 4
+    d2h = h_rows.numel() * 8 + (h_sk.numel() + h_sv.numel()) * 4
+    return {"value": 1000.0 / ms, "unit": "compressions/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": ms}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-agents", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    run_b200(args)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

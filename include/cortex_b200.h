@@ -1,0 +1,264 @@
+/*
+ * cortex_b200.h -- C-ABI of the B200-native Topological Synapse hot path.
+ *
+ * The reference (/root/reference/proj) is a C++20 library with no FFI layer;
+ * its hot path is the cortex:: header API compiled into cortex_core
+ * (SURVEY.md §8(b)).  This header is the drop-in boundary: one extern "C"
+ * entry point per reference function on the path (the citation on each line
+ * is the cortex:: declaration it replaces), plain pointers + sizes, no torch
+ * or CUDA types (streams are passed as void* = cudaStream_t).  The C++ shim
+ * in include/cortex/*.hpp re-exports the exact cortex:: declarations on top
+ * of these entry points, so code written against the reference links
+ * unchanged.
+ *
+ * Error convention: every call returns cx_status.  Categories map 1:1 onto
+ * the reference's exception types (proj/include/cortex/errors.hpp:10-41) and
+ * validation happens before any device work, as in the reference.  A failed
+ * CUDA call returns CX_DEVICE_ERROR (never one of the reference categories).
+ * cx_last_error() returns the thread-local message of the last failure.
+ *
+ * Pointer conventions:
+ *   *_host entry points and the un-suffixed reference-shaped calls take HOST
+ *   pointers, are synchronous, and have the reference's semantics;
+ *   *_dev entry points take DEVICE pointers and are ordered on `stream`.
+ * There is no CPU fallback: without a CUDA device every compute call returns
+ * CX_DEVICE_ERROR.
+ */
+#ifndef CORTEX_B200_H
+#define CORTEX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CX_ABI_VERSION 1
+
+typedef enum cx_status {
+    CX_OK = 0,
+    CX_CONFIG_ERROR = 1,           /* cortex::config_error          errors.hpp:13 */
+    CX_CAPACITY_ERROR = 2,         /* cortex::capacity_error        errors.hpp:18 */
+    CX_TOPOLOGY_ERROR = 3,         /* cortex::topology_error        errors.hpp:23 */
+    CX_SEQUENCING_ERROR = 4,       /* cortex::sequencing_error      errors.hpp:28 */
+    CX_PRECONDITION_ERROR = 5,     /* cortex::precondition_error    errors.hpp:32 */
+    CX_CAP_ERROR = 6,              /* cortex::cap_error             errors.hpp:37 */
+    CX_DEGENERATE_INPUT_ERROR = 7, /* cortex::degenerate_input_error errors.hpp:41 */
+    CX_DEVICE_ERROR = 100,         /* CUDA failure / no device (new; never a reference type) */
+    CX_INVALID_ARGUMENT = 101      /* null handle / impossible size at the C boundary (new) */
+} cx_status;
+
+typedef enum cx_origin { CX_ORIGIN_CONTEXT = 0, CX_ORIGIN_INJECTED = 1 } cx_origin; /* model.hpp:16 */
+
+int cx_abi_version(void);
+const char* cx_last_error(void);
+/* Number of sm_100a kernel launches this process issued (all entry points). */
+uint64_t cx_kernel_launch_count(void);
+
+/* ======================================================================
+ * Point-level synapse operations, reference semantics, HOST pointers.
+ * ====================================================================== */
+
+/* synapse.hpp:62-64 attention_scores_points(const PointCloud&, span<const float> query, int n_heads) */
+cx_status cx_attention_scores_points(const float* keys, int64_t count, int dim,
+                                     const float* query, int64_t query_len, int n_heads,
+                                     double* out /* [count] */);
+
+/* synapse.hpp:73-74 coverage_scores_points(const PointCloud&, span<const int64_t> selected) */
+cx_status cx_coverage_scores_points(const float* cloud, int64_t count, int dim,
+                                    const int64_t* selected, int64_t n_selected,
+                                    double* out /* [count] */);
+
+/* synapse.hpp:104-106 select_landmarks_points(const PointCloud&, span<const double>, int k, double lambda)
+ * out_indices/out_scores must hold min(k, count) entries; *out_n receives it. */
+cx_status cx_select_landmarks_points(const float* cloud, int64_t count, int dim,
+                                     const double* attention, int64_t attention_len,
+                                     int k, double lambda,
+                                     int64_t* out_indices, double* out_scores, int64_t* out_n);
+
+/* synapse.hpp:83-91 metrics */
+cx_status cx_hausdorff_distance(const float* cloud, int64_t count, int dim,
+                                const float* landmarks, int64_t m, int ldim, double* out);
+cx_status cx_hausdorff_to_subset(const float* cloud, int64_t count, int dim,
+                                 const int64_t* rows, int64_t n_rows, double* out);
+cx_status cx_mean_pairwise_reduction(const float* cloud, int64_t count, int dim,
+                                     const float* landmarks, int64_t m, int ldim, double* out);
+cx_status cx_mean_pairwise_reduction_subset(const float* cloud, int64_t count, int dim,
+                                            const int64_t* rows, int64_t n_rows, double* out);
+
+/* kernels.hpp:40-42 attend(q, keys, values, n_entries, n_heads, d_k, out)
+ * fp64 accumulation like the reference (tolerance 1e-6, test_kernels.cpp:159). */
+cx_status cx_attend(const float* q, const float* keys, const float* values,
+                    int64_t n_entries, int n_heads, int d_k, float* out);
+
+/* ======================================================================
+ * Grouped device path (per-(layer, KV-head) groups).
+ * ====================================================================== */
+
+typedef struct cx_ctx cx_ctx; /* device workspace + default stream; one per host thread */
+
+cx_status cx_ctx_create(int device, cx_ctx** out);
+cx_status cx_ctx_destroy(cx_ctx* ctx);
+
+/* A batch of G independent selection groups.  Group g's cloud row i, column c
+ * is clouds[g * group_stride + i * row_stride + c] (fp32, device).  Queries:
+ * queries[(g * n_pass + p) * d_k + c].  Pass p scores columns
+ * [p * col_step, p * col_step + d_k) -- col_step = d_k reproduces the
+ * reference's head-concatenated MHA cloud (attention_scores_points with
+ * n_heads = n_pass, synapse.cpp:200-230); col_step = 0 is the GQA group mode
+ * (sum over the group's q-heads of attention_scores_points(cloud, q_h, 1)). */
+typedef struct cx_groups {
+    int n_groups;
+    int64_t count;       /* L rows per group */
+    int dim;             /* cloud width */
+    const float* clouds; /* device */
+    int64_t group_stride;
+    int64_t row_stride;
+    const float* queries; /* device, [G][n_pass][d_k] */
+    int n_pass;
+    int d_k;
+    int col_step;
+} cx_groups;
+
+/* attention mass per row for every group: out[G][count] (device, fp64). */
+cx_status cx_attention_grouped_dev(cx_ctx* ctx, const cx_groups* g, double* out, void* stream);
+
+/* Greedy hybrid selection (synapse.cpp:353-421) for every group given its
+ * attention [G][count] (device).  Outputs (device): rows [G][take] ascending,
+ * scores [G][take], take = min(k, count).  flags: CX_SELECT_* below. */
+#define CX_SELECT_EXACT_ONLY 1u /* disable the conservative fp32 distance filter */
+cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* attention,
+                                int k, double lambda, unsigned flags,
+                                int64_t* out_rows, double* out_scores, void* stream);
+
+/* Landmark gather (synapse.cpp:440-455 copy, per group): dst[g][s][:] =
+ * src row rows[g][s] of group g (same addressing as g->clouds, base `src`). */
+cx_status cx_gather_grouped_dev(cx_ctx* ctx, const cx_groups* g, const float* src,
+                                const int64_t* rows, int take, float* dst, void* stream);
+
+/* One synapse compression: attention + selection + landmark K/V gather.
+ * values: same addressing as g->clouds (separate base pointer).  Outputs
+ * (device): rows/scores [G][take], syn_keys/syn_values [G][take][dim]. */
+cx_status cx_compress_grouped_dev(cx_ctx* ctx, const cx_groups* g, const float* values,
+                                  int k, double lambda, unsigned flags,
+                                  int64_t* out_rows, double* out_scores,
+                                  float* syn_keys, float* syn_values, void* stream);
+
+/* ======================================================================
+ * Batched decode attention of N agents against the shared synapse
+ * (kernels.cpp:103-142 per (agent, layer, q-head), fp32 accumulate).
+ * ====================================================================== */
+typedef struct cx_decode_batch {
+    int n_agents, n_layers, n_kv, n_q, d_k;
+    int k_syn;                 /* synapse rows per (layer, kv head) */
+    const float* syn_keys;     /* [n_layers][n_kv][k_syn][d_k] */
+    const float* syn_values;
+    float* tail_keys;          /* [N][n_layers][n_kv][t_cap][d_k]  private rows */
+    float* tail_values;
+    int t_cap;
+    const int32_t* tail_len;   /* [N] rows already in each private tail */
+    const float* new_keys;     /* [N][n_layers][n_kv][d_k]  appended at tail_len (or NULL) */
+    const float* new_values;
+    const float* q;            /* [N][n_layers][n_q][d_k] */
+    float* out;                /* [N][n_layers][n_q][d_k] */
+} cx_decode_batch;
+
+cx_status cx_decode_step_dev(cx_ctx* ctx, const cx_decode_batch* b, void* stream);
+
+/* ======================================================================
+ * Device-resident KvCache (model.hpp:67-113) and Referential Injection.
+ * Layout: keys/values [n_layers][capacity][d_model] fp32, positions int64,
+ * origins u8.  Checks and error categories follow model.cpp:124-173.
+ * ====================================================================== */
+typedef struct cx_kvcache cx_kvcache;
+
+cx_status cx_kvcache_create(int n_layers, int n_heads, int d_model, int d_k,
+                            int64_t max_positions, int64_t capacity, cx_kvcache** out);
+cx_status cx_kvcache_destroy(cx_kvcache* c);
+int64_t cx_kvcache_size(const cx_kvcache* c);
+int64_t cx_kvcache_context_count(const cx_kvcache* c);
+int64_t cx_kvcache_last_context_position(const cx_kvcache* c);
+int cx_kvcache_entry_open(const cx_kvcache* c);
+int64_t cx_kvcache_capacity(const cx_kvcache* c);
+/* device base pointers (layer-major) for zero-copy consumers */
+float* cx_kvcache_keys_dev(cx_kvcache* c);
+float* cx_kvcache_values_dev(cx_kvcache* c);
+const int64_t* cx_kvcache_positions_host(const cx_kvcache* c);
+const uint8_t* cx_kvcache_origins_host(const cx_kvcache* c);
+
+cx_status cx_kvcache_begin_entry(cx_kvcache* c, int64_t position, cx_origin origin); /* model.cpp:124-140 */
+cx_status cx_kvcache_write_layer(cx_kvcache* c, int layer, const float* key, const float* value,
+                                 int64_t width);                                      /* model.cpp:142-152 */
+cx_status cx_kvcache_end_entry(cx_kvcache* c);                                        /* model.cpp:154-159 */
+cx_status cx_kvcache_append_entry(cx_kvcache* c, int64_t position, cx_origin origin,
+                                  const float* keys, const float* values);            /* model.cpp:161-173 */
+/* copy rows [first, first+n) of one layer to host */
+cx_status cx_kvcache_read(const cx_kvcache* c, int layer, int64_t first, int64_t n,
+                          float* keys_out, float* values_out);
+
+/* injector.hpp:27-35 */
+typedef struct cx_injection_record {
+    int64_t thought_id;
+    int64_t token_count;
+    int64_t virtual_position_base;
+    int64_t applied_at_stream_position;
+} cx_injection_record;
+
+/* injector.hpp:46-47 inject(KvCache&, const KvBlock&, thought_id, stream_position).
+ * block keys/values: [n_layers][token_count][d_model]; *_host = host pointers,
+ * *_dev = device pointers ordered on stream. */
+cx_status cx_inject_host(cx_kvcache* c, const float* keys, const float* values,
+                         int64_t base_position, int64_t token_count, int n_layers, int d_model,
+                         int64_t thought_id, int64_t stream_position, cx_injection_record* rec);
+cx_status cx_inject_dev(cx_kvcache* c, const float* keys, const float* values,
+                        int64_t base_position, int64_t token_count, int n_layers, int d_model,
+                        int64_t thought_id, int64_t stream_position, cx_injection_record* rec,
+                        void* stream);
+
+/* ======================================================================
+ * Cache-level selection (synapse.hpp:110-111 select_landmarks) and the
+ * SynapseBuffer (synapse.hpp:115-135).
+ * ====================================================================== */
+typedef struct cx_snapshot cx_snapshot;
+
+cx_status cx_select_landmarks(const cx_kvcache* c, const float* query, int64_t query_len, int k,
+                              double lambda, cx_snapshot** out);
+/* A snapshot from host data (SynapseSnapshot built by value, synapse.hpp:37-49):
+ * positions/scores [count]; keys/values [count][n_layers][d_model] (may be NULL
+ * when count == 0).  The K/V are copied to the device. */
+cx_status cx_snapshot_create(int64_t source_length, int k_configured, int n_layers, int d_model,
+                             int64_t count, const int64_t* positions, const double* scores,
+                             const float* keys, const float* values, cx_snapshot** out);
+cx_status cx_snapshot_destroy(cx_snapshot* s);
+uint64_t cx_snapshot_version(const cx_snapshot* s);
+int64_t cx_snapshot_source_length(const cx_snapshot* s);
+int cx_snapshot_k_configured(const cx_snapshot* s);
+int cx_snapshot_n_layers(const cx_snapshot* s);
+int cx_snapshot_d_model(const cx_snapshot* s);
+int64_t cx_snapshot_count(const cx_snapshot* s);
+/* host copies: positions/scores [count]; keys/values [count][n_layers][d_model] */
+cx_status cx_snapshot_read(const cx_snapshot* s, int64_t* positions, double* scores,
+                           float* keys, float* values);
+/* device views: keys/values [n_layers][count][d_model] (decode-friendly) */
+const float* cx_snapshot_keys_dev(const cx_snapshot* s);
+const float* cx_snapshot_values_dev(const cx_snapshot* s);
+
+typedef struct cx_synapse_buffer cx_synapse_buffer;
+cx_status cx_synapse_buffer_create(cx_synapse_buffer** out);
+cx_status cx_synapse_buffer_destroy(cx_synapse_buffer* b);
+/* Takes ownership of snap; stamps and returns the version (1, 2, ...). */
+cx_status cx_synapse_buffer_push(cx_synapse_buffer* b, cx_snapshot* snap, uint64_t* version);
+/* *out = NULL before the first push; the returned reference must be released
+ * with cx_snapshot_release (shared ownership, like shared_ptr<const>). */
+cx_status cx_synapse_buffer_read_latest(cx_synapse_buffer* b, const cx_snapshot** out);
+cx_status cx_synapse_buffer_wait_nonempty(cx_synapse_buffer* b, int64_t timeout_ms,
+                                          const cx_snapshot** out);
+cx_status cx_synapse_buffer_shutdown(cx_synapse_buffer* b);
+cx_status cx_snapshot_release(const cx_snapshot* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CORTEX_B200_H */

@@ -1,0 +1,80 @@
+"""In-tree build of libcortex_b200.so (sm_100a) with nvcc.
+
+The shared library holds the CUDA kernels, the extern "C" boundary
+(include/cortex_b200.h) and the C++ cortex:: drop-in shim (include/cortex/).
+It is written next to this file so it travels to the GPU box with the repo.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libcortex_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+CU_SOURCES = ["synapse_kernels.cu", "attend_kernels.cu", "capi.cu"]
+CPP_SOURCES = ["cortex_api.cpp"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++20",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+    "--expt-relaxed-constexpr",
+    "-I" + INCLUDE, "-I" + CSRC,
+]
+
+
+def _sources():
+    srcs = [os.path.join(CSRC, s) for s in CU_SOURCES]
+    srcs += [os.path.join(CSRC, s) for s in CPP_SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    return srcs
+
+
+def _deps():
+    out = []
+    for d in (CSRC, INCLUDE, os.path.join(INCLUDE, "cortex")):
+        if os.path.isdir(d):
+            out += [os.path.join(d, f) for f in os.listdir(d)]
+    return out
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    return all(os.path.getmtime(p) <= t for p in _deps() + [__file__])
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return LIB
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for src in _sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+        if src.endswith(".cu"):
+            cmd += ["-Xptxas", "-v"] if verbose else []
+        else:
+            cmd = [NVCC, "-x", "cu"] + NVCC_FLAGS + ["-c", src, "-o", obj] if False else \
+                  ["g++", "-std=c++20", "-O3", "-fPIC", "-I" + INCLUDE, "-I/usr/local/cuda/include", "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    tmp = LIB + ".tmp"
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs + ["-lcudart_static", "-lpthread", "-ldl", "-lrt"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

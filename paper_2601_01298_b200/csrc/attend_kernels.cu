@@ -1,0 +1,283 @@
+// attend_kernels.cu -- decode attention against the shared synapse (SURVEY.md
+// §8(a) A9) and the KV append used by Referential Injection (A10/A11).
+//
+// attend_fp64: the reference-shaped kernels::attend (kernels.cpp:147-186) for
+//   the drop-in call, fp64 scores/softmax/accumulation (reference tolerance
+//   1e-6, test_kernels.cpp:159-160).
+// decode_step: one decode step of N agents.  For every (agent, layer, q-head)
+//   the agent's cache is [k synapse rows of its KV head || private tail rows],
+//   exactly what run_agent builds by copying the snapshot (scheduler.cpp:
+//   245-262) -- here the synapse is shared, not copied.  The new token's K/V
+//   is appended to the private tail first (fused), then attended, fp32
+//   accumulate (north_star tolerance 1e-3 relative).
+#include "cx_internal.cuh"
+
+namespace cx {
+
+namespace {
+
+template <class T, class Op>
+__device__ __forceinline__ T warp_all(T v, Op op) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ---- attend_fp64: one block per head ---------------------------------------
+__global__ void attend_fp64_kernel(const float* __restrict__ q, const float* __restrict__ keys,
+                                   const float* __restrict__ values, int64_t n, int H, int dk,
+                                   double inv_sqrt_dk, double* __restrict__ w, float* __restrict__ out) {
+    __shared__ double red[32];
+    const int h = blockIdx.x;
+    const int dm = H * dk;
+    double* wh = w + (int64_t)h * n;
+    const float* qh = q + (int64_t)h * dk;
+    double m = -INFINITY;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const float* kj = keys + j * dm + (int64_t)h * dk;
+        double dot = 0.0;
+        for (int c = 0; c < dk; ++c) dot = __dadd_rn(dot, __dmul_rn((double)qh[c], (double)kj[c]));
+        const double s = __dmul_rn(dot, inv_sqrt_dk);
+        wh[j] = s;
+        m = (m < s) ? s : m;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    m = warp_all(m, [](double a, double b) { return (a < b) ? b : a; });
+    if (lane == 0) red[wid] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = red[0];
+        for (int i = 1; i < nw; ++i) mm = (mm < red[i]) ? red[i] : mm;
+        red[0] = mm;
+    }
+    __syncthreads();
+    m = red[0];
+    __syncthreads();
+    double acc = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const double e = exp(__dsub_rn(wh[j], m));
+        wh[j] = e;
+        acc = __dadd_rn(acc, e);
+    }
+    acc = warp_all(acc, [](double a, double b) { return __dadd_rn(a, b); });
+    if (lane == 0) red[wid] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s = __dadd_rn(s, red[i]);
+        red[0] = s;
+    }
+    __syncthreads();
+    const double sum = red[0];
+    for (int c = threadIdx.x; c < dk; c += blockDim.x) {
+        double a = 0.0;
+        for (int64_t j = 0; j < n; ++j)  // reference order over entries
+            a = __dadd_rn(a, __dmul_rn(wh[j], (double)values[j * dm + (int64_t)h * dk + c]));
+        out[(int64_t)h * dk + c] = (float)__ddiv_rn(a, sum);
+    }
+}
+
+// ---- batched decode step (fp32) ----------------------------------------------
+// grid.x = n_layers * n_kv; grid.y = agent chunks.  blockDim = apb * qpg warps:
+// warp (a_slot, hh) handles q-head g*qpg+hh of the a_slot-th agent of the batch.
+// Shared memory: synapse K,V of this (layer, kv head) [k][d_k+1] (padded, so
+// lane-per-row dot products and lane-per-column mixes are conflict-free),
+// per-agent-slot tail K,V [t_cap+1][d_k+1], per-warp q and probabilities.
+struct DecodeSmem {
+    size_t ks, vs, tk, tv, qv, pw, total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline DecodeSmem decode_layout(int k_syn, int t_rows, int dk, int apb, int warps,
+                                                    int n_max) {
+    DecodeSmem L;
+    const size_t pitch = (size_t)dk + 1;
+    size_t o = 0;
+    L.ks = o; o = al16(o + sizeof(float) * (size_t)k_syn * pitch);
+    L.vs = o; o = al16(o + sizeof(float) * (size_t)k_syn * pitch);
+    L.tk = o; o = al16(o + sizeof(float) * (size_t)apb * t_rows * pitch);
+    L.tv = o; o = al16(o + sizeof(float) * (size_t)apb * t_rows * pitch);
+    L.qv = o; o = al16(o + sizeof(float) * (size_t)warps * dk);
+    L.pw = o; o = al16(o + sizeof(float) * (size_t)warps * n_max);
+    L.total = o;
+    return L;
+}
+
+__global__ void __launch_bounds__(256) decode_step_kernel(cx_decode_batch b, int apb, int agents_per_cta,
+                                                         float inv_sqrt_dk) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int qpg = b.n_q / b.n_kv;
+    const int lh = blockIdx.x;
+    const int l = lh / b.n_kv, g = lh % b.n_kv;
+    const int dk = b.d_k, pitch = dk + 1;
+    const int t_rows = b.t_cap + 1;
+    const int warps = apb * qpg;
+    const int n_max = b.k_syn + t_rows;
+    const DecodeSmem lay = decode_layout(b.k_syn, t_rows, dk, apb, warps, n_max);
+    float* Ks = reinterpret_cast<float*>(smem + lay.ks);
+    float* Vs = reinterpret_cast<float*>(smem + lay.vs);
+    float* Tk = reinterpret_cast<float*>(smem + lay.tk);
+    float* Tv = reinterpret_cast<float*>(smem + lay.tv);
+    float* Qv = reinterpret_cast<float*>(smem + lay.qv);
+    float* Pw = reinterpret_cast<float*>(smem + lay.pw);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int a_slot = warp / qpg, hh = warp % qpg;
+
+    // synapse rows of this (layer, kv head): loaded once, reused by every agent
+    const float* sk = b.syn_keys + (size_t)lh * b.k_syn * dk;
+    const float* sv = b.syn_values + (size_t)lh * b.k_syn * dk;
+    for (int e = tid; e < b.k_syn * dk; e += nt) {
+        const int j = e / dk, c = e % dk;
+        Ks[j * pitch + c] = __ldg(sk + e);
+        Vs[j * pitch + c] = __ldg(sv + e);
+    }
+
+    const int a_begin = blockIdx.y * agents_per_cta;
+    const int a_end = min(b.n_agents, a_begin + agents_per_cta);
+    for (int a0 = a_begin; a0 < a_end; a0 += apb) {
+        __syncthreads();  // previous batch done with tails / synapse staged
+        // stage private tails (+ append the new row) for the apb agents of this batch
+        for (int s = 0; s < apb; ++s) {
+            const int a = a0 + s;
+            if (a >= a_end) break;
+            const int len = min(b.tail_len[a], b.t_cap - (b.new_keys ? 1 : 0));
+            const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * dk;
+            float* tk = Tk + (size_t)s * t_rows * pitch;
+            float* tv = Tv + (size_t)s * t_rows * pitch;
+            for (int e = tid; e < len * dk; e += nt) {
+                const int j = e / dk, c = e % dk;
+                tk[j * pitch + c] = __ldg(b.tail_keys + toff + e);
+                tv[j * pitch + c] = __ldg(b.tail_values + toff + e);
+            }
+            if (b.new_keys) {
+                const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * dk;
+                for (int c = tid; c < dk; c += nt) {
+                    const float nk = __ldg(b.new_keys + noff + c), nv = __ldg(b.new_values + noff + c);
+                    tk[len * pitch + c] = nk;
+                    tv[len * pitch + c] = nv;
+                    b.tail_keys[toff + (size_t)len * dk + c] = nk;  // append into the private cache
+                    b.tail_values[toff + (size_t)len * dk + c] = nv;
+                }
+            }
+        }
+        __syncthreads();
+        const int a = a0 + a_slot;
+        if (a < a_end) {
+            const int h = g * qpg + hh;
+            const int tn = min(b.tail_len[a], b.t_cap - (b.new_keys ? 1 : 0)) + (b.new_keys ? 1 : 0);
+            const int n = b.k_syn + tn;
+            const size_t qoff = (((size_t)a * b.n_layers + l) * b.n_q + h) * dk;
+            float* qv = Qv + (size_t)warp * dk;
+            float* pw = Pw + (size_t)warp * n_max;
+            for (int c = lane; c < dk; c += 32) qv[c] = __ldg(b.q + qoff + c);
+            __syncwarp();
+            const float* tk = Tk + (size_t)a_slot * t_rows * pitch;
+            const float* tv = Tv + (size_t)a_slot * t_rows * pitch;
+            float m = -INFINITY;
+            for (int j = lane; j < n; j += 32) {
+                const float* kr = (j < b.k_syn) ? Ks + j * pitch : tk + (j - b.k_syn) * pitch;
+                float d0 = 0.f, d1 = 0.f;
+                int c = 0;
+                for (; c + 2 <= dk; c += 2) {
+                    d0 = fmaf(qv[c], kr[c], d0);
+                    d1 = fmaf(qv[c + 1], kr[c + 1], d1);
+                }
+                if (c < dk) d0 = fmaf(qv[c], kr[c], d0);
+                const float s = (d0 + d1) * inv_sqrt_dk;
+                pw[j] = s;
+                m = fmaxf(m, s);
+            }
+            m = warp_all(m, [](float x, float y) { return fmaxf(x, y); });
+            float sum = 0.f;
+            for (int j = lane; j < n; j += 32) {
+                const float e = __expf(pw[j] - m);
+                pw[j] = e;
+                sum += e;
+            }
+            sum = warp_all(sum, [](float x, float y) { return x + y; });
+            __syncwarp();
+            const float inv = 1.0f / sum;
+            for (int c = lane; c < dk; c += 32) {
+                float acc0 = 0.f, acc1 = 0.f;
+                int j = 0;
+                for (; j + 2 <= b.k_syn; j += 2) {
+                    acc0 = fmaf(pw[j], Vs[j * pitch + c], acc0);
+                    acc1 = fmaf(pw[j + 1], Vs[(j + 1) * pitch + c], acc1);
+                }
+                for (; j < b.k_syn; ++j) acc0 = fmaf(pw[j], Vs[j * pitch + c], acc0);
+                for (int t = 0; t < tn; ++t) acc1 = fmaf(pw[b.k_syn + t], tv[t * pitch + c], acc1);
+                b.out[qoff + c] = (acc0 + acc1) * inv;
+            }
+        }
+    }
+}
+
+// ---- KV append: [n_layers][T][d_model] block into [n_layers][cap][d_model] --
+__global__ void kv_append_kernel(float* __restrict__ ck, float* __restrict__ cv, int64_t cap, int dm,
+                                 const float* __restrict__ bk, const float* __restrict__ bv, int64_t T,
+                                 int64_t dst_row) {
+    const int64_t t = blockIdx.x;
+    const int l = blockIdx.y;
+    const float* sk = bk + ((int64_t)l * T + t) * dm;
+    const float* sv = bv + ((int64_t)l * T + t) * dm;
+    float* dk = ck + ((int64_t)l * cap + dst_row + t) * dm;
+    float* dv = cv + ((int64_t)l * cap + dst_row + t) * dm;
+    if ((dm & 3) == 0 && ((reinterpret_cast<uintptr_t>(sk) | reinterpret_cast<uintptr_t>(sv) |
+                           reinterpret_cast<uintptr_t>(dk) | reinterpret_cast<uintptr_t>(dv)) & 15) == 0) {
+        for (int c = threadIdx.x; c < dm / 4; c += blockDim.x) {
+            reinterpret_cast<float4*>(dk)[c] = __ldg(reinterpret_cast<const float4*>(sk) + c);
+            reinterpret_cast<float4*>(dv)[c] = __ldg(reinterpret_cast<const float4*>(sv) + c);
+        }
+    } else {
+        for (int c = threadIdx.x; c < dm; c += blockDim.x) {
+            dk[c] = __ldg(sk + c);
+            dv[c] = __ldg(sv + c);
+        }
+    }
+}
+
+}  // namespace
+
+void attend_fp64_ws(const float* q, const float* k, const float* v, int64_t n, int H, int dk, double* w,
+                    float* out, cudaStream_t s) {
+    attend_fp64_kernel<<<H, 256, 0, s>>>(q, k, v, n, H, dk, 1.0 / std::sqrt((double)dk), w, out);
+    check_launch("attend_fp64_kernel");
+}
+
+void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
+    const int qpg = b.n_q / b.n_kv;
+    int apb = std::max(1, 8 / qpg);
+    const int warps = apb * qpg;
+    const int t_rows = b.t_cap + 1;
+    const DecodeSmem lay = decode_layout(b.k_syn, t_rows, b.d_k, apb, warps, b.k_syn + t_rows);
+    static int max_optin = -1;
+    if (max_optin < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    }
+    if (lay.total > (size_t)max_optin) fail(CX_DEVICE_ERROR, "decode_step: synapse tile exceeds shared memory");
+    const int n_lh = b.n_layers * b.n_kv;
+    const int sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
+    // aim for ~2 CTAs per SM over the whole grid; each CTA reuses its staged synapse
+    int chunks = std::max(1, (2 * sms + n_lh - 1) / n_lh);
+    chunks = std::min(chunks, (b.n_agents + apb - 1) / apb);
+    int per = (b.n_agents + chunks - 1) / chunks;
+    per = ((per + apb - 1) / apb) * apb;
+    chunks = (b.n_agents + per - 1) / per;
+    CX_CUDA(cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    decode_step_kernel<<<dim3((unsigned)n_lh, (unsigned)chunks), warps * 32, lay.total, s>>>(
+        b, apb, per, (float)(1.0 / std::sqrt((double)b.d_k)));
+    check_launch("decode_step_kernel");
+}
+
+void kv_append_rows(float* ck, float* cv, int64_t cap, int n_layers, int dm, const float* bk, const float* bv,
+                    int64_t T, int64_t dst_row, cudaStream_t s) {
+    if (T <= 0) return;
+    kv_append_kernel<<<dim3((unsigned)T, (unsigned)n_layers), 128, 0, s>>>(ck, cv, cap, dm, bk, bv, T, dst_row);
+    check_launch("kv_append_kernel");
+}
+
+}  // namespace cx

@@ -1,0 +1,164 @@
+// cx_internal.cuh -- shared plumbing for the sm_100a synapse kernels and the
+// C-ABI (include/cortex_b200.h).  Host-side errors are C++ exceptions carrying
+// a cx_status; every extern "C" entry point catches them at the boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cortex_b200.h"
+
+namespace cx {
+
+struct Failure : std::runtime_error {
+    cx_status st;
+    Failure(cx_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+[[noreturn]] inline void fail(cx_status s, const std::string& m) { throw Failure(s, m); }
+
+#define CX_CUDA(call)                                                                         \
+    do {                                                                                      \
+        cudaError_t cx_e_ = (call);                                                           \
+        if (cx_e_ != cudaSuccess)                                                             \
+            ::cx::fail(CX_DEVICE_ERROR, std::string(#call) + ": " + cudaGetErrorString(cx_e_)); \
+    } while (0)
+
+// Counts every kernel launch issued by this library (cx_kernel_launch_count).
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+inline void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(CX_DEVICE_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    count_launch();
+}
+
+void set_last_error(const std::string& m);
+
+// Runs f, mapping exceptions to cx_status (the C boundary).
+template <class F>
+cx_status guard(F&& f) {
+    try {
+        f();
+        return CX_OK;
+    } catch (const Failure& e) {
+        set_last_error(e.what());
+        return e.st;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return CX_DEVICE_ERROR;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return CX_DEVICE_ERROR;
+    }
+}
+
+// Grow-only device arena; one per cx_ctx.  take() hands out 256-byte aligned
+// slices that stay valid until reset() (called at the start of each entry point).
+struct Arena {
+    char* base = nullptr;
+    size_t cap = 0;
+    size_t used = 0;
+    void reserve(size_t bytes) {
+        if (bytes <= cap) return;
+        if (base) cudaFree(base);
+        base = nullptr;
+        cap = 0;
+        size_t want = bytes + (bytes >> 2);
+        CX_CUDA(cudaMalloc(&base, want));
+        cap = want;
+    }
+    void reset() { used = 0; }
+    template <class T>
+    T* take(size_t n) {
+        size_t off = (used + 255) & ~size_t(255);
+        size_t bytes = n * sizeof(T);
+        if (off + bytes > cap) fail(CX_DEVICE_ERROR, "workspace arena overflow (reserve too small)");
+        used = off + bytes;
+        return reinterpret_cast<T*>(base + off);
+    }
+};
+
+// Sizing pass: counts bytes a sequence of take() calls needs.
+struct ArenaPlan {
+    size_t used = 0;
+    template <class T>
+    void take(size_t n) { used = ((used + 255) & ~size_t(255)) + n * sizeof(T); }
+};
+
+}  // namespace cx
+
+struct cx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;  // used by the host-pointer (reference-shaped) calls
+    cx::Arena arena;                // device scratch
+    int* d_flag = nullptr;          // device-side error flag (softmax non-finite, ...)
+    int num_sms = 0;
+    std::mutex mu;
+};
+
+namespace cx {
+
+// Thread-local default context for the reference-shaped host calls.
+cx_ctx* default_ctx();
+
+// Device error flags written by kernels (bitmask in ctx->d_flag).
+enum : int { FLAG_NONFINITE = 1 };
+
+// ---- launch helpers implemented in the .cu files ----------------------------
+struct GroupView {  // device-side view of cx_groups
+    int G;
+    int64_t L;
+    int dim;
+    const float* X;
+    int64_t gstride, rstride;
+    const float* Q;
+    int P, d_k, col_step;
+};
+
+// attention mass: out[G][L]; uses arena scratch (scores [G][P][L] + sums [G][P]).
+void attention_grouped(cx_ctx* ctx, const GroupView& g, double* out, cudaStream_t s);
+// bytes of arena scratch attention_grouped needs
+void plan_attention(ArenaPlan& p, const GroupView& g);
+
+// greedy selection for all groups.  rows/scores out [G][take] ascending.
+void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
+                    unsigned flags, int64_t* rows, double* scores, cudaStream_t s);
+void plan_select(ArenaPlan& p, const GroupView& g, int k);
+
+// gather selected rows from a (values or keys) tensor with the group addressing.
+void gather_rows(const GroupView& g, const float* src, const int64_t* rows, int take, float* dst,
+                 cudaStream_t s);
+
+// coverage_scores_points with a non-empty selection (one group).
+void coverage_selected(const GroupView& g, const int64_t* sel, int64_t n_sel, double* out,
+                       cudaStream_t s);
+// centroid + centroid-distance coverage (one group).
+void coverage_centroid(cx_ctx* ctx, const GroupView& g, double* out, cudaStream_t s);
+
+// metrics (one cloud): sq-dist min/max reduction and pairwise means.
+void hausdorff(const float* cloud, int64_t count, int dim, const float* lm, int64_t m,
+               const int64_t* rows, double* out_worst_sq, cudaStream_t s);
+void mean_pairwise(const float* pts, int64_t count, int dim, const int64_t* rows, double* out_sum,
+                   cudaStream_t s);
+
+// attend (reference-shaped, fp64 accumulate)
+void attend_fp64_ws(const float* q, const float* k, const float* v, int64_t n, int H, int dk,
+                    double* w /* [H][n] scratch */, float* out, cudaStream_t s);
+// batched decode step (fp32 accumulate)
+void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s);
+
+// KV append: copies block [n_layers][T][d_model] (device) into the cache
+// arrays at rows [dst_row, dst_row+T) of every layer.
+void kv_append_rows(float* cache_k, float* cache_v, int64_t capacity, int n_layers, int d_model,
+                    const float* blk_k, const float* blk_v, int64_t T, int64_t dst_row,
+                    cudaStream_t s);
+
+}  // namespace cx

@@ -1,0 +1,146 @@
+"""The B200 batched path on device tensors (torch is plumbing only: device
+memory, streams).  Each call is one C-ABI entry point (include/cortex_b200.h)
+ordered on the current torch CUDA stream.
+
+Layouts (HBM, fp32):
+  keys / values      [G][L][d]              G = n_layers * n_kv selection groups
+  queries            [G][P][d_k]            P q-heads per KV head (GQA) or MHA heads
+  synapse K / V      [G][take][d]           ascending source rows
+  decode tails       [N][n_layers][n_kv][t_cap][d_k]
+  decode q / out     [N][n_layers][n_q][d_k]
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import torch
+
+from ._lib import CxDecodeBatch, CxGroups, c_vp, check, lib
+
+SELECT_EXACT_ONLY = 1
+
+_ctx_lock = threading.Lock()
+_ctxs = {}
+
+
+def ctx(device: int | None = None) -> int:
+    """Per-(thread, device) cx_ctx (workspace arena)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    key = (threading.get_ident(), device)
+    with _ctx_lock:
+        h = _ctxs.get(key)
+        if h is None:
+            p = c_vp()
+            check(lib.cx_ctx_create(int(device), C.byref(p)), "ctx_create")
+            h = _ctxs[key] = p.value
+    return h
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _groups(keys: torch.Tensor, queries: torch.Tensor | None, mode: str) -> CxGroups:
+    if keys.dtype != torch.float32 or not keys.is_cuda:
+        raise TypeError("keys must be a CUDA float32 tensor [G, L, d]")
+    G, L, d = keys.shape
+    if keys.stride(2) != 1:
+        raise ValueError("keys rows must be contiguous")
+    g = CxGroups()
+    g.n_groups, g.count, g.dim = G, L, d
+    g.clouds = keys.data_ptr()
+    g.group_stride, g.row_stride = keys.stride(0), keys.stride(1)
+    if queries is not None:
+        if queries.dtype != torch.float32 or not queries.is_contiguous() or queries.shape[0] != G:
+            raise TypeError("queries must be a contiguous CUDA float32 tensor [G, P, d_k]")
+        g.queries = queries.data_ptr()
+        g.n_pass, g.d_k = queries.shape[1], queries.shape[2]
+        g.col_step = g.d_k if mode == "mha" else 0
+    return g
+
+
+def attention_grouped(keys: torch.Tensor, queries: torch.Tensor, mode: str = "gqa") -> torch.Tensor:
+    """Attention mass per row of every group -> [G, L] fp64 (synapse.cpp:200-230)."""
+    g = _groups(keys, queries, mode)
+    out = torch.empty((g.n_groups, g.count), dtype=torch.float64, device=keys.device)
+    check(lib.cx_attention_grouped_dev(ctx(keys.device.index), C.byref(g), out.data_ptr(), _stream()),
+          "attention_grouped")
+    return out
+
+
+def select_grouped(keys: torch.Tensor, attention: torch.Tensor, k: int, lam: float, flags: int = 0):
+    """Greedy hybrid selection per group -> (rows [G, take] int64, scores [G, take] fp64)."""
+    g = _groups(keys, None, "gqa")
+    take = min(k, g.count)
+    rows = torch.empty((g.n_groups, max(take, 0)), dtype=torch.int64, device=keys.device)
+    scores = torch.empty((g.n_groups, max(take, 0)), dtype=torch.float64, device=keys.device)
+    att = attention.contiguous()
+    check(lib.cx_select_grouped_dev(ctx(keys.device.index), C.byref(g), att.data_ptr(), int(k), float(lam),
+                                    int(flags), rows.data_ptr(), scores.data_ptr(), _stream()), "select_grouped")
+    return rows, scores
+
+
+def gather_rows(src: torch.Tensor, rows: torch.Tensor, dst: torch.Tensor) -> torch.Tensor:
+    """Landmark gather: dst[g, s] = src[g, rows[g, s]] (synapse.cpp:440-455 copy)."""
+    g = _groups(src, None, "gqa")
+    if not rows.is_contiguous() or rows.dtype != torch.int64 or not dst.is_contiguous():
+        raise TypeError("rows must be contiguous int64 [G, take]; dst contiguous [G, take, d]")
+    check(lib.cx_gather_grouped_dev(ctx(src.device.index), C.byref(g), src.data_ptr(), rows.data_ptr(),
+                                    int(rows.shape[1]), dst.data_ptr(), _stream()), "gather_rows")
+    return dst
+
+
+def compress_grouped(keys: torch.Tensor, values: torch.Tensor, queries: torch.Tensor, k: int, lam: float,
+                     mode: str = "gqa", flags: int = 0, out=None):
+    """One synapse compression for G groups: attention + greedy selection +
+    landmark K/V gather.  Returns (rows, scores, syn_keys [G,take,d], syn_values)."""
+    g = _groups(keys, queries, mode)
+    if values.shape != keys.shape or values.stride() != keys.stride():
+        raise ValueError("values must match keys' shape and strides")
+    take = min(k, g.count)
+    if out is None:
+        dev = keys.device
+        out = (torch.empty((g.n_groups, take), dtype=torch.int64, device=dev),
+               torch.empty((g.n_groups, take), dtype=torch.float64, device=dev),
+               torch.empty((g.n_groups, take, g.dim), dtype=torch.float32, device=dev),
+               torch.empty((g.n_groups, take, g.dim), dtype=torch.float32, device=dev))
+    rows, scores, sk, sv = out
+    check(lib.cx_compress_grouped_dev(ctx(keys.device.index), C.byref(g), values.data_ptr(), int(k), float(lam),
+                                      int(flags), rows.data_ptr(), scores.data_ptr(), sk.data_ptr(), sv.data_ptr(),
+                                      _stream()), "compress_grouped")
+    return out
+
+
+def decode_step(syn_keys: torch.Tensor, syn_values: torch.Tensor, tail_keys: torch.Tensor,
+                tail_values: torch.Tensor, tail_len: torch.Tensor, q: torch.Tensor, out: torch.Tensor,
+                new_keys: torch.Tensor | None = None, new_values: torch.Tensor | None = None) -> torch.Tensor:
+    """One decode step of N agents against the shared synapse (append + attend).
+
+    syn_*: [n_layers, n_kv, k, d_k]; tail_*: [N, n_layers, n_kv, t_cap, d_k];
+    tail_len: [N] int32; q/out: [N, n_layers, n_q, d_k]; new_*: [N, n_layers, n_kv, d_k].
+    """
+    n_layers, n_kv, k_syn, d_k = syn_keys.shape
+    N, _, _, t_cap, _ = tail_keys.shape
+    n_q = q.shape[2]
+    for t in (syn_keys, syn_values, tail_keys, tail_values, q, out):
+        if not t.is_contiguous() or t.dtype != torch.float32:
+            raise TypeError("decode tensors must be contiguous float32")
+    if tail_len.dtype != torch.int32:
+        raise TypeError("tail_len must be int32")
+    b = CxDecodeBatch()
+    b.n_agents, b.n_layers, b.n_kv, b.n_q, b.d_k, b.k_syn = N, n_layers, n_kv, n_q, d_k, k_syn
+    b.syn_keys, b.syn_values = syn_keys.data_ptr(), syn_values.data_ptr()
+    b.tail_keys, b.tail_values = tail_keys.data_ptr(), tail_values.data_ptr()
+    b.t_cap = t_cap
+    b.tail_len = tail_len.data_ptr()
+    b.new_keys = new_keys.data_ptr() if new_keys is not None else None
+    b.new_values = new_values.data_ptr() if new_values is not None else None
+    b.q, b.out = q.data_ptr(), out.data_ptr()
+    check(lib.cx_decode_step_dev(ctx(q.device.index), C.byref(b), _stream()), "decode_step")
+    return out
+
+
+def kernel_launch_count() -> int:
+    return int(lib.cx_kernel_launch_count())

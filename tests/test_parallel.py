@@ -1,0 +1,67 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): group / agent sharding
+and the single synapse all-gather exchange."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2601_01298_b200.parallel import all_gather_groups, shard_range
+
+
+def test_shard_range_covers_exactly():
+    for n in (0, 1, 7, 48, 100, 1000):
+        for w in (1, 2, 3, 4, 8):
+            spans = [shard_range(n, r, w) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
+                assert e0 == b1
+            sizes = [e - b for b, e in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_groups, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b, e = shard_range(n_groups, rank, world)
+        # each rank "selects" its own groups: rows = group id * 1000 + s, K/V encode (g, s)
+        take, d = 5, 3
+        g = torch.arange(b, e, dtype=torch.int64)[:, None]
+        rows = g * 1000 + torch.arange(take)[None]
+        scores = rows.to(torch.float64) / 7
+        sk = rows[..., None].to(torch.float32).expand(-1, -1, d).contiguous()
+        full = all_gather_groups([rows, scores, sk], n_groups)
+        exp_rows = torch.arange(n_groups)[:, None] * 1000 + torch.arange(take)[None]
+        ok = (torch.equal(full[0], exp_rows) and torch.equal(full[1], exp_rows.to(torch.float64) / 7)
+              and torch.equal(full[2], exp_rows[..., None].to(torch.float32).expand(-1, -1, d)))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_groups", [48, 7])
+def test_all_gather_synapse_world2(n_groups):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_groups, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(0, True), (1, True)]
