@@ -128,6 +128,7 @@ cx_status cx_attention_grouped_dev(cx_ctx* ctx, const cx_groups* g, double* out,
  * attention [G][count] (device).  Outputs (device): rows [G][take] ascending,
  * scores [G][take], take = min(k, count).  flags: CX_SELECT_* below. */
 #define CX_SELECT_EXACT_ONLY 1u /* disable the conservative fp32 distance filter */
+#define CX_SELECT_GENERIC 2u    /* force the generic-dim kernel (testing) */
 cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* attention,
                                 int k, double lambda, unsigned flags,
                                 int64_t* out_rows, double* out_scores, void* stream);

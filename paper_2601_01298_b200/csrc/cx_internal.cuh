@@ -132,6 +132,10 @@ void plan_attention(ArenaPlan& p, const GroupView& g);
 void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
                     unsigned flags, int64_t* rows, double* scores, cudaStream_t s);
 void plan_select(ArenaPlan& p, const GroupView& g, int k);
+// dim-64 fast path (select64.cu); false when it does not apply
+bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
+                     unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
+                     cudaStream_t s);
 
 // gather selected rows from a (values or keys) tensor with the group addressing.
 void gather_rows(const GroupView& g, const float* src, const int64_t* rows, int take, float* dst,

@@ -1,0 +1,697 @@
+// select64.cu -- the greedy hybrid selection (SURVEY.md §8(a) A4/A6,
+// synapse.cpp:353-421) specialised for d = 64, the per-(layer, KV-head) key
+// width of the 0.5B-class shape.
+//
+// Layout: one thread-block cluster of C CTAs per group; CTA r owns rows
+// [r*S, r*S+S).  Thread t owns rows t, 512+t, 1024+t, ...; row t lives in 64
+// fp32 REGISTERS, the others in shared memory (float4-interleaved,
+// conflict-free) or, for very long contexts, in place in L2.  All per-row
+// state (running min distance, attention, bound threshold, removed flag) is in
+// the owner's registers.  Per round:
+//   U  distance update against the previous pick.  A Gram-form fp32 lower
+//      bound (packed fma.rn.f32x2) rules out rows whose min cannot change;
+//      the rest are queued and evaluated exactly in fp64 in the reference's
+//      operation order by otherwise idle threads;
+//   X1 cluster exchange of (amin, amax, cmin, cmax) over remaining rows;
+//   H  hybrid argmax: a multiply-by-reciprocal fp64 approximation ranks all
+//      rows; only rows within 1e-12 of the approximate maximum evaluate the
+//      reference's exact divisions; exact argmax via two shared atomics
+//      (max score bits, then min row among ties);
+//   X2 cluster exchange of every CTA's (score, row, |b|^2, coordinates).
+// Exchanges are DSMEM st.async pushes completing on a per-CTA mbarrier (no
+// cluster-wide barrier per round).  Every decision is bit-identical to the
+// reference.
+#include <cooperative_groups.h>
+
+#include "cx_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace cx {
+
+namespace {
+
+constexpr int D = 64;
+constexpr int NT = 512;          // threads per CTA (one register row each)
+constexpr int NW = NT / 32;
+constexpr int QCAP = 160;        // exact-evaluation queue capacity per pass
+constexpr int SPITCH = D + 1;    // staged-row pitch (conflict-free column reads)
+constexpr int MAXC = 16;
+constexpr int MAXRPT_ALL = 4;    // rows per thread (S <= 2048)
+constexpr double HYB_MARGIN = 1e-12;
+
+__device__ __forceinline__ double dmin_std(double a, double b) { return (b < a) ? b : a; }  // std::min
+__device__ __forceinline__ double dmax_std(double a, double b) { return (a < b) ? b : a; }  // std::max
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+    const uint32_t a = smem_u32(m);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint64_t a, uint64_t b, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "l"(a), "l"(b), "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+                 "r"(__float_as_uint(v.w)), "r"(rmbar)
+                 : "memory");
+}
+// packed fp32x2 FMA (sm_100): two independent fp32 FMAs per instruction
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+          "l"(*reinterpret_cast<uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
+
+struct Sel64Params {
+    const float* X;
+    int64_t gstride, rstride;
+    int64_t L;
+    const double* attn;  // [G][L]
+    const double* cen;   // [G][64]
+    int take;
+    double lambda;
+    int S;               // rows per CTA
+    int Rs;              // rows per CTA beyond the register rows (S - 512, >= 0)
+    int filter;
+    int64_t* pick_rows;
+    double* pick_scores;
+    int64_t* out_rows;
+    double* out_scores;
+    long long* trace;    // optional per-round phase timestamps (CX_SEL_TRACE=1)
+};
+
+#define STAMP(k)                                                        \
+    do {                                                                \
+        if (p.trace && p.trace != (long long*)1 && tid == 0 && rank == 0 && g == 0 && round < 4096) \
+            p.trace[round * 8 + (k)] = clock64();                       \
+    } while (0)
+
+// X2 payload header: (score, row) + (|b|^2 of the candidate row, pad)
+struct alignas(16) Hdr {
+    double score;
+    long long row;
+    double nb;
+    double pad;
+};
+
+struct Sel64Layout {
+    size_t mbar, mm, hdr, bc, cand, hw, misc, qown, qres, stage, xs, total;
+};
+
+__host__ __device__ inline size_t al(size_t x, size_t a = 16) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline Sel64Layout sel64_layout(int Rs, bool smem_rows) {
+    Sel64Layout l;
+    size_t o = 0;
+    l.mbar = o;  o = al(o + 2 * sizeof(uint64_t));
+    l.mm = o;    o = al(o + sizeof(double) * 4 * MAXC);       // X1 slots
+    l.hdr = o;   o = al(o + sizeof(Hdr) * MAXC);              // X2 headers
+    l.bc = o;    o = al(o + sizeof(float) * D * MAXC);        // X2 coordinates
+    l.cand = o;  o = al(o + sizeof(float) * D + sizeof(Hdr)); // this CTA's candidate (coords + header)
+    l.hw = o;    o = al(o + sizeof(double) * 4 * NW);         // per-warp partials
+    l.misc = o;  o = al(o + sizeof(unsigned long long) * 8);  // counters / atomics
+    l.qown = o;  o = al(o + sizeof(int) * QCAP);
+    l.qres = o;  o = al(o + sizeof(double) * 2 * QCAP);
+    l.stage = o; o = al(o + sizeof(float) * QCAP * SPITCH);
+    l.xs = o;    o = al(o + (smem_rows ? sizeof(float) * (size_t)Rs * D : 0));
+    l.total = o;
+    return l;
+}
+
+// exact sq_dist(point, pick) in the reference's order (synapse.cpp:155-162);
+// the row is read through get4(c4) -> float4, the pick as floats (exact in fp64).
+template <int UNR = 16, class Get4>
+__device__ __forceinline__ double exact_sq(Get4 get4, const float* b) {
+    double acc = 0.0;
+#pragma unroll UNR
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 v = get4(c4);
+        const float4 w = reinterpret_cast<const float4*>(b)[c4];
+        double d = __dsub_rn((double)v.x, (double)w.x);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.y, (double)w.y);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.z, (double)w.z);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.w, (double)w.w);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    return acc;
+}
+
+// same against the fp64 centroid (sq_dist(span<float>, vector<double>), synapse.cpp:164-171)
+template <int UNR = 16, class Get4>
+__device__ __forceinline__ double exact_sq_d(Get4 get4, const double* b) {
+    double acc = 0.0;
+#pragma unroll UNR
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 v = get4(c4);
+        double d = __dsub_rn((double)v.x, b[4 * c4]);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.y, b[4 * c4 + 1]);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.z, b[4 * c4 + 2]);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.w, b[4 * c4 + 3]);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    return acc;
+}
+
+// squared norm in fp64 (each square of an fp32 value is exact)
+template <int UNR = 16, class Get4>
+__device__ __forceinline__ double norm2(Get4 get4) {
+    double acc = 0.0;
+#pragma unroll UNR
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 v = get4(c4);
+        acc += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    }
+    return acc;
+}
+
+// x . b in fp32 with packed FMAs (4 independent chains)
+template <int UNR = 16, class Get4>
+__device__ __forceinline__ float dot_f32x2(Get4 get4, const float* b) {
+    float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll UNR
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 v = get4(c4);
+        const float4 w = reinterpret_cast<const float4*>(b)[c4];
+        s0 = ffma2(make_float2(v.x, v.y), make_float2(w.x, w.y), s0);
+        s1 = ffma2(make_float2(v.z, v.w), make_float2(w.z, w.w), s1);
+    }
+    return (s0.x + s0.y) + (s1.x + s1.y);
+}
+
+// Lower bound of the fp64 squared distance from the Gram form
+// S = |x|^2 + |b|^2 - 2 x.b: every fp32 rounding above is
+// covered by 64 u (|x|^2 + |b|^2), u = 2^-24, plus an underflow allowance.
+__device__ __forceinline__ float gram_lower_bound(float nx, float nb, float dot) {
+    const float sum = __fadd_rn(nx, nb);
+    const float s = __fsub_rn(sum, __fmul_rn(2.0f, dot));
+    const float e = __fmaf_ru(0x1p-18f, sum, 0x1p-100f);
+    return __fsub_rd(s, e);
+}
+
+template <int RPT, bool SMEM_ROWS>
+__global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
+    constexpr int MAXRPT = RPT;  // rows per thread of this instantiation
+    cg::cluster_group cluster = cg::this_cluster();
+    const uint32_t C = cluster.num_blocks();
+    const uint32_t rank = cluster.block_rank();
+    const int g = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int S = p.S;
+    const int64_t r0 = (int64_t)rank * S;
+    const int nrows = (int)max((int64_t)0, min((int64_t)S, p.L - r0));
+    int round = -1;  // for STAMP outside the loop
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Sel64Layout lay = sel64_layout(p.Rs, SMEM_ROWS);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
+    double* mm = reinterpret_cast<double*>(smem + lay.mm);
+    Hdr* hdr = reinterpret_cast<Hdr*>(smem + lay.hdr);
+    float* bc = reinterpret_cast<float*>(smem + lay.bc);
+    float* cand = reinterpret_cast<float*>(smem + lay.cand);
+    Hdr* cand_hdr = reinterpret_cast<Hdr*>(cand + D);
+    double* hw = reinterpret_cast<double*>(smem + lay.hw);
+    unsigned long long* misc = reinterpret_cast<unsigned long long*>(smem + lay.misc);
+    int* qown = reinterpret_cast<int*>(smem + lay.qown);
+    double* qres = reinterpret_cast<double*>(smem + lay.qres);
+    float* stage = reinterpret_cast<float*>(smem + lay.stage);
+    float4* xs4 = reinterpret_cast<float4*>(smem + lay.xs);  // [D/4][Rs] float4
+    int* qn = reinterpret_cast<int*>(&misc[0]);              // queue length
+    unsigned long long* hkey = &misc[1];                      // max exact score bits
+    unsigned long long* hrow = &misc[2];                      // min row among ties
+
+    const float* gX = p.X + g * p.gstride + r0 * p.rstride;
+
+    // ---- stage rows ---------------------------------------------------------
+    float xr[D];
+    if (tid < nrows) {
+        const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)tid * p.rstride);
+#pragma unroll
+        for (int c4 = 0; c4 < D / 4; ++c4) {
+            const float4 v = __ldg(src + c4);
+            xr[4 * c4 + 0] = v.x; xr[4 * c4 + 1] = v.y; xr[4 * c4 + 2] = v.z; xr[4 * c4 + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < D; ++c) xr[c] = 0.f;
+    }
+    const int nsm = max(0, nrows - NT);
+    if (SMEM_ROWS) {
+        for (int e = tid; e < nsm * (D / 4); e += NT) {
+            const int j = e / (D / 4), c4 = e % (D / 4);
+            xs4[(size_t)c4 * p.Rs + j] = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)(NT + j) * p.rstride) + c4);
+        }
+    }
+    auto reg4 = [&](int c4) { return make_float4(xr[4 * c4], xr[4 * c4 + 1], xr[4 * c4 + 2], xr[4 * c4 + 3]); };
+    auto far4 = [&](int j) {  // row NT + j
+        return [&, j](int c4) -> float4 {
+            if (SMEM_ROWS) return xs4[(size_t)c4 * p.Rs + j];
+            return __ldg(reinterpret_cast<const float4*>(gX + (int64_t)(NT + j) * p.rstride) + c4);
+        };
+    };
+
+    // ---- per-row state in registers: rows tid + k*NT -------------------------
+    const int nr = tid < nrows ? 1 + (nrows - 1 - tid) / NT : 0;
+    double m[MAXRPT], a[MAXRPT];
+    float th[MAXRPT], nx[MAXRPT];
+    uint32_t remm = 0;
+    {
+        const double* cen = p.cen + (int64_t)g * D;  // L1-resident broadcast reads
+#pragma unroll
+        for (int k = 0; k < MAXRPT; ++k) {
+            m[k] = 0.0; a[k] = 0.0; th[k] = INFINITY; nx[k] = 0.f;
+            if (k < nr) {
+                const int li = tid + k * NT;
+                a[k] = p.attn[(int64_t)g * p.L + r0 + li];
+                // coverage init: distance to the centroid (synapse.cpp:244-249)
+                if (k == 0) {
+                    m[k] = __dsqrt_rn(exact_sq_d(reg4, cen));
+                    nx[k] = (float)norm2(reg4);
+                } else {
+                    m[k] = __dsqrt_rn(exact_sq_d<2>(far4(li - NT), cen));
+                    nx[k] = (float)norm2<2>(far4(li - NT));
+                }
+                remm |= 1u << k;
+            }
+        }
+    }
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        qn[0] = 0;
+        *hkey = 0ull;
+        *hrow = ~0ull;
+    }
+    __syncthreads();
+    cluster.sync();  // mbarriers visible cluster-wide before any remote push
+    const uint32_t tx1 = C * 32u, tx2 = C * (uint32_t)(sizeof(Hdr) + D * sizeof(float));
+    if (tid == 0) {
+        mbar_arrive_expect(&mbar[0], tx1);
+        mbar_arrive_expect(&mbar[1], tx2);
+    }
+
+    const double lam = p.lambda;
+    const double one_m_lam = __dsub_rn(1.0, lam);
+    int64_t* pick_rows = p.pick_rows + (int64_t)g * p.take;
+    double* pick_scores = p.pick_scores + (int64_t)g * p.take;
+    uint32_t ph1 = 0, ph2 = 0;
+    const float* bw = nullptr;  // winner coordinates of the previous round (in bc)
+    float nbw = 0.f;
+
+    for (round = 0; round < p.take; ++round) {
+        STAMP(0);
+        // ======== U: distance update against the previous pick ========
+        if (round > 0) {
+            const bool assign = (round == 1);  // the first pick REPLACES the centroid distances
+            int slot[MAXRPT];
+#pragma unroll
+            for (int k = 0; k < MAXRPT; ++k) {
+                slot[k] = -1;
+                if (k >= nr || !(remm >> k & 1u)) continue;
+                bool need;
+                if (assign || !p.filter) {
+                    need = true;
+                } else {
+                    const float dt = (k == 0) ? dot_f32x2(reg4, bw) : dot_f32x2<4>(far4(tid + k * NT - NT), bw);
+                    need = !(gram_lower_bound(nx[k], nbw, dt) > th[k]);
+                }
+                if (!need) continue;
+                const int sl = atomicAdd(qn, 1);
+                if (sl < QCAP) {
+                    slot[k] = sl;
+                    qown[sl] = tid;
+                    float* st = stage + sl * SPITCH;
+#pragma unroll
+                    for (int c4 = 0; c4 < D / 4; ++c4) {
+                        const float4 v = (k == 0) ? reg4(c4) : far4(tid + k * NT - NT)(c4);
+                        st[4 * c4] = v.x; st[4 * c4 + 1] = v.y; st[4 * c4 + 2] = v.z; st[4 * c4 + 3] = v.w;
+                    }
+                } else {  // queue full: evaluate in place
+                    const double d2 = (k == 0) ? exact_sq(reg4, bw) : exact_sq<2>(far4(tid + k * NT - NT), bw);
+                    const double d = __dsqrt_rn(d2);
+                    if (assign || d < m[k]) {
+                        m[k] = d;
+                        th[k] = __double2float_ru(d2);
+                    }
+                }
+            }
+            __syncthreads();
+            const int nq = min(qn[0], QCAP);
+            if (tid < nq) {
+                const float* st = stage + tid * SPITCH;
+                const double d2 = exact_sq<2>([&](int c4) {
+                    return make_float4(st[4 * c4], st[4 * c4 + 1], st[4 * c4 + 2], st[4 * c4 + 3]);
+                }, bw);
+                qres[2 * tid] = d2;
+                qres[2 * tid + 1] = __dsqrt_rn(d2);
+            }
+            __syncthreads();
+            if (tid == 0) qn[0] = 0;  // next use is after >= 2 more barriers
+#pragma unroll
+            for (int k = 0; k < MAXRPT; ++k) {
+                if (slot[k] < 0) continue;
+                const double d2 = qres[2 * slot[k]], d = qres[2 * slot[k] + 1];
+                if (assign || d < m[k]) {  // round 1 assigns; later rounds take std::min
+                    m[k] = d;
+                    th[k] = __double2float_ru(d2);
+                }
+            }
+        }
+        STAMP(1);
+
+        // ======== X1: cluster-wide min/max over remaining rows ========
+        double amin = INFINITY, amax = -INFINITY, cmin = INFINITY, cmax = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < MAXRPT; ++k) {
+            if (!(remm >> k & 1u)) continue;
+            amin = dmin_std(amin, a[k]);
+            amax = dmax_std(amax, a[k]);
+            cmin = dmin_std(cmin, m[k]);
+            cmax = dmax_std(cmax, m[k]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            amin = dmin_std(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+            amax = dmax_std(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            cmin = dmin_std(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+            cmax = dmax_std(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+        }
+        if (lane == 0) {
+            hw[wid] = amin; hw[NW + wid] = amax; hw[2 * NW + wid] = cmin; hw[3 * NW + wid] = cmax;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            double v0 = lane < NW ? hw[lane] : INFINITY;
+            double v1 = lane < NW ? hw[NW + lane] : -INFINITY;
+            double v2 = lane < NW ? hw[2 * NW + lane] : INFINITY;
+            double v3 = lane < NW ? hw[3 * NW + lane] : -INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                v0 = dmin_std(v0, __shfl_xor_sync(0xffffffffu, v0, o));
+                v1 = dmax_std(v1, __shfl_xor_sync(0xffffffffu, v1, o));
+                v2 = dmin_std(v2, __shfl_xor_sync(0xffffffffu, v2, o));
+                v3 = dmax_std(v3, __shfl_xor_sync(0xffffffffu, v3, o));
+            }
+            if (lane < (int)C) {
+                const uint32_t dst = mapa(smem_u32(mm + rank * 4), lane);
+                const uint32_t mb = mapa(smem_u32(&mbar[0]), lane);
+                st_async_v2(dst, __double_as_longlong(v0), __double_as_longlong(v1), mb);
+                st_async_v2(dst + 16, __double_as_longlong(v2), __double_as_longlong(v3), mb);
+            }
+        }
+        STAMP(2);
+        mbar_wait(&mbar[0], ph1);
+        ph1 ^= 1u;
+        if (tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[0], tx1);
+        {
+            double v0 = lane < (int)C ? mm[lane * 4 + 0] : INFINITY;
+            double v1 = lane < (int)C ? mm[lane * 4 + 1] : -INFINITY;
+            double v2 = lane < (int)C ? mm[lane * 4 + 2] : INFINITY;
+            double v3 = lane < (int)C ? mm[lane * 4 + 3] : -INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                v0 = dmin_std(v0, __shfl_xor_sync(0xffffffffu, v0, o));
+                v1 = dmax_std(v1, __shfl_xor_sync(0xffffffffu, v1, o));
+                v2 = dmin_std(v2, __shfl_xor_sync(0xffffffffu, v2, o));
+                v3 = dmax_std(v3, __shfl_xor_sync(0xffffffffu, v3, o));
+            }
+            amin = v0; amax = v1; cmin = v2; cmax = v3;
+        }
+        STAMP(3);
+
+        // ======== H: hybrid argmax (synapse.cpp:384-397) ========
+        const bool a_span = amax > amin, c_span = cmax > cmin;
+        const double ar = __dsub_rn(amax, amin), cr = __dsub_rn(cmax, cmin);
+        const double iar = a_span ? __drcp_rn(ar) : 0.0, icr = c_span ? __drcp_rn(cr) : 0.0;
+        double happ[MAXRPT];
+        double hmax = -1.0;
+#pragma unroll
+        for (int k = 0; k < MAXRPT; ++k) {
+            happ[k] = -1.0;
+            if (!(remm >> k & 1u)) continue;
+            const double na = __dmul_rn(__dsub_rn(a[k], amin), iar);
+            const double nc = __dmul_rn(__dsub_rn(m[k], cmin), icr);
+            happ[k] = __dadd_rn(__dmul_rn(lam, nc), __dmul_rn(one_m_lam, na));
+            hmax = dmax_std(hmax, happ[k]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hmax = dmax_std(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+        if (lane == 0) hw[wid] = hmax;  // hw (X1 partials) is dead: every warp passed the X1 wait
+        __syncthreads();
+        {
+            double v = lane < NW ? hw[lane] : -1.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = dmax_std(v, __shfl_xor_sync(0xffffffffu, v, o));
+            hmax = v;
+        }
+        // the reciprocal form is within ~1e-15 of the exact hybrid unless a range
+        // is so small that 1/range leaves the normal range: then rank exactly
+        const bool approx_ok = (!a_span || ar >= 1e-290) && (!c_span || cr >= 1e-290);
+        const double cut = approx_ok ? hmax - HYB_MARGIN : -INFINITY;
+        double hex[MAXRPT];
+#pragma unroll
+        for (int k = 0; k < MAXRPT; ++k) {
+            hex[k] = -1.0;
+            if (!(remm >> k & 1u) || happ[k] < cut) continue;
+            const double na = a_span ? __ddiv_rn(__dsub_rn(a[k], amin), ar) : 0.0;
+            const double nc = c_span ? __ddiv_rn(__dsub_rn(m[k], cmin), cr) : 0.0;
+            hex[k] = __dadd_rn(__dmul_rn(lam, nc), __dmul_rn(one_m_lam, na));
+            // hybrid >= 0 (both terms are), so the bit pattern orders like the value
+            atomicMax(hkey, (unsigned long long)__double_as_longlong(hex[k]));
+        }
+        __syncthreads();
+        const unsigned long long kbest = *hkey;
+#pragma unroll
+        for (int k = 0; k < MAXRPT; ++k)
+            if ((remm >> k & 1u) && hex[k] >= 0.0 && (unsigned long long)__double_as_longlong(hex[k]) == kbest)
+                atomicMin(hrow, (unsigned long long)(r0 + tid + k * NT));  // strict >: lowest row wins ties
+        __syncthreads();
+        const unsigned long long rbest = *hrow;
+        if (p.trace == (long long*)1 && round < 3 && tid < 64 && (remm & 1u))
+            printf("r%d tid%d a=%.17g m=%.17g happ=%.17g hex=%.17g | amin=%.17g amax=%.17g cmin=%.17g cmax=%.17g hmax=%.17g kbest=%llx rbest=%llx\n",
+                   round, tid, a[0], m[0], happ[0], hex[0], amin, amax, cmin, cmax, hmax, kbest, rbest);
+        if (rbest != ~0ull) {  // owner of the local winner publishes its coordinates
+            const int li = (int)((long long)rbest - r0);
+            if (li < NT) {
+                if (tid == li) {
+#pragma unroll
+                    for (int c4 = 0; c4 < D / 4; ++c4) reinterpret_cast<float4*>(cand)[c4] = reg4(c4);
+                    cand_hdr->nb = (double)nx[0];
+                }
+            } else if (tid == (li & (NT - 1))) {
+                const int k = li / NT;
+                auto get = far4(li - NT);
+#pragma unroll
+                for (int c4 = 0; c4 < D / 4; ++c4) reinterpret_cast<float4*>(cand)[c4] = get(c4);
+#pragma unroll
+                for (int kk = 1; kk < MAXRPT; ++kk)
+                    if (kk == k) cand_hdr->nb = (double)nx[kk];
+            }
+        } else if (tid < D) {
+            cand[tid] = 0.f;
+            if (tid == 0) cand_hdr->nb = 0.0;
+        }
+        __syncthreads();
+        STAMP(4);
+
+        // ======== X2: push (score, row, |b|^2, coordinates) to every CTA ========
+        if (tid < (int)C) {
+            const uint32_t dst = mapa(smem_u32(hdr + rank), tid);
+            const uint32_t mb = mapa(smem_u32(&mbar[1]), tid);
+            const double sc = rbest != ~0ull ? __longlong_as_double((long long)kbest) : -1.0;
+            const long long rw = rbest != ~0ull ? (long long)rbest : LLONG_MAX;
+            st_async_v2(dst, __double_as_longlong(sc), (uint64_t)rw, mb);
+            st_async_v2(dst + 16, __double_as_longlong(cand_hdr->nb), 0ull, mb);
+        }
+        if (tid >= 32 && tid < 32 + (int)C * (D / 4)) {
+            const int e = tid - 32, dst_rank = e / (D / 4), c4 = e % (D / 4);
+            const uint32_t dst = mapa(smem_u32(bc + rank * D + 4 * c4), dst_rank);
+            st_async_v4(dst, reinterpret_cast<const float4*>(cand)[c4], mapa(smem_u32(&mbar[1]), dst_rank));
+        }
+        if (tid == 0) {  // reset the argmax atomics (next use is after >= 2 more barriers)
+            *hkey = 0ull;
+            *hrow = ~0ull;
+        }
+        mbar_wait(&mbar[1], ph2);
+        ph2 ^= 1u;
+        if (tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[1], tx2);
+        // winner across the cluster (every warp, same order -> same answer)
+        double bs = lane < (int)C ? hdr[lane].score : -1.0;
+        long long br = lane < (int)C ? hdr[lane].row : LLONG_MAX;
+        int w = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+            const long long orow = __shfl_xor_sync(0xffffffffu, br, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, w, o);
+            if (os > bs || (os == bs && orow < br)) { bs = os; br = orow; w = ow; }
+        }
+        bw = bc + w * D;
+        nbw = (float)hdr[w].nb;
+        if (br >= r0 && br < r0 + nrows) {
+            const int li = (int)(br - r0);
+            if (tid == (li & (NT - 1))) remm &= ~(1u << (li / NT));
+        }
+        if (tid == 0 && rank == 0) {
+            pick_rows[round] = br;
+            pick_scores[round] = bs;
+        }
+        STAMP(5);
+    }
+
+    // ---- sort the picks ascending by row (synapse.cpp:413-414) ----
+    __syncthreads();
+    if (rank == 0) {
+        int64_t* out_rows = p.out_rows + (int64_t)g * p.take;
+        double* out_scores = p.out_scores + (int64_t)g * p.take;
+        for (int s = tid; s < p.take; s += NT) {
+            const int64_t r = pick_rows[s];
+            int pos = 0;
+            for (int t = 0; t < p.take; ++t) pos += pick_rows[t] < r;
+            out_rows[pos] = r;
+            out_scores[pos] = pick_scores[s];
+        }
+    }
+    cluster.sync();  // no CTA exits while a peer may still push into it
+}
+
+}  // namespace
+
+// Host side: choose the cluster size and residency, launch.  Returns false
+// when the dim-64 kernel does not apply (caller uses the generic kernel).
+bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
+                     unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
+                     cudaStream_t s) {
+    if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 ||
+        (reinterpret_cast<uintptr_t>(g.X) & 15) != 0 || g.L < 1)
+        return false;
+    static int max_optin = -1;
+    if (max_optin < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+            max_optin = 232448;
+    }
+    const size_t budget = (size_t)max_optin - 2048;
+    // smallest cluster whose slice fits on chip (512 register rows + shared rows)
+    int C = 0, S = 0, Rs = 0;
+    bool smem_rows = true;
+    for (int c = 1; c <= MAXC; c *= 2) {
+        const int s_ = (int)((g.L + c - 1) / c);
+        const int rs = std::max(0, s_ - NT);
+        if (s_ <= MAXRPT_ALL * NT && sel64_layout(rs, true).total <= budget) {
+            C = c; S = s_; Rs = rs;
+            break;
+        }
+    }
+    if (C == 0) {  // too large for one cluster on chip: rows beyond 512 stay in L2
+        C = MAXC;
+        S = (int)((g.L + C - 1) / C);
+        Rs = std::max(0, S - NT);
+        smem_rows = false;
+        if (S > MAXRPT_ALL * NT) return false;
+    }
+    Sel64Params prm;
+    prm.X = g.X;
+    prm.gstride = g.gstride;
+    prm.rstride = g.rstride;
+    prm.L = g.L;
+    prm.attn = attn;
+    prm.cen = cen;
+    prm.take = take;
+    prm.lambda = lambda;
+    prm.S = S;
+    prm.Rs = Rs;
+    prm.filter = (flags & CX_SELECT_EXACT_ONLY) ? 0 : 1;
+    prm.pick_rows = pick_rows;
+    prm.pick_scores = pick_scores;
+    prm.out_rows = rows;
+    prm.out_scores = scores;
+    prm.trace = nullptr;
+    const char* tr = getenv("CX_SEL_TRACE");
+    if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 8 * 4096));
+    if (tr && tr[0] == 'p') prm.trace = (long long*)1;
+    const size_t smem = sel64_layout(Rs, smem_rows).total;
+    const int rpt = (S + NT - 1) / NT;
+    void (*kern)(Sel64Params) = nullptr;
+    if (smem_rows) kern = rpt <= 1 ? select64_kernel<1, true> : rpt <= 2 ? select64_kernel<2, true> : select64_kernel<4, true>;
+    else kern = rpt <= 1 ? select64_kernel<1, false> : rpt <= 2 ? select64_kernel<2, false> : select64_kernel<4, false>;
+    CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (C > 8) CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)C, (unsigned)g.G, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CX_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+    count_launch();
+    const char* dump = getenv("CX_SEL_DUMP");
+    if (dump && dump[0] == '1') {  // debugging aid: picks in selection order (group 0)
+        CX_CUDA(cudaStreamSynchronize(s));
+        std::vector<int64_t> pr(take);
+        std::vector<double> ps(take);
+        CX_CUDA(cudaMemcpy(pr.data(), pick_rows, sizeof(int64_t) * take, cudaMemcpyDeviceToHost));
+        CX_CUDA(cudaMemcpy(ps.data(), pick_scores, sizeof(double) * take, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < std::min(take, 12); ++i) fprintf(stderr, "pick %d: row %lld score %.17g\n", i, (long long)pr[i], ps[i]);
+    }
+    if (prm.trace && prm.trace != (long long*)1) {  // debugging aid: average cycles per phase over rounds 2..take-2
+        CX_CUDA(cudaStreamSynchronize(s));
+        double acc[6] = {0};
+        int n = 0;
+        for (int r = 2; r < std::min(take, 4096) - 1; ++r, ++n) {
+            const long long* t = prm.trace + r * 8;
+            for (int k = 0; k < 5; ++k) acc[k] += (double)(t[k + 1] - t[k]);
+            acc[5] += (double)(prm.trace[(r + 1) * 8] - t[0]);
+        }
+        if (n > 0)
+            fprintf(stderr, "select64 C=%d S=%d Rs=%d smem_rows=%d cycles/round: U=%.0f X1send=%.0f X1wait=%.0f "
+                            "H=%.0f X2=%.0f total=%.0f\n",
+                    C, S, Rs, (int)smem_rows, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
+        cudaFree(prm.trace);
+    }
+    return true;
+}
+
+}  // namespace cx

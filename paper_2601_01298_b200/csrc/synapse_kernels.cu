@@ -49,6 +49,47 @@ __global__ void attn_scores_kernel(GroupView gv, double inv_sqrt_dk, double* __r
     }
 }
 
+// dim-64 fast path for the same scores (GQA groups, or a single pass): the row
+// is loaded once into registers (16 x float4) and all passes are accumulated
+// in one sweep over the coordinates -- P independent fp64 chains per thread,
+// each still summed in the reference's coordinate order.
+constexpr int kAttnMaxP = 8;
+__global__ void __launch_bounds__(256) attn64_scores_kernel(GroupView gv, double inv_sqrt_dk,
+                                                          double* __restrict__ scores, int* flag) {
+    __shared__ double qs[kAttnMaxP][64];
+    const int g = blockIdx.y;
+    for (int e = threadIdx.x; e < gv.P * 64; e += blockDim.x)
+        qs[e / 64][e % 64] = (double)__ldg(gv.Q + (int64_t)g * gv.P * 64 + e);
+    __syncthreads();
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= gv.L) return;
+    const float4* row = reinterpret_cast<const float4*>(gv.X + g * gv.gstride + i * gv.rstride);
+    float x[64];
+#pragma unroll
+    for (int c4 = 0; c4 < 16; ++c4) {
+        const float4 v = __ldg(row + c4);
+        x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
+    }
+    double acc[kAttnMaxP];
+#pragma unroll
+    for (int p = 0; p < kAttnMaxP; ++p) acc[p] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 64; ++c) {
+        const double xc = (double)x[c];
+#pragma unroll
+        for (int p = 0; p < kAttnMaxP; ++p)
+            if (p < gv.P) acc[p] = __dadd_rn(acc[p], __dmul_rn(qs[p][c], xc));
+    }
+#pragma unroll
+    for (int p = 0; p < kAttnMaxP; ++p) {
+        if (p < gv.P) {
+            const double s = __dmul_rn(acc[p], inv_sqrt_dk);
+            if (!isfinite(s)) atomicOr(flag, FLAG_NONFINITE);
+            scores[((int64_t)g * gv.P + p) * gv.L + i] = s;
+        }
+    }
+}
+
 template <class T, class Op>
 __device__ __forceinline__ T warp_reduce(T v, Op op) {
 #pragma unroll
@@ -549,8 +590,15 @@ void attention_grouped(cx_ctx* ctx, const GroupView& g, double* out, cudaStream_
     double* sums = ctx->arena.take<double>((size_t)g.G * g.P);
     const double inv = 1.0 / std::sqrt((double)g.d_k);
     dim3 grid((unsigned)((g.L + 255) / 256), (unsigned)g.G);
-    attn_scores_kernel<<<grid, 256, 0, s>>>(g, inv, scores, ctx->d_flag);
-    check_launch("attn_scores_kernel");
+    const bool fast = g.dim == 64 && g.d_k == 64 && g.P <= kAttnMaxP && (g.col_step == 0 || g.P == 1) &&
+                      (g.rstride & 3) == 0 && (g.gstride & 3) == 0 && (reinterpret_cast<uintptr_t>(g.X) & 15) == 0;
+    if (fast) {
+        attn64_scores_kernel<<<grid, 256, 0, s>>>(g, inv, scores, ctx->d_flag);
+        check_launch("attn64_scores_kernel");
+    } else {
+        attn_scores_kernel<<<grid, 256, 0, s>>>(g, inv, scores, ctx->d_flag);
+        check_launch("attn_scores_kernel");
+    }
     attn_softmax_kernel<<<g.G * g.P, 1024, 0, s>>>(g.L, g.P, scores, sums);
     check_launch("attn_softmax_kernel");
     attn_total_kernel<<<grid, 256, 0, s>>>(g.L, g.P, scores, sums, out);
@@ -609,6 +657,10 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     if (g.dim > 1024) fail(CX_DEVICE_ERROR, "select: dim > 1024 unsupported");
     centroid_kernel<<<g.G, ((g.dim + 31) / 32) * 32, 0, s>>>(g, cen);
     check_launch("centroid_kernel");
+
+    if (!(flags & CX_SELECT_GENERIC) &&
+        select64_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, s))
+        return;
 
     SelectPlan pl = plan_select_shape(g);
     SelectParams prm;

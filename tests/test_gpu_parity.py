@@ -106,7 +106,7 @@ def test_golden_small_cases(cx, orc):
 
 
 @pytest.mark.parametrize("name", ["cfg1_points.npz", "cfg2_group.npz", "cfg4_group.npz"])
-@pytest.mark.parametrize("flags", [0, 1], ids=["filter", "exact_only"])
+@pytest.mark.parametrize("flags", [0, 1, 2], ids=["filter", "exact_only", "generic"])
 def test_golden_group_selection(dev, orc, name, flags):
     import torch
     g = np.load(os.path.join(GOLDEN, name))
