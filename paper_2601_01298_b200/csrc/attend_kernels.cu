@@ -214,6 +214,222 @@ __global__ void __launch_bounds__(256) decode_step_kernel(cx_decode_batch b, int
     }
 }
 
+// ---- decode v2: warp per agent, register-tiled (d_k = 64, <= 8 q-heads / KV head) ----
+// CTA = one (layer, KV head) and a contiguous agent range; the synapse K (rows
+// padded to 68 floats: conflict-free per-lane row reads) and V are staged once
+// and reused by every agent of the range.  Each warp owns one agent at a time:
+//   scores  lane j holds keys j, j+32, ... for all q-heads of the group
+//           (QPG x 6 accumulators; q broadcast from shared memory, K rows as float4);
+//           private rows are read straight from global memory (lane per row);
+//   softmax per q-head with warp shuffles, unnormalised weights to shared memory;
+//   mix     lane owns output dims (2 lane, 2 lane + 1): synapse V from shared
+//           memory, private V rows coalesced from global memory.
+// The new token's K/V is appended to the private rows first (fused).
+constexpr int DV2_DK = 64;
+constexpr int DV2_MAXQ = 8;
+constexpr int DV2_KPL = 6;       // synapse keys per lane (k_syn <= 192)
+constexpr int DV2_KPITCH = 68;
+constexpr int DV2_WARPS = 16;
+
+struct DecodeV2Smem {
+    size_t ks, vs, qs, ps, total;
+    int pstride;
+};
+
+__host__ __device__ inline DecodeV2Smem decode_v2_layout(int k_syn, int t_cap) {
+    DecodeV2Smem L;
+    L.pstride = ((k_syn + t_cap + 3) / 4) * 4;
+    size_t o = 0;
+    L.ks = o; o = al16(o + sizeof(float) * (size_t)k_syn * DV2_KPITCH);
+    L.vs = o; o = al16(o + sizeof(float) * (size_t)k_syn * DV2_DK);
+    L.qs = o; o = al16(o + sizeof(float) * (size_t)DV2_WARPS * DV2_MAXQ * DV2_DK);
+    L.ps = o; o = al16(o + sizeof(float) * (size_t)DV2_WARPS * DV2_MAXQ * L.pstride);
+    L.total = o;
+    return L;
+}
+
+template <int QPG>
+__global__ void __launch_bounds__(DV2_WARPS * 32, 1) decode_v2_kernel(cx_decode_batch b, int agents_per_cta,
+                                                                    float scale) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const DecodeV2Smem lay = decode_v2_layout(b.k_syn, b.t_cap);
+    float* Ks = reinterpret_cast<float*>(smem + lay.ks);
+    float* Vs = reinterpret_cast<float*>(smem + lay.vs);
+    const int lh = blockIdx.x;
+    const int l = lh / b.n_kv, g = lh % b.n_kv;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ks = b.k_syn;
+    float* Qw = reinterpret_cast<float*>(smem + lay.qs) + warp * DV2_MAXQ * DV2_DK;
+    float* Pw = reinterpret_cast<float*>(smem + lay.ps) + warp * DV2_MAXQ * lay.pstride;
+
+    // stage the synapse rows of this (layer, KV head)
+    const float4* sk4 = reinterpret_cast<const float4*>(b.syn_keys + (size_t)lh * ks * DV2_DK);
+    const float4* sv4 = reinterpret_cast<const float4*>(b.syn_values + (size_t)lh * ks * DV2_DK);
+    for (int e = tid; e < ks * (DV2_DK / 4); e += blockDim.x) {
+        const int j = e / (DV2_DK / 4), c4 = e % (DV2_DK / 4);
+        reinterpret_cast<float4*>(Ks + j * DV2_KPITCH)[c4] = __ldg(sk4 + e);
+        reinterpret_cast<float4*>(Vs)[e] = __ldg(sv4 + e);
+    }
+    __syncthreads();
+
+    const int a_begin = blockIdx.y * agents_per_cta;
+    const int a_end = min(b.n_agents, a_begin + agents_per_cta);
+    const bool app = b.new_keys != nullptr;
+    for (int a = a_begin + warp; a < a_end; a += DV2_WARPS) {
+        const int len = min(b.tail_len[a], b.t_cap - (app ? 1 : 0));
+        const int nt = len + (app ? 1 : 0);
+        const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * DV2_DK;
+        const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * DV2_DK;
+        const size_t qoff = (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG) * DV2_DK;
+        const float* tk = b.tail_keys + toff;
+        const float* tv = b.tail_values + toff;
+        // q-heads of this group -> shared (coalesced), append the new row (fused)
+        for (int e = lane; e < QPG * DV2_DK / 4; e += 32)
+            reinterpret_cast<float4*>(Qw)[e] = __ldg(reinterpret_cast<const float4*>(b.q + qoff) + e);
+        if (app && lane < 16) {
+            reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * DV2_DK)[lane] =
+                __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + lane);
+            reinterpret_cast<float4*>(b.tail_values + toff + (size_t)len * DV2_DK)[lane] =
+                __ldg(reinterpret_cast<const float4*>(b.new_values + noff) + lane);
+        }
+        __syncwarp();
+        // ---- scores: synapse keys lane + 32 i, private row lane (+32) ----
+        float acc[DV2_KPL][QPG];
+        float acct[2][QPG];
+#pragma unroll
+        for (int i = 0; i < DV2_KPL; ++i)
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) acc[i][h] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) acct[i][h] = 0.f;
+        const float* trow0 = (app && lane == len) ? b.new_keys + noff : tk + (size_t)lane * DV2_DK;
+        const float* trow1 = (app && lane + 32 == len) ? b.new_keys + noff : tk + (size_t)(lane + 32) * DV2_DK;
+#pragma unroll 2
+        for (int c4 = 0; c4 < DV2_DK / 4; ++c4) {
+            float4 qv[QPG];
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) qv[h] = reinterpret_cast<const float4*>(Qw + h * DV2_DK)[c4];
+#pragma unroll
+            for (int i = 0; i < DV2_KPL; ++i) {
+                const int j = lane + 32 * i;
+                if (j < ks) {
+                    const float4 kv = reinterpret_cast<const float4*>(Ks + j * DV2_KPITCH)[c4];
+#pragma unroll
+                    for (int h = 0; h < QPG; ++h) {
+                        acc[i][h] = fmaf(qv[h].x, kv.x, acc[i][h]);
+                        acc[i][h] = fmaf(qv[h].y, kv.y, acc[i][h]);
+                        acc[i][h] = fmaf(qv[h].z, kv.z, acc[i][h]);
+                        acc[i][h] = fmaf(qv[h].w, kv.w, acc[i][h]);
+                    }
+                }
+            }
+            if (lane < nt) {
+                const float4 kv = __ldg(reinterpret_cast<const float4*>(trow0) + c4);
+#pragma unroll
+                for (int h = 0; h < QPG; ++h) {
+                    acct[0][h] = fmaf(qv[h].x, kv.x, acct[0][h]);
+                    acct[0][h] = fmaf(qv[h].y, kv.y, acct[0][h]);
+                    acct[0][h] = fmaf(qv[h].z, kv.z, acct[0][h]);
+                    acct[0][h] = fmaf(qv[h].w, kv.w, acct[0][h]);
+                }
+            }
+            if (lane + 32 < nt) {
+                const float4 kv = __ldg(reinterpret_cast<const float4*>(trow1) + c4);
+#pragma unroll
+                for (int h = 0; h < QPG; ++h) {
+                    acct[1][h] = fmaf(qv[h].x, kv.x, acct[1][h]);
+                    acct[1][h] = fmaf(qv[h].y, kv.y, acct[1][h]);
+                    acct[1][h] = fmaf(qv[h].z, kv.z, acct[1][h]);
+                    acct[1][h] = fmaf(qv[h].w, kv.w, acct[1][h]);
+                }
+            }
+        }
+        // ---- softmax per q-head (max, exp, sum over k_syn + nt keys) ----
+        float inv[QPG];
+#pragma unroll
+        for (int h = 0; h < QPG; ++h) {
+            float m = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < DV2_KPL; ++i)
+                if (lane + 32 * i < ks) m = fmaxf(m, acc[i][h] * scale);
+            if (lane < nt) m = fmaxf(m, acct[0][h] * scale);
+            if (lane + 32 < nt) m = fmaxf(m, acct[1][h] * scale);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            float s = 0.f;
+            float* ph = Pw + h * lay.pstride;
+#pragma unroll
+            for (int i = 0; i < DV2_KPL; ++i) {
+                const int j = lane + 32 * i;
+                if (j < ks) {
+                    const float e = __expf(acc[i][h] * scale - m);
+                    ph[j] = e;
+                    s += e;
+                }
+            }
+            if (lane < nt) {
+                const float e = __expf(acct[0][h] * scale - m);
+                ph[ks + lane] = e;
+                s += e;
+            }
+            if (lane + 32 < nt) {
+                const float e = __expf(acct[1][h] * scale - m);
+                ph[ks + lane + 32] = e;
+                s += e;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            inv[h] = 1.0f / s;
+        }
+        __syncwarp();
+        // ---- mix: lane owns dims 2 lane, 2 lane + 1 ----
+        float2 o[QPG];
+#pragma unroll
+        for (int h = 0; h < QPG; ++h) o[h] = make_float2(0.f, 0.f);
+        int j = 0;
+        for (; j + 4 <= ks; j += 4) {
+            float4 p4[QPG];
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) p4[h] = reinterpret_cast<const float4*>(Pw + h * lay.pstride + j)[0];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 v = reinterpret_cast<const float2*>(Vs + (j + u) * DV2_DK)[lane];
+#pragma unroll
+                for (int h = 0; h < QPG; ++h) {
+                    const float pw = u == 0 ? p4[h].x : u == 1 ? p4[h].y : u == 2 ? p4[h].z : p4[h].w;
+                    o[h].x = fmaf(pw, v.x, o[h].x);
+                    o[h].y = fmaf(pw, v.y, o[h].y);
+                }
+            }
+        }
+        for (; j < ks; ++j) {
+            const float2 v = reinterpret_cast<const float2*>(Vs + j * DV2_DK)[lane];
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) {
+                const float pw = Pw[h * lay.pstride + j];
+                o[h].x = fmaf(pw, v.x, o[h].x);
+                o[h].y = fmaf(pw, v.y, o[h].y);
+            }
+        }
+        for (int t = 0; t < nt; ++t) {
+            const float* vrow = (app && t == len) ? b.new_values + noff : tv + (size_t)t * DV2_DK;
+            const float2 v = __ldg(reinterpret_cast<const float2*>(vrow) + lane);
+#pragma unroll
+            for (int h = 0; h < QPG; ++h) {
+                const float pw = Pw[h * lay.pstride + ks + t];
+                o[h].x = fmaf(pw, v.x, o[h].x);
+                o[h].y = fmaf(pw, v.y, o[h].y);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < QPG; ++h)
+            reinterpret_cast<float2*>(b.out + qoff + (size_t)h * DV2_DK)[lane] = make_float2(o[h].x * inv[h], o[h].y * inv[h]);
+        __syncwarp();  // Qw / Pw reuse by the next agent of this warp
+    }
+}
+
 // ---- KV append: [n_layers][T][d_model] block into [n_layers][cap][d_model] --
 __global__ void kv_append_kernel(float* __restrict__ ck, float* __restrict__ cv, int64_t cap, int dm,
                                  const float* __restrict__ bk, const float* __restrict__ bv, int64_t T,
@@ -246,8 +462,43 @@ void attend_fp64_ws(const float* q, const float* k, const float* v, int64_t n, i
     check_launch("attend_fp64_kernel");
 }
 
+template <int QPG>
+static bool launch_decode_v2(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
+    const DecodeV2Smem lay = decode_v2_layout(b.k_syn, b.t_cap);
+    static int max_optin = -1;
+    if (max_optin < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    }
+    if (lay.total > (size_t)max_optin) return false;
+    const int n_lh = b.n_layers * b.n_kv;
+    const int sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
+    int chunks = std::max(1, sms / n_lh);  // ~one CTA per SM; each stages its synapse once
+    chunks = std::min(chunks, (b.n_agents + DV2_WARPS - 1) / DV2_WARPS);
+    chunks = std::max(chunks, 1);
+    const int per = (b.n_agents + chunks - 1) / chunks;
+    CX_CUDA(cudaFuncSetAttribute(decode_v2_kernel<QPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    decode_v2_kernel<QPG><<<dim3((unsigned)n_lh, (unsigned)chunks), DV2_WARPS * 32, lay.total, s>>>(
+        b, per, (float)(1.0 / std::sqrt((double)b.d_k)));
+    check_launch("decode_v2_kernel");
+    return true;
+}
+
 void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int qpg = b.n_q / b.n_kv;
+    if (b.d_k == DV2_DK && b.k_syn <= 32 * DV2_KPL && b.t_cap <= 64) {
+        bool done = false;
+        switch (qpg) {
+            case 1: done = launch_decode_v2<1>(ctx, b, s); break;
+            case 2: done = launch_decode_v2<2>(ctx, b, s); break;
+            case 4: done = launch_decode_v2<4>(ctx, b, s); break;
+            case 7: done = launch_decode_v2<7>(ctx, b, s); break;
+            case 8: done = launch_decode_v2<8>(ctx, b, s); break;
+            default: break;
+        }
+        if (done) return;
+    }
     int apb = std::max(1, 8 / qpg);
     const int warps = apb * qpg;
     const int t_rows = b.t_cap + 1;

@@ -61,7 +61,7 @@ __global__ void tput_ffma(float* out, float x, int n) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
 }
 
-int main() {
+int main1() {
     double* dd; float* df; long long* cyc;
     cudaMalloc(&dd, 1 << 26); cudaMalloc(&df, 1 << 26); cudaMallocManaged(&cyc, 8);
     const int n = 4096;
@@ -92,3 +92,55 @@ int main() {
     printf("FFMA throughput %.1f Gop/s = %.1f /clk/SM\n", ops / ms / 1e6, ops / (ms * 1e-3) / sms / (clk * 1e3));
     return 0;
 }
+
+// ---- exact squared-distance chain microbench (appended) ----
+__global__ void chain_sq(const float* __restrict__ xin, const float* __restrict__ bin, double* out, int reps,
+                         long long* cyc) {
+    __shared__ float xs[64 * 65];
+    __shared__ float bs[64];
+    for (int i = threadIdx.x; i < 64 * 65; i += blockDim.x) xs[i] = xin[i % 256];
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) bs[i] = bin[i];
+    __syncthreads();
+    const float* row = xs + threadIdx.x * 65;
+    double acc = 0.0;
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+            const double d = __dsub_rn((double)row[c], (double)bs[c]);
+            acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = acc;
+    if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+__global__ void tput_f2f(double* out, float x, int n) {
+    float a0 = x, a1 = x + 1, a2 = x + 2, a3 = x + 3;
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int i = 0; i < n; ++i) {
+        s0 = (double)a0; s1 = (double)a1; s2 = (double)a2; s3 = (double)a3;
+        a0 = __uint_as_float(__double2hiint(s0) ^ 1); a1 = __uint_as_float(__double2hiint(s1) ^ 1);
+        a2 = __uint_as_float(__double2hiint(s2) ^ 1); a3 = __uint_as_float(__double2hiint(s3) ^ 1);
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s0 + s1 + s2 + s3;
+}
+int main2() {
+    float *x, *b; double* o; long long* cyc;
+    cudaMalloc(&x, 4096); cudaMalloc(&b, 4096); cudaMalloc(&o, 1 << 20); cudaMallocManaged(&cyc, 8);
+    cudaMemset(x, 0, 4096); cudaMemset(b, 0, 4096);
+    for (int th : {1, 32, 64}) {
+        chain_sq<<<1, th>>>(x, b, o, 1, cyc); cudaDeviceSynchronize();
+        chain_sq<<<1, th>>>(x, b, o, 16, cyc); cudaDeviceSynchronize();
+        printf("exact_sq chain, %d threads: %.1f cycles per 64-term sum\n", th, (double)*cyc / 16);
+    }
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1); float ms;
+    tput_f2f<<<sms * 8, 256>>>(o, 1.0f, 16); cudaDeviceSynchronize();
+    cudaEventRecord(e0); tput_f2f<<<sms * 8, 256>>>(o, 1.0f, 4096); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    double ops = (double)sms * 8 * 256 * 4096 * 4;
+    printf("F2F.F64.F32 (+int ops) throughput %.1f /clk/SM\n", ops / (ms * 1e-3) / sms / 1.965e9);
+    return 0;
+}
+int main() { main1(); return main2(); }
