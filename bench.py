@@ -243,32 +243,39 @@ def run_b200(args):
         full_compress()
     torch.cuda.synchronize()
 
-    # ---- timed: compression with inputs resident in HBM, L2 flushed between steps
+    # ---- timed: compression with inputs resident in HBM, L2 flushed between steps.
+    # One step = ONE C-ABI call (cx_compress_grouped_dev: centroid || attention,
+    # greedy selection, landmark K/V gather) + the synapse all-gather when N > 1.
     launches0 = cxd.kernel_launch_count()
-    times, sel_times = [], []
+    times = []
     with ClockSampler(local) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         for _ in range(args.steps):
             flush.zero_()
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            e[0].record(stream)
-            a = cxd.attention_grouped(keys, queries)
-            e[1].record(stream)
-            r, s = cxd.select_grouped(keys, a, K, LAM)
-            e[2].record(stream)
-            # landmark K/V gather (A5) through the grouped C-ABI on the chosen rows
-            cxd.gather_rows(keys, r, sk)
-            cxd.gather_rows(values, r, sv)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            full_compress()
             if world > 1:
-                all_gather_groups([r, s, sk, sv], G)
-            e[3].record(stream)
+                all_gather_groups([rows, scores, sk, sv], G)
+            e1.record(stream)
             torch.cuda.synchronize()
-            times.append(e[0].elapsed_time(e[3]))
-            sel_times.append(e[1].elapsed_time(e[2]))
+            times.append(e0.elapsed_time(e1))
         torch.cuda.synchronize()
     launches = cxd.kernel_launch_count() - launches0
+    # the dominant kernel (greedy selection, incl. its centroid prologue) timed
+    # alone with events on its stream, same inputs, L2 flushed
+    sel_times = []
+    a = cxd.attention_grouped(keys, queries)
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        cxd.select_grouped(keys, a, K, LAM)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sel_times.append(e0.elapsed_time(e1))
     ms = statistics.mean(times)
     sel_ms = statistics.mean(sel_times)
     if world > 1:

@@ -35,6 +35,9 @@ void ctx_init(cx_ctx* c, int device) {
     int lo = 0, hi = 0;
     CX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CX_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CX_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CX_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CX_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
     CX_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
 }
@@ -147,8 +150,12 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
     return guard([&] {
         if (!c) return;
         cudaStreamSynchronize(c->stream);
+        cudaStreamSynchronize(c->side);
         if (c->arena.base) cudaFree(c->arena.base);
         if (c->d_flag) cudaFree(c->d_flag);
+        cudaEventDestroy(c->ev_fork);
+        cudaEventDestroy(c->ev_join);
+        cudaStreamDestroy(c->side);
         cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -467,16 +474,25 @@ extern "C" cx_status cx_compress_grouped_dev(cx_ctx* c, const cx_groups* gr, con
         const int take = (int)std::min<int64_t>(k, g.L);
         ArenaPlan pl;
         pl.take<double>((size_t)g.G * g.L);
+        pl.take<double>((size_t)g.G * g.dim);
         plan_attention(pl, g);
         plan_select(pl, g, k);
         c->arena.reserve(pl.used);
         c->arena.reset();
         cudaStream_t s = (cudaStream_t)stream;
         double* attn = c->arena.take<double>((size_t)g.G * g.L);
+        double* cen = c->arena.take<double>((size_t)g.G * g.dim);
+        // fork: the centroids (A2, a latency-bound serial sum per coordinate)
+        // run on the side stream while the attention mass (A3) runs on `s`
+        CX_CUDA(cudaEventRecord(c->ev_fork, s));
+        CX_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        centroid_launch(g, cen, c->side);
+        CX_CUDA(cudaEventRecord(c->ev_join, c->side));
         const size_t mark = c->arena.used;
         attention_grouped(c, g, attn, s);
         c->arena.used = mark;  // attention scratch is dead once `attn` is written (stream-ordered)
-        select_grouped(c, g, attn, k, lambda, flags, out_rows, out_scores, s);
+        CX_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+        select_grouped(c, g, attn, k, lambda, flags, out_rows, out_scores, s, cen);
         if (syn_keys) gather_rows(g, g.X, out_rows, take, syn_keys, s);
         if (syn_values && values) gather_rows(g, values, out_rows, take, syn_values, s);
     });

@@ -98,6 +98,8 @@ struct ArenaPlan {
 struct cx_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;  // used by the host-pointer (reference-shaped) calls
+    cudaStream_t side = nullptr;    // fork target (centroid alongside attention)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cx::Arena arena;                // device scratch
     int* d_flag = nullptr;          // device-side error flag (softmax non-finite, ...)
     int num_sms = 0;
@@ -130,7 +132,10 @@ void plan_attention(ArenaPlan& p, const GroupView& g);
 
 // greedy selection for all groups.  rows/scores out [G][take] ascending.
 void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
-                    unsigned flags, int64_t* rows, double* scores, cudaStream_t s);
+                    unsigned flags, int64_t* rows, double* scores, cudaStream_t s,
+                    const double* centroids = nullptr /* [G][dim], computed here when null */);
+// centroid_of for every group (synapse.cpp:173-181), bit-exact sequential sums
+void centroid_launch(const GroupView& g, double* cen, cudaStream_t s);
 void plan_select(ArenaPlan& p, const GroupView& g, int k);
 // dim-64 fast path (select64.cu); false when it does not apply
 bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,

@@ -167,6 +167,82 @@ __global__ void centroid_kernel(GroupView gv, double* __restrict__ cen) {
     cen[(int64_t)g * gv.dim + j] = __ddiv_rn(c, (double)gv.L);
 }
 
+// Same sum with the loads off the critical path: one warp per 32 coordinates
+// of one group; rows stream through an 8-stage cp.async ring (32 rows x 128 B
+// per stage) so the only serial cost is the fp64 add chain (L x 8.4 cycles).
+constexpr int kCpStages = 8;
+constexpr int kCpRows = 32;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__global__ void __launch_bounds__(32) centroid_pipe_kernel(GroupView gv, double* __restrict__ cen) {
+    __shared__ __align__(16) float ring[kCpStages][kCpRows][32];
+    const int g = blockIdx.y;
+    const int c0 = blockIdx.x * 32;
+    const int lane = threadIdx.x;
+    const float* base = gv.X + g * gv.gstride + c0;
+    const int64_t nst = (gv.L + kCpRows - 1) / kCpRows;
+    auto issue = [&](int64_t st) {
+        if (st < nst) {
+            const int64_t r0 = st * kCpRows;
+            const int rows = (int)min((int64_t)kCpRows, gv.L - r0);
+            float(*buf)[32] = ring[st % kCpStages];
+            for (int e = lane; e < rows * 8; e += 32) {  // 8 x 16 B per row
+                const int r = e >> 3, q = e & 7;
+                cp_async16(&buf[r][q * 4], base + (r0 + r) * gv.rstride + q * 4);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int st = 0; st < kCpStages - 1; ++st) issue(st);
+    double acc = 0.0;
+    for (int64_t st = 0; st < nst; ++st) {
+        issue(st + kCpStages - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kCpStages - 1) : "memory");
+        __syncwarp();
+        const float(*buf)[32] = ring[st % kCpStages];
+        const int rows = (int)min((int64_t)kCpRows, gv.L - st * kCpRows);
+        if (c0 + lane < gv.dim) {
+#pragma unroll 8
+            for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, (double)buf[r][lane]);
+        }
+        __syncwarp();
+    }
+    if (c0 + lane < gv.dim) cen[(int64_t)g * gv.dim + c0 + lane] = __ddiv_rn(acc, (double)gv.L);
+}
+
+constexpr int kCenRows = 64;
+__global__ void __launch_bounds__(256) centroid_staged_kernel(GroupView gv, double* __restrict__ cen) {
+    extern __shared__ __align__(16) float cbuf[];  // [2][kCenRows][dim]
+    const int g = blockIdx.x;
+    const int dim = gv.dim;
+    const float* base = gv.X + g * gv.gstride;
+    const int64_t nchunks = (gv.L + kCenRows - 1) / kCenRows;
+    auto load = [&](int64_t ch, float* dst) {
+        const int64_t r0 = ch * kCenRows;
+        const int rows = (int)min((int64_t)kCenRows, gv.L - r0);
+        for (int e = threadIdx.x; e < rows * dim; e += blockDim.x) {
+            const int r = e / dim, c = e % dim;
+            dst[r * dim + c] = __ldg(base + (r0 + r) * gv.rstride + c);
+        }
+    };
+    double acc = 0.0;
+    load(0, cbuf);
+    __syncthreads();
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        float* cur = cbuf + (ch & 1) * kCenRows * dim;
+        if (ch + 1 < nchunks) load(ch + 1, cbuf + ((ch + 1) & 1) * kCenRows * dim);
+        if (threadIdx.x < dim) {
+            const int rows = (int)min((int64_t)kCenRows, gv.L - ch * kCenRows);
+            for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, (double)cur[r * dim + threadIdx.x]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < dim) cen[(int64_t)g * dim + threadIdx.x] = __ddiv_rn(acc, (double)gv.L);
+}
+
 // sq_dist(span<float>, vector<double>) / sq_dist(span<float>, span<float>)
 // (synapse.cpp:155-171): sequential over coordinates, no FMA.
 __device__ __forceinline__ double sq_dist_exact(const float* x, int64_t xs, const double* b, int dim) {
@@ -646,17 +722,34 @@ void plan_select(ArenaPlan& p, const GroupView& g, int k) {
     p.take<double>((size_t)g.G * take);         // pick scores
 }
 
+void centroid_launch(const GroupView& g, double* cen, cudaStream_t s) {
+    if (g.dim > 1024) fail(CX_DEVICE_ERROR, "select: dim > 1024 unsupported");
+    if (g.dim % 32 == 0 && (g.rstride & 3) == 0 && (g.gstride & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(g.X) & 15) == 0) {
+        centroid_pipe_kernel<<<dim3((unsigned)(g.dim / 32), (unsigned)g.G), 32, 0, s>>>(g, cen);
+        check_launch("centroid_pipe_kernel");
+    } else if (g.dim <= 256) {
+        const size_t smem = sizeof(float) * 2 * kCenRows * g.dim;
+        if (smem > 48 * 1024)
+            CX_CUDA(cudaFuncSetAttribute(centroid_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        centroid_staged_kernel<<<g.G, 256, smem, s>>>(g, cen);
+        check_launch("centroid_staged_kernel");
+    } else {
+        centroid_kernel<<<g.G, ((g.dim + 31) / 32) * 32, 0, s>>>(g, cen);
+        check_launch("centroid_kernel");
+    }
+}
+
 void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
-                    unsigned flags, int64_t* rows, double* scores, cudaStream_t s) {
+                    unsigned flags, int64_t* rows, double* scores, cudaStream_t s, const double* cen_in) {
     const int take = (int)std::min<int64_t>(k, g.L);
     if (take <= 0 || g.G <= 0) return;
     double* cen = ctx->arena.take<double>((size_t)g.G * g.dim);
     int64_t* pr = ctx->arena.take<int64_t>((size_t)g.G * take);
     double* ps = ctx->arena.take<double>((size_t)g.G * take);
 
-    if (g.dim > 1024) fail(CX_DEVICE_ERROR, "select: dim > 1024 unsupported");
-    centroid_kernel<<<g.G, ((g.dim + 31) / 32) * 32, 0, s>>>(g, cen);
-    check_launch("centroid_kernel");
+    if (cen_in) cen = const_cast<double*>(cen_in);
+    else centroid_launch(g, cen, s);
 
     if (!(flags & CX_SELECT_GENERIC) &&
         select64_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, s))
@@ -711,8 +804,7 @@ void coverage_selected(const GroupView& g, const int64_t* sel, int64_t n_sel, do
 void coverage_centroid(cx_ctx* ctx, const GroupView& g, double* out, cudaStream_t s) {
     if (g.L <= 0) return;
     double* cen = ctx->arena.take<double>((size_t)g.G * g.dim);
-    centroid_kernel<<<g.G, ((g.dim + 31) / 32) * 32, 0, s>>>(g, cen);
-    check_launch("centroid_kernel");
+    centroid_launch(g, cen, s);
     coverage_centroid_kernel<<<dim3((unsigned)((g.L + 255) / 256), (unsigned)g.G), 256, sizeof(double) * g.dim, s>>>(
         g, cen, out);
     check_launch("coverage_centroid_kernel");
