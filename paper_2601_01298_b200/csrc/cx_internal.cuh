@@ -163,6 +163,8 @@ void attend_fp64_ws(const float* q, const float* k, const float* v, int64_t n, i
                     double* w /* [H][n] scratch */, float* out, cudaStream_t s);
 // batched decode step (fp32 accumulate)
 void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s);
+// tcgen05 variant (decode_tc.cu); false when the shape does not apply
+bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s);
 
 // KV append: copies block [n_layers][T][d_model] (device) into the cache
 // arrays at rows [dst_row, dst_row+T) of every layer.

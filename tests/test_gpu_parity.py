@@ -369,12 +369,15 @@ def test_synapse_buffer(cx):
     assert b4.wait_nonempty(5000) is None
 
 
-def test_decode_step_vs_oracle(dev, orc):
+@pytest.mark.parametrize("impl,N,k", [("tc", 9, 164), ("tc", 40, 100), ("v2", 9, 164), ("v1", 5, 164)])
+def test_decode_step_vs_oracle(dev, orc, monkeypatch, impl, N, k):
     """Batched decode (append + attend) == kernels::attend(n_heads=1) per (agent, layer, q-head)
-    over [synapse rows of its KV head || private rows] (scheduler.cpp:245-262), 1e-3 rel."""
+    over [synapse rows of its KV head || private rows] (scheduler.cpp:245-262), 1e-3 rel.
+    impl: tc = tcgen05 synapse GEMMs, v2 = CUDA-core register-tiled, v1 = generic."""
     import torch
+    monkeypatch.setenv("CX_DECODE", impl)
     gen = torch.Generator(device="cuda").manual_seed(11)
-    Lr, H, Q, dk, Tc, N, k = 3, 2, 14, 64, 33, 9, 164
+    Lr, H, Q, dk, Tc = 3, 2, 14, 64, 33
     syn_k = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
     syn_v = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
     tk = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
