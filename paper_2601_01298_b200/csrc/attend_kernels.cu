@@ -487,10 +487,10 @@ static bool launch_decode_v2(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t
 
 void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int qpg = b.n_q / b.n_kv;
-    // CX_DECODE=tc|v2|v1 pins an implementation (testing); default: v2, then v1.
-    // The tcgen05 kernel (decode_tc.cu) runs only when pinned until it beats v2.
+    // CX_DECODE=tc|v2|v1 pins an implementation (testing); default: the tcgen05
+    // kernel (decode_tc.cu), then v2 (CUDA cores), then the generic v1.
     const char* pin = getenv("CX_DECODE");
-    const bool allow_tc = pin && !strcmp(pin, "tc");
+    const bool allow_tc = !pin || !strcmp(pin, "tc");
     const bool allow_v2 = !pin || !strcmp(pin, "tc") || !strcmp(pin, "v2");
     if (allow_tc && decode_tc_launch(ctx, b, s)) return;
     if (allow_v2 && b.d_k == DV2_DK && b.k_syn <= 32 * DV2_KPL && b.t_cap <= 64) {

@@ -3,22 +3,32 @@
 //
 // For one (layer, KV head) the synapse part of every agent's attention is a
 // GEMM across agents: S = Q K_syn^T with M = agents x q-heads, N = k_syn,
-// K = d_k = 64, then O_syn = P V_syn.  A CTA owns one (layer, KV head) and
-// loops over tiles of 128 query rows (18 agents x 7 q-heads):
-//   1. Q tile -> shared memory as a bf16 hi/lo pair (x = hi + lo exactly to
-//      2^-17), K_syn / V_syn^T staged once per CTA the same way;
-//   2. one thread issues S = Qhi Khi + Qhi Klo + Qlo Khi (tcgen05.mma kind::f16,
-//      fp32 accumulate in TMEM) while all warps compute the private-row scores
-//      on CUDA cores (warp per agent, lane per private row);
-//   3. thread-per-row softmax over [synapse || private] (tcgen05.ld of the S
-//      row, max/exp/sum in fp32), unnormalised P_syn written back as bf16 hi/lo;
-//   4. one thread issues O = P V_syn (3 MMAs per k-step) while the warps mix the
-//      private rows (lane per output dim) into shared memory;
-//   5. thread-per-row epilogue: (O_syn + O_priv) / sum -> global.
-// The new token's K/V is appended to the private rows first (fused).
-// Accuracy: every product is formed to ~2^-16 relative, accumulated in fp32,
-// i.e. the north_star's "fp32 accumulate, 1e-3 relative" contract.
+// K = d_k = 64, then O_syn = P V_syn.  The private rows (each agent's own
+// recent K/V, the dominant HBM stream) are per-agent and have no reuse.  A CTA
+// owns one (layer, KV head), stages K_syn / V_syn^T once, and loops over tiles
+// of 128 query rows (e.g. 18 agents x 7 q-heads) with two warp roles that run
+// concurrently and meet once per tile:
+//   synapse warps 0-3 (thread per TMEM lane = query row):
+//     1. Q tile -> shared memory as a bf16 hi/lo pair (x = hi + lo to 2^-17);
+//     2. one thread issues S = Qlo Khi + Qhi Klo + Qhi Khi (tcgen05.mma
+//        kind::f16, fp32 accumulate in TMEM);
+//     3. row softmax over the synapse keys (m_s, l_s), unnormalised P as bf16
+//        hi/lo in 96-key chunks, O_syn = P V_syn (3 MMAs per k-step) into TMEM;
+//     5. epilogue: merge with the private partial (flash-style rescale).
+//   private warps 4-15 (warp per agent, all q-heads of the KV group):
+//     4. append the new token's K/V (fused), stream the private K rows (lane
+//        per row, full-row loads in flight) and V rows (lane per 2 dims), form
+//        scores / softmax (m_p, l_p) / O_priv on CUDA cores, publish to shared
+//        memory (O_priv aliases the Q tile once the score MMAs have read it).
+// The merge (m = max(m_s, m_p); O = (O_s e^{m_s-m} + O_p e^{m_p-m}) /
+// (l_s e^{m_s-m} + l_p e^{m_p-m})) is the same softmax the oracle computes in
+// one pass (oracle/cortex_oracle.c cx_o_attend, reference kernels.cpp:127-158).
+// Accuracy: every synapse product is formed to ~2^-16 relative and all sums
+// accumulate in fp32: the north_star's "fp32 accumulate, 1e-3 relative".
 #include <cuda_bf16.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "cx_internal.cuh"
 
@@ -26,11 +36,17 @@ namespace cx {
 
 namespace {
 
-constexpr int TD = 64;         // d_k
-constexpr int TM = 128;        // MMA M (query rows per tile)
-constexpr int TNS_MAX = 176;   // padded synapse keys (multiple of 16)
-constexpr int TTAIL = 64;      // max private rows
-constexpr int TTHREADS = 256;
+constexpr int TD = 64;          // d_k
+constexpr int TM = 128;         // MMA M (query rows per tile)
+constexpr int TNS_MAX = 176;    // padded synapse keys (multiple of 16)
+constexpr int TTAIL = 64;       // max private rows
+constexpr int SWARPS = 4;       // synapse warps (TMEM lanes 0-127)
+constexpr int PWARPS = 12;      // private-row warps (13+ warps allocate registers like 16)
+constexpr int TTHREADS = 32 * (SWARPS + PWARPS);
+constexpr int TPCH = 96;        // synapse keys per P.V chunk
+constexpr int OPS = TD + 4;     // O_priv row stride (floats; conflict-free float4 rows)
+constexpr int SST = TTAIL + 4;  // private score row stride (16-B aligned, conflict-free stores)
+
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -73,6 +89,42 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* m, uint32_t parity) {
                      : "r"(su32(m)), "r"(parity)
                      : "memory");
     } while (!ok);
+    __syncwarp();
+}
+
+// Named barriers count whole warps (.aligned): reconverge first -- lanes leave the
+// mbarrier spin loops at different iterations, and a diverged warp would arrive twice.
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    __syncwarp();
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    __syncwarp();
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// packed fp32x2 FMA (sm_100): two independent fp32 FMAs per instruction
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+          "l"(*reinterpret_cast<uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
+
+// long waits (a role waiting for the other): back off instead of spinning on issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* m, uint32_t parity) {
+    uint32_t ok = 0;
+    for (;;) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(su32(m)), "r"(parity)
+                     : "memory");
+        if (ok) break;
+        __nanosleep(128);
+    }
+    __syncwarp();
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* out) {
@@ -93,54 +145,181 @@ __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bflo
     lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
-constexpr int TPCH = 96;       // synapse keys per P.V chunk (P buffer = 128 x 96 bf16 hi/lo)
+// 8 floats -> one 16-byte core-matrix row chunk of hi and of lo (packed bf16x2 conversions)
+__device__ __forceinline__ void split8_store(const float* x, unsigned char* hi_base, unsigned char* lo_base, uint32_t off) {
+    uint32_t hv[4], lv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * u], x[2 * u + 1]);
+        const float2 hf = __bfloat1622float2(h2);
+        const __nv_bfloat162 l2 = __floats2bfloat162_rn(x[2 * u] - hf.x, x[2 * u + 1] - hf.y);
+        hv[u] = *reinterpret_cast<const uint32_t*>(&h2);
+        lv[u] = *reinterpret_cast<const uint32_t*>(&l2);
+    }
+    *reinterpret_cast<uint4*>(hi_base + off) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    *reinterpret_cast<uint4*>(lo_base + off) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
 struct TcLayout {
-    size_t kh, kl, vh, vl, qh, ql, ph, pl, st, rs, mbar, tbase, total;
-    int ns;       // padded synapse keys
-    int sstride;  // private-score row stride
+    size_t kh, kl, vh, vl, qo, ph, pl, sw, mp, lp, mbar, tbase, total;
+    int ns;  // padded synapse keys
 };
 
-__host__ __device__ inline TcLayout tc_layout(int k_syn, int t_cap) {
+__host__ __device__ inline TcLayout tc_layout(int k_syn, int qpg) {
     TcLayout L;
     L.ns = ((k_syn + 15) / 16) * 16;
-    L.sstride = t_cap + 1;
-    const size_t kv = (size_t)L.ns * TD * 2;       // one bf16 operand
-    const size_t q = (size_t)TM * TD * 2;
+    const size_t kv = (size_t)L.ns * TD * 2;  // one bf16 operand
+    const size_t q2 = (size_t)2 * TM * TD * 2, op = sizeof(float) * (size_t)TM * OPS;
     const size_t pp = (size_t)TM * TPCH * 2;
+    const size_t pw = sizeof(float) * (size_t)PWARPS * qpg * SST;
     size_t o = 0;
     L.kh = o; o += kv;
     L.kl = o; o += kv;
     L.vh = o; o += kv;
     L.vl = o; o += kv;
-    L.qh = o; o += q;   // Q hi/lo; reused as the private-row output [TM][TD] fp32 in step 4
-    L.ql = o; o += q;
+    L.qo = o; o += q2 > op ? q2 : op;  // Q hi|lo, then O_priv [TM][OPS] once the score MMAs are done
     L.ph = o; o += pp;
     L.pl = o; o += pp;
-    L.st = o; o += sizeof(float) * (size_t)TM * L.sstride;  // private scores / weights
-    L.rs = o; o += sizeof(float) * TM;                       // row sums
-    L.mbar = o; o += 16;
+    L.sw = o; o += pw;                 // per private warp: scores / weights [qpg][SST]
+    L.mp = o; o += sizeof(float) * 2 * TM;  // private (m, l) per row, double-buffered by tile parity
+    L.lp = o; o += sizeof(float) * 2 * TM;
+    L.mbar = o; o += 32;
     L.tbase = o; o += 16;
     L.total = (o + 127) & ~(size_t)127;
     return L;
 }
 
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// trc (CX_TC_TRACE=1, debugging only): phase timestamps of CTA (0, 0)
+#define TC_TRACE(slot)                                                                  \
+    do {                                                                                \
+        if (trc && blockIdx.x == 0 && blockIdx.y == 0) trc[(slot)] = gtime();            \
+    } while (0)
+
+// ---- private-row helpers (warp per agent) ----
+// Private rows are read with ld.global.cg (L2-coherent, no L1 allocation: they have
+// no reuse).  q lives in registers: lane rl of a row's 8 lanes holds dims
+// [4 rl, 4 rl + 4) and [32 + 4 rl, 32 + 4 rl + 4) of every head.
+
+// scores of rows [r0, r0 + 4 NG): 8 lanes per row, 4 rows per warp load (4 x 128
+// contiguous bytes), packed FMAs, reduce-scatter so that the 8 lanes of a row end
+// up with one head each; rows at or beyond nt are masked when PRED.
+template <int QPG, int NG, bool PRED>
+__device__ __forceinline__ void score_rows(const float* tk, int r0, int nt, const float4 (&qa)[QPG],
+                                           const float4 (&qb)[QPG], float* Sw, int lane, float scale) {
+    constexpr int NV = QPG <= 1 ? 1 : QPG <= 2 ? 2 : QPG <= 4 ? 4 : 8;
+    constexpr int RB = 8 / NV;
+    const int rl = lane & 7, rg = lane >> 3;
+    int hown = 0;
+#pragma unroll
+    for (int w = NV / 2, bit = 4; w >= 1; w >>= 1, bit >>= 1)
+        if (lane & bit) hown += w;
+    float4 ka[NG], kb[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+        const int t = r0 + 4 * j + rg;
+        const float4* kp = reinterpret_cast<const float4*>(tk + (size_t)t * TD);
+        if (!PRED || t < nt) {
+            ka[j] = __ldcg(kp + rl);
+            kb[j] = __ldcg(kp + 8 + rl);
+        } else {
+            ka[j] = kb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+        float v[NV];
+#pragma unroll
+        for (int h = 0; h < NV; ++h) {
+            v[h] = 0.f;
+            if (h < QPG) {
+                float2 acc = ffma2(make_float2(qa[h].x, qa[h].y), make_float2(ka[j].x, ka[j].y), make_float2(0.f, 0.f));
+                acc = ffma2(make_float2(qa[h].z, qa[h].w), make_float2(ka[j].z, ka[j].w), acc);
+                acc = ffma2(make_float2(qb[h].x, qb[h].y), make_float2(kb[j].x, kb[j].y), acc);
+                acc = ffma2(make_float2(qb[h].z, qb[h].w), make_float2(kb[j].z, kb[j].w), acc);
+                v[h] = acc.x + acc.y;
+            }
+        }
+#pragma unroll
+        for (int w = NV / 2, bit = 4; w >= 1; w >>= 1, bit >>= 1) {
+            const bool up = lane & bit;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+                const float send = up ? v[i] : v[i + w];
+                const float keep = up ? v[i + w] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+            }
+        }
+#pragma unroll
+        for (int bit = RB / 2; bit >= 1; bit >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], bit);
+        const int t = r0 + 4 * j + rg;
+        if ((lane & (RB - 1)) == 0 && hown < QPG && (!PRED || t < nt)) Sw[hown * SST + t] = v[0] * scale;
+    }
+}
+
+// o[h] += sum_{t in [r0, r0 + NR)} w[h][t] v[t][2 lane .. 2 lane + 1]; rows >= nt masked when PRED
+template <int QPG, int NR, bool PRED>
+__device__ __forceinline__ void mix_rows(const float* tv, int r0, int nt, const float* Sw, float2 (&o)[QPG], int lane) {
+    float2 v[NR];
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+        v[t] = (!PRED || r0 + t < nt) ? __ldcg(reinterpret_cast<const float2*>(tv + (size_t)(r0 + t) * TD) + lane)
+                                      : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int t4 = 0; t4 < NR / 4; ++t4)
+#pragma unroll
+        for (int h = 0; h < QPG; ++h) {
+            const float4 p4 = reinterpret_cast<const float4*>(Sw + h * SST + r0)[t4];
+            o[h].x = fmaf(p4.x, v[4 * t4].x, o[h].x);
+            o[h].y = fmaf(p4.x, v[4 * t4].y, o[h].y);
+            o[h].x = fmaf(p4.y, v[4 * t4 + 1].x, o[h].x);
+            o[h].y = fmaf(p4.y, v[4 * t4 + 1].y, o[h].y);
+            o[h].x = fmaf(p4.z, v[4 * t4 + 2].x, o[h].x);
+            o[h].y = fmaf(p4.z, v[4 * t4 + 2].y, o[h].y);
+            o[h].x = fmaf(p4.w, v[4 * t4 + 3].x, o[h].x);
+            o[h].y = fmaf(p4.w, v[4 * t4 + 3].y, o[h].y);
+        }
+}
+
 template <int QPG>
-__global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch b, float scale) {
+__global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch b, float scale,
+                                                                 unsigned long long* trc, int skip) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const TcLayout lay = tc_layout(b.k_syn, b.t_cap);
+    const TcLayout lay = tc_layout(b.k_syn, QPG);
     const int NS = lay.ns;
-    __nv_bfloat16* Kh = reinterpret_cast<__nv_bfloat16*>(smem + lay.kh);
-    __nv_bfloat16* Kl = reinterpret_cast<__nv_bfloat16*>(smem + lay.kl);
-    __nv_bfloat16* Vh = reinterpret_cast<__nv_bfloat16*>(smem + lay.vh);
-    __nv_bfloat16* Vl = reinterpret_cast<__nv_bfloat16*>(smem + lay.vl);
-    __nv_bfloat16* Qh = reinterpret_cast<__nv_bfloat16*>(smem + lay.qh);
-    __nv_bfloat16* Ql = reinterpret_cast<__nv_bfloat16*>(smem + lay.ql);
-    float* Ot = reinterpret_cast<float*>(smem + lay.qh);  // aliases Q after the score MMAs
-    __nv_bfloat16* Ph = reinterpret_cast<__nv_bfloat16*>(smem + lay.ph);
-    __nv_bfloat16* Pl = reinterpret_cast<__nv_bfloat16*>(smem + lay.pl);
-    float* St = reinterpret_cast<float*>(smem + lay.st);   // [TM][TTAIL + 1]
-    float* Rs = reinterpret_cast<float*>(smem + lay.rs);
+    unsigned char* Kh = smem + lay.kh;
+    unsigned char* Kl = smem + lay.kl;
+    unsigned char* Vh = smem + lay.vh;
+    unsigned char* Vl = smem + lay.vl;
+    unsigned char* Qh = smem + lay.qo;
+    unsigned char* Ql = smem + lay.qo + (size_t)TM * TD * 2;
+    float* Op = reinterpret_cast<float*>(smem + lay.qo);
+    unsigned char* Ph = smem + lay.ph;
+    unsigned char* Pl = smem + lay.pl;
+    float* Mp = reinterpret_cast<float*>(smem + lay.mp);
+    float* Lp = reinterpret_cast<float*>(smem + lay.lp);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     uint32_t* tbase_s = reinterpret_cast<uint32_t*>(smem + lay.tbase);
 
@@ -159,247 +338,302 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[1])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mbar[2])), "r"(PWARPS));
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
-    const float* sk = b.syn_keys + (size_t)lh * ks * TD;
-    const float* sv = b.syn_values + (size_t)lh * ks * TD;
-    for (int e = tid; e < NS * TD; e += blockDim.x) {
-        const int j = e / TD, c = e % TD;
-        const float kv = j < ks ? __ldg(sk + (size_t)j * TD + c) : 0.f;
-        const float vv = j < ks ? __ldg(sv + (size_t)j * TD + c) : 0.f;
-        __nv_bfloat16 h, lo;
-        split_bf16(kv, h, lo);
-        Kh[cm_off(j, c, NS) >> 1] = h;   // B of S = Q K^T: N = keys, K = dims
-        Kl[cm_off(j, c, NS) >> 1] = lo;
-        split_bf16(vv, h, lo);
-        Vh[cm_off(c, j, TD) >> 1] = h;   // B of O = P V: N = dims, K = keys (V^T)
-        Vl[cm_off(c, j, TD) >> 1] = lo;
+    {
+        const float* sk = b.syn_keys + (size_t)lh * ks * TD;
+        const float* sv = b.syn_values + (size_t)lh * ks * TD;
+        constexpr int IT = (TNS_MAX * 8 + TTHREADS - 1) / TTHREADS;
+        // K: item = (key j, 8-dim chunk c): two float4 loads, one hi and one lo store
+        float4 ka[IT], kb[IT];
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int it = tid + k * TTHREADS, j = it >> 3, c = it & 7;
+            ka[k] = kb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j < ks) {
+                ka[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c));
+                kb[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c) + 1);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int it = tid + k * TTHREADS, j = it >> 3, c = it & 7;
+            if (j < NS) {
+                const float x[8] = {ka[k].x, ka[k].y, ka[k].z, ka[k].w, kb[k].x, kb[k].y, kb[k].z, kb[k].w};
+                split8_store(x, Kh, Kl, cm_off(j, 8 * c, NS));  // B of S = Q K^T: N = keys, K = dims
+            }
+        }
+        // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int it = tid + k * TTHREADS, c = it & (TD - 1), jc = it >> 6;
+            if (jc < NS / 8) {
+                float x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = 8 * jc + u;
+                    x[u] = j < ks ? __ldg(sv + (size_t)j * TD + c) : 0.f;
+                }
+                split8_store(x, Vh, Vl, cm_off(c, 8 * jc, TD));  // B of O = P V: N = dims, K = keys
+            }
+        }
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0) TC_TRACE(1000);
     const uint32_t tS = *tbase_s, tO = tS + (uint32_t)NS;
-    const uint32_t idS = idesc_bf16_f32(TM, NS), idO = idesc_bf16_f32(TM, TD);
-    uint32_t ph0 = 0, ph1 = 0;
-
     const int n_tiles = (b.n_agents + AT - 1) / AT;
-    for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y) {
-        const int a0 = tile * AT;
-        const int na = min(AT, b.n_agents - a0);
-        const int rows = na * QPG;
-        // ---- 1. Q tile -> bf16 hi/lo (rows >= `rows` zero) ----
-        for (int e = tid; e < TM * TD; e += blockDim.x) {
-            const int r = e / TD, c = e % TD;
-            float x = 0.f;
-            if (r < rows) {
-                const int a = a0 + r / QPG, hh = r % QPG;
-                x = __ldg(b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD + c);
-            }
-            __nv_bfloat16 h, lo;
-            split_bf16(x, h, lo);
-            Qh[cm_off(r, c, TM) >> 1] = h;
-            Ql[cm_off(r, c, TM) >> 1] = lo;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        // ---- 2. S = Q K^T on the tensor cores (3 MMAs per 16-wide k-step) ----
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t qlbo = (TM / 8) * 128, klbo = (uint32_t)(NS / 8) * 128;
-            for (int kk = 0; kk < TD / 16; ++kk) {
-                const uint32_t qo = kk * 2 * qlbo, ko = kk * 2 * klbo;
-                const uint64_t qh = sdesc(su32(Qh) + qo, qlbo, 128), ql = sdesc(su32(Ql) + qo, qlbo, 128);
-                const uint64_t kh = sdesc(su32(Kh) + ko, klbo, 128), kl = sdesc(su32(Kl) + ko, klbo, 128);
-                mma_bf16(tS, ql, kh, idS, kk > 0 ? 1u : 0u);
-                mma_bf16(tS, qh, kl, idS, 1u);
-                mma_bf16(tS, qh, kh, idS, 1u);
-            }
-            mma_commit(&mbar[0]);
-        }
-        // private-row scores on CUDA cores while the MMAs run: warp per agent,
-        // lane t (and t + 32) per private row, all q-heads of the group
-        for (int ai = warp; ai < na; ai += TTHREADS / 32) {
-            const int a = a0 + ai;
-            const int len = min(b.tail_len[a], b.t_cap - (app ? 1 : 0));
-            const int nt = len + (app ? 1 : 0);
-            const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
-            const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * TD;
-            if (app && lane < 16) {  // append the new row (fused)
-                reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[lane] =
-                    __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + lane);
-                reinterpret_cast<float4*>(b.tail_values + toff + (size_t)len * TD)[lane] =
-                    __ldg(reinterpret_cast<const float4*>(b.new_values + noff) + lane);
-            }
-            float acc[2][QPG];
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int h = 0; h < QPG; ++h) acc[i][h] = 0.f;
-            const float* r0p = (app && lane == len) ? b.new_keys + noff : b.tail_keys + toff + (size_t)lane * TD;
-            const float* r1p = (app && lane + 32 == len) ? b.new_keys + noff : b.tail_keys + toff + (size_t)(lane + 32) * TD;
-#pragma unroll 2
-            for (int c8 = 0; c8 < TD / 8; ++c8) {
-                float4 k0a = make_float4(0.f, 0.f, 0.f, 0.f), k0b = k0a, k1a = k0a, k1b = k0a;
-                if (lane < nt) {
-                    k0a = __ldg(reinterpret_cast<const float4*>(r0p) + 2 * c8);
-                    k0b = __ldg(reinterpret_cast<const float4*>(r0p) + 2 * c8 + 1);
-                }
-                if (lane + 32 < nt) {
-                    k1a = __ldg(reinterpret_cast<const float4*>(r1p) + 2 * c8);
-                    k1b = __ldg(reinterpret_cast<const float4*>(r1p) + 2 * c8 + 1);
-                }
-                const float k0[8] = {k0a.x, k0a.y, k0a.z, k0a.w, k0b.x, k0b.y, k0b.z, k0b.w};
-                const float k1[8] = {k1a.x, k1a.y, k1a.z, k1a.w, k1b.x, k1b.y, k1b.z, k1b.w};
-#pragma unroll
-                for (int h = 0; h < QPG; ++h) {
-                    const int r = ai * QPG + h;  // q = hi + lo, read back from the A operand
-                    const uint4 hv = *reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(Qh) + cm_off(r, 8 * c8, TM));
-                    const uint4 lv = *reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(Ql) + cm_off(r, 8 * c8, TM));
-                    const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
-                    const __nv_bfloat16* lb = reinterpret_cast<const __nv_bfloat16*>(&lv);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const float qv = __bfloat162float(hb[u]) + __bfloat162float(lb[u]);
-                        acc[0][h] = fmaf(qv, k0[u], acc[0][h]);
-                        acc[1][h] = fmaf(qv, k1[u], acc[1][h]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < QPG; ++h) {
-                float* srow = St + (ai * QPG + h) * lay.sstride;
-                if (lane < nt) srow[lane] = acc[0][h] * scale;
-                if (lane + 32 < nt) srow[lane + 32] = acc[1][h] * scale;
-            }
-        }
-        mbar_wait_parity(&mbar[0], ph0);
-        ph0 ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        __syncthreads();  // private scores in St; S in TMEM; Q (shared) is dead -> Ot may reuse it
+    uint32_t tpar = 0;  // mbar[0] completes once per tile (score MMAs)
 
-        // ---- 3. softmax per row (warps 0-3 own TMEM lanes 0-127 = rows) ----
-        const int sst = lay.sstride;
-        const uint32_t trow = tS + ((uint32_t)((warp & 3) * 32) << 16);
-        const int r_own = (warp & 3) * 32 + lane;
-        float m_row = -INFINITY, sum_row = 0.f;
-        if (warp < 4) {
-            const bool live = r_own < rows;
-            int nt = 0;
-            if (live) {
-                const int a = a0 + r_own / QPG;
-                nt = min(b.tail_len[a], b.t_cap - (app ? 1 : 0)) + (app ? 1 : 0);
+    if (warp < SWARPS) {
+        // ======================= synapse warps =======================
+        const uint32_t idS = idesc_bf16_f32(TM, NS), idO = idesc_bf16_f32(TM, TD);
+        const uint32_t trow = tS + ((uint32_t)(warp * 32) << 16);
+        const int r_own = warp * 32 + lane;
+        uint32_t ph1 = 0;
+        int ti = 0;
+        for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
+            if (tid == 0) TC_TRACE(ti * 16 + 0);
+            const int a0 = tile * AT;
+            const int rows = min(AT, b.n_agents - a0) * QPG;
+            if (skip & 1) {  // debugging only (CX_TC_SKIP): keep the hand-off protocol, skip the math
+                if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[0])) : "memory");
+                mbar_wait_parity(&mbar[0], tpar);
+                mbar_wait_sleep(&mbar[2], tpar);
+                bar_sync(1, SWARPS * 32);
+                tpar ^= 1u;
+                continue;
             }
-            for (int c0 = 0; c0 < NS; c0 += 16) {
-                float v[16];
-                tmem_ld16(trow + (uint32_t)c0, v);
+            // 1. Q tile -> bf16 hi/lo; lane -> (row rb + lane%8, chunk cb + lane/8):
+            //    4 lanes read 128 contiguous bytes of a row, 8 lanes store 128 contiguous bytes
+            {
+                float4 xa[8], xb[8];
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c0 + j < ks) m_row = fmaxf(m_row, v[j] * scale);
-            }
-            float* srow = St + r_own * sst;
-            for (int t = 0; t < nt; ++t) m_row = fmaxf(m_row, srow[t]);
-            for (int t = 0; t < nt; ++t) {  // private weights (unnormalised)
-                const float p = __expf(srow[t] - m_row);
-                srow[t] = p;
-                sum_row += p;
-            }
-        }
-        // ---- 4. O_syn = P V_syn on the tensor cores in 96-key chunks; the
-        //         private rows are mixed on CUDA cores during the first chunk ----
-        for (int k0 = 0; k0 < NS; k0 += TPCH) {
-            const int kn = min(TPCH, NS - k0);
-            if (warp < 4) {
-                const bool live = r_own < rows;
-                for (int c0 = 0; c0 < kn; c0 += 16) {
-                    float v[16];
-                    tmem_ld16(trow + (uint32_t)(k0 + c0), v);
-#pragma unroll
-                    for (int j8 = 0; j8 < 2; ++j8) {  // 8 keys = one 16-byte core-matrix row chunk
-                        __align__(16) __nv_bfloat16 hv[8], lv[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int j = k0 + c0 + j8 * 8 + u;
-                            const float p = (live && j < ks) ? __expf(v[j8 * 8 + u] * scale - m_row) : 0.f;
-                            sum_row += p;
-                            split_bf16(p, hv[u], lv[u]);
-                        }
-                        const uint32_t off = cm_off(r_own, c0 + j8 * 8, TM);
-                        *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(Ph) + off) = *reinterpret_cast<uint4*>(hv);
-                        *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(Pl) + off) = *reinterpret_cast<uint4*>(lv);
+                for (int it = 0; it < 8; ++it) {
+                    const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
+                    xa[it] = xb[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (r < rows) {
+                        const int a = a0 + r / QPG, hh = r % QPG;
+                        const float4* src = reinterpret_cast<const float4*>(
+                            b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD + 8 * c);
+                        xa[it] = __ldg(src);
+                        xb[it] = __ldg(src + 1);
                     }
+                }
+#pragma unroll
+                for (int it = 0; it < 8; ++it) {
+                    const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
+                    const float x[8] = {xa[it].x, xa[it].y, xa[it].z, xa[it].w, xb[it].x, xb[it].y, xb[it].z, xb[it].w};
+                    split8_store(x, Qh, Ql, cm_off(r, 8 * c, TM));
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncthreads();
+            bar_sync(1, SWARPS * 32);
+            if (tid == 0) TC_TRACE(ti * 16 + 1);
+            // 2. S = Q K^T on the tensor cores (3 MMAs per 16-wide k-step)
             if (tid == 0) {
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t plbo = (TM / 8) * 128, vlbo = (TD / 8) * 128;
-                for (int kk = 0; kk < kn / 16; ++kk) {
-                    const uint32_t po = kk * 2 * plbo, vo = ((k0 >> 3) + kk * 2) * vlbo;
-                    const uint64_t ph = sdesc(su32(Ph) + po, plbo, 128), pl = sdesc(su32(Pl) + po, plbo, 128);
-                    const uint64_t vh = sdesc(su32(Vh) + vo, vlbo, 128), vl = sdesc(su32(Vl) + vo, vlbo, 128);
-                    mma_bf16(tO, pl, vh, idO, (k0 > 0 || kk > 0) ? 1u : 0u);
-                    mma_bf16(tO, ph, vl, idO, 1u);
-                    mma_bf16(tO, ph, vh, idO, 1u);
-                }
-                mma_commit(&mbar[1]);
-            }
-            if (k0 == 0) {
-                for (int ai = warp; ai < na; ai += TTHREADS / 32) {  // lane owns dims 2 lane, 2 lane + 1
-            const int a = a0 + ai;
-            const int len = min(b.tail_len[a], b.t_cap - (app ? 1 : 0));
-            const int nt = len + (app ? 1 : 0);
-            const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
-            const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * TD;
-            float2 o[QPG];
+                const uint32_t qlbo = (TM / 8) * 128, klbo = (uint32_t)(NS / 8) * 128;
 #pragma unroll
-            for (int h = 0; h < QPG; ++h) o[h] = make_float2(0.f, 0.f);
-#pragma unroll 4
-            for (int t = 0; t < nt; ++t) {
-                const float* vrow = (app && t == len) ? b.new_values + noff : b.tail_values + toff + (size_t)t * TD;
-                const float2 v = __ldg(reinterpret_cast<const float2*>(vrow) + lane);
+                for (int kk = 0; kk < TD / 16; ++kk) {
+                    const uint32_t qo = kk * 2 * qlbo, ko = kk * 2 * klbo;
+                    const uint64_t qh = sdesc(su32(Qh) + qo, qlbo, 128), ql = sdesc(su32(Ql) + qo, qlbo, 128);
+                    const uint64_t kh = sdesc(su32(Kh) + ko, klbo, 128), kl = sdesc(su32(Kl) + ko, klbo, 128);
+                    mma_bf16(tS, ql, kh, idS, kk > 0 ? 1u : 0u);
+                    mma_bf16(tS, qh, kl, idS, 1u);
+                    mma_bf16(tS, qh, kh, idS, 1u);
+                }
+                mma_commit(&mbar[0]);
+            }
+            mbar_wait_parity(&mbar[0], tpar);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (tid == 0) TC_TRACE(ti * 16 + 2);
+            // 3. softmax over the synapse keys, thread per row
+            const bool live = r_own < rows;
+            float mx = -INFINITY, l_s = 0.f;
+            for (int c0 = 0; c0 < NS; c0 += 16) {
+                float v[16];
+                tmem_ld16(trow + (uint32_t)c0, v);
+                if (c0 + 16 <= ks) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) mx = fmaxf(mx, v[j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (c0 + j < ks) mx = fmaxf(mx, v[j]);
+                }
+            }
+            const float m_s = mx * scale;                   // scale > 0
+            const float c2 = scale * 1.4426950408889634f;   // e^{(s - mx) scale} = 2^{s c2 - mx c2}
+            const float m2 = live ? mx * c2 : INFINITY;     // padding rows: all weights 0
+            if (tid == 0) TC_TRACE(ti * 16 + 3);
+            for (int k0 = 0; k0 < NS; k0 += TPCH) {
+                const int kn = min(TPCH, NS - k0);
+                for (int c0 = 0; c0 < kn; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(trow + (uint32_t)(k0 + c0), v);
+                    float p[16];
+                    if (k0 + c0 + 16 <= ks) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) p[j] = ex2(fmaf(v[j], c2, -m2));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) p[j] = k0 + c0 + j < ks ? ex2(fmaf(v[j], c2, -m2)) : 0.f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) l_s += p[j];
+                    split8_store(p, Ph, Pl, cm_off(r_own, c0, TM));
+                    split8_store(p + 8, Ph, Pl, cm_off(r_own, c0 + 8, TM));
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                bar_sync(1, SWARPS * 32);
+                if (tid == 0) {
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t plbo = (TM / 8) * 128, vlbo = (TD / 8) * 128;
+                    for (int kk = 0; kk < kn / 16; ++kk) {
+                        const uint32_t po = kk * 2 * plbo, vo = ((k0 >> 3) + kk * 2) * vlbo;
+                        const uint64_t ph = sdesc(su32(Ph) + po, plbo, 128), pl = sdesc(su32(Pl) + po, plbo, 128);
+                        const uint64_t vh = sdesc(su32(Vh) + vo, vlbo, 128), vl = sdesc(su32(Vl) + vo, vlbo, 128);
+                        mma_bf16(tO, pl, vh, idO, (k0 > 0 || kk > 0) ? 1u : 0u);
+                        mma_bf16(tO, ph, vl, idO, 1u);
+                        mma_bf16(tO, ph, vh, idO, 1u);
+                    }
+                    mma_commit(&mbar[1]);
+                }
+                mbar_wait_parity(&mbar[1], ph1);  // P chunk consumed (and O complete after the last)
+                ph1 ^= 1u;
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            // 5. epilogue: wait for the private partials, merge, store
+            if (tid == 0) TC_TRACE(ti * 16 + 4);
+            mbar_wait_sleep(&mbar[2], tpar);  // every private warp has published this tile
+            if (tid == 0) TC_TRACE(ti * 16 + 5);
+            {
+                float v[TD];
+                const uint32_t trow_o = tO + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+                for (int c0 = 0; c0 < TD; c0 += 16) tmem_ld16(trow_o + (uint32_t)c0, v + c0);
+                if (live) {
+                    const int a = a0 + r_own / QPG, hh = r_own % QPG;
+                    const float m_p = Mp[tpar * TM + r_own], l_p = Lp[tpar * TM + r_own];
+                    const float m = fmaxf(m_s, m_p);
+                    const float as = __expf(m_s - m), ap = __expf(m_p - m);
+                    const float inv = 1.0f / (l_s * as + l_p * ap);
+                    const float cs = as * inv, cp = ap * inv;
+                    float* out = b.out + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD;
+                    const float4* op = reinterpret_cast<const float4*>(Op + r_own * OPS);
+#pragma unroll
+                    for (int c4 = 0; c4 < TD / 4; ++c4) {
+                        const float4 p = op[c4];
+                        reinterpret_cast<float4*>(out)[c4] =
+                            make_float4(v[4 * c4] * cs + p.x * cp, v[4 * c4 + 1] * cs + p.y * cp,
+                                        v[4 * c4 + 2] * cs + p.z * cp, v[4 * c4 + 3] * cs + p.w * cp);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            bar_sync(1, SWARPS * 32);  // Op / TMEM reuse by the next tile
+            if (tid == 0) TC_TRACE(ti * 16 + 6);
+            tpar ^= 1u;
+        }
+    } else {
+        // ======================= private warps =======================
+        const int pw = warp - SWARPS;
+        float* Sw = reinterpret_cast<float*>(smem + lay.sw) + pw * QPG * SST;
+        static_assert(QPG <= 8, "the score reduce-scatter handles up to 8 q-heads per KV head");
+        int ti = 0;
+        for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
+            const int a0 = tile * AT;
+            const int na = min(AT, b.n_agents - a0);
+            bool published = false;
+            if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + 8);
+            for (int ai = pw; ai < na; ai += PWARPS) {
+                if (skip & 2) {  // debugging only (CX_TC_SKIP)
+                    if (!published) mbar_wait_sleep(&mbar[0], tpar);
+                    published = true;
+                    continue;
+                }
+                const int a = a0 + ai;
+                const int len = min(b.tail_len[a], b.t_cap - (app ? 1 : 0));
+                const int nt = len + (app ? 1 : 0);
+                const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
+                const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * TD;
+                const float* tk = b.tail_keys + toff;
+                const float* tv = b.tail_values + toff;
+                const float* qrow = b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG) * TD;
+                if (app && lane < 16) {  // append the new row (fused); read back below like any other row
+                    reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[lane] =
+                        __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + lane);
+                    reinterpret_cast<float4*>(b.tail_values + toff + (size_t)len * TD)[lane] =
+                        __ldg(reinterpret_cast<const float4*>(b.new_values + noff) + lane);
+                }
+                float4 qa[QPG], qb[QPG];
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) {
-                    const float p = St[(ai * QPG + h) * sst + t];
-                    o[h].x = fmaf(p, v.x, o[h].x);
-                    o[h].y = fmaf(p, v.y, o[h].y);
+                    qa[h] = __ldg(reinterpret_cast<const float4*>(qrow + (size_t)h * TD) + (lane & 7));
+                    qb[h] = __ldg(reinterpret_cast<const float4*>(qrow + (size_t)h * TD) + 8 + (lane & 7));
                 }
-            }
+                // The warp barrier orders the appended row before the warp's own reads of it.
+                __syncwarp();
+                // ---- scores: 16-row batches, then 4-row groups ----
+                int r0 = 0;
+                for (; r0 + 16 <= nt; r0 += 16) score_rows<QPG, 4, false>(tk, r0, nt, qa, qb, Sw, lane, scale);
+                for (; r0 < nt; r0 += 4) score_rows<QPG, 1, true>(tk, r0, nt, qa, qb, Sw, lane, scale);
+                if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == 0 ? 9 : 12));
+                __syncwarp();
+                // softmax per q-head over the private rows (weights 0 up to TTAIL)
 #pragma unroll
-            for (int h = 0; h < QPG; ++h) reinterpret_cast<float2*>(Ot + (ai * QPG + h) * TD)[lane] = o[h];
+                for (int h = 0; h < QPG; ++h) {
+                    const float s0 = lane < nt ? Sw[h * SST + lane] : -INFINITY;
+                    const float s1 = lane + 32 < nt ? Sw[h * SST + lane + 32] : -INFINITY;
+                    const float m = warp_max(fmaxf(s0, s1));
+                    const float p0 = lane < nt ? __expf(s0 - m) : 0.f;
+                    const float p1 = lane + 32 < nt ? __expf(s1 - m) : 0.f;
+                    Sw[h * SST + lane] = p0;
+                    Sw[h * SST + lane + 32] = p1;
+                    const float lsum = warp_sum(p0 + p1);
+                    if (lane == 0) {  // this buffer's previous tile was merged two tiles ago
+                        Mp[tpar * TM + ai * QPG + h] = m;
+                        Lp[tpar * TM + ai * QPG + h] = lsum;
+                    }
                 }
+                __syncwarp();
+                // ---- O_priv = P V_priv (lane: dims 2 lane, 2 lane + 1) ----
+                float2 o[QPG];
+#pragma unroll
+                for (int h = 0; h < QPG; ++h) o[h] = make_float2(0.f, 0.f);
+                r0 = 0;
+                for (; r0 + 16 <= nt; r0 += 16) mix_rows<QPG, 16, false>(tv, r0, nt, Sw, o, lane);
+                for (; r0 < nt; r0 += 4) mix_rows<QPG, 4, true>(tv, r0, nt, Sw, o, lane);
+                if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == 0 ? 10 : 13));
+                // publish into the (dead) Q tile once this tile's score MMAs are complete
+                if (!published) {
+                    mbar_wait_sleep(&mbar[0], tpar);
+                    published = true;
+                }
+#pragma unroll
+                for (int h = 0; h < QPG; ++h) {
+                    const int r = ai * QPG + h;
+                    reinterpret_cast<float2*>(Op + r * OPS)[lane] = o[h];
+                }
+                __syncwarp();  // Sw reuse
             }
-            mbar_wait_parity(&mbar[1], ph1);  // P chunk consumed (and O complete after the last)
-            ph1 ^= 1u;
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            __syncthreads();
+            // Arrive only after this tile's score phase, even with no agents: a warp
+            // must never arrive for tile i+1 before barrier 2 of tile i has completed.
+            if (!published) mbar_wait_sleep(&mbar[0], tpar);
+            if (lane == 0 && pw == 0) TC_TRACE(ti * 16 + 11);
+            if (lane == 0 && pw == PWARPS - 1) TC_TRACE(ti * 16 + 14);
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[2])) : "memory");
+            tpar ^= 1u;
         }
-        // ---- 5. epilogue: (O_syn + O_priv) / sum ----
-        if (warp < 4) {
-            const int r = r_own;
-            const uint32_t trow_o = tO + ((uint32_t)(warp * 32) << 16);
-            float v[TD];
-#pragma unroll
-            for (int c0 = 0; c0 < TD; c0 += 16) tmem_ld16(trow_o + (uint32_t)c0, v + c0);
-            if (r < rows) {
-                const int a = a0 + r / QPG, hh = r % QPG;
-                const float inv = 1.0f / sum_row;
-                float* out = b.out + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD;
-                const float* ot = Ot + r * TD;
-#pragma unroll
-                for (int c4 = 0; c4 < TD / 4; ++c4) {
-                    const float4 p = reinterpret_cast<const float4*>(ot)[c4];
-                    reinterpret_cast<float4*>(out)[c4] =
-                        make_float4((v[4 * c4] + p.x) * inv, (v[4 * c4 + 1] + p.y) * inv, (v[4 * c4 + 2] + p.z) * inv,
-                                    (v[4 * c4 + 3] + p.w) * inv);
-                }
-            }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // Ot / St / TMEM reuse by the next tile
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tbase_s), "r"(256));
 }
 
@@ -408,7 +642,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
 bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int qpg = b.n_q / b.n_kv;
     if (b.d_k != TD || b.k_syn < 1 || b.k_syn > TNS_MAX || b.t_cap > TTAIL) return false;
-    const TcLayout lay = tc_layout(b.k_syn, b.t_cap);
+    const TcLayout lay = tc_layout(b.k_syn, qpg);
     static int max_optin = -1;
     if (max_optin < 0) {
         int dev = 0;
@@ -416,7 +650,7 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
         cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     }
     if (lay.total > (size_t)max_optin) return false;
-    void (*kern)(cx_decode_batch, float) = nullptr;
+    void (*kern)(cx_decode_batch, float, unsigned long long*, int) = nullptr;
     switch (qpg) {
         case 1: kern = decode_tc_kernel<1>; break;
         case 2: kern = decode_tc_kernel<2>; break;
@@ -429,10 +663,34 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int at = TM / qpg;
     const int n_tiles = (b.n_agents + at - 1) / at;
     const int sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
-    const int per_lh = std::max(1, std::min(n_tiles, (sms + n_lh - 1) / n_lh));
+    // one resident CTA per SM: fill the SMs in a single wave
+    const int per_lh = std::max(1, std::min(n_tiles, sms / n_lh));
     CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
-    kern<<<dim3((unsigned)n_lh, (unsigned)per_lh), TTHREADS, lay.total, s>>>(b, (float)(1.0 / std::sqrt((double)b.d_k)));
+    static unsigned long long* trc = nullptr;
+    const bool tracing = getenv("CX_TC_TRACE") != nullptr;
+    if (tracing && !trc) {
+        CX_CUDA(cudaMalloc(&trc, 2048 * sizeof(unsigned long long)));
+        CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
+    }
+    kern<<<dim3((unsigned)n_lh, (unsigned)per_lh), TTHREADS, lay.total, s>>>(b, (float)(1.0 / std::sqrt((double)b.d_k)),
+                                                                             tracing ? trc : nullptr,
+                                                                             getenv("CX_TC_SKIP") ? atoi(getenv("CX_TC_SKIP")) : 0);
     check_launch("decode_tc_kernel");
+    if (tracing) {  // debugging only: per-tile phase times of CTA (0, 0), us since the staging ended
+        std::vector<unsigned long long> h(2048);
+        CX_CUDA(cudaStreamSynchronize(s));
+        CX_CUDA(cudaMemcpy(h.data(), trc, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost));
+        const double t0 = (double)h[1000];
+        fprintf(stderr, "decode_tc trace: grid %d x %d\n", n_lh, per_lh);
+        for (int ti = 0; ti < 62 && h[ti * 16]; ++ti) {
+            fprintf(stderr, "tile %2d syn:", ti);
+            for (int k = 0; k < 7; ++k) fprintf(stderr, " %7.2f", (h[ti * 16 + k] - t0) / 1e3);
+            fprintf(stderr, " | priv0:");
+            for (int k = 8; k < 15; ++k) fprintf(stderr, " %7.2f", h[ti * 16 + k] ? (h[ti * 16 + k] - t0) / 1e3 : -1.0);
+            fprintf(stderr, "\n");
+        }
+        CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
+    }
     return true;
 }
 

@@ -369,15 +369,18 @@ def test_synapse_buffer(cx):
     assert b4.wait_nonempty(5000) is None
 
 
-@pytest.mark.parametrize("impl,N,k", [("tc", 9, 164), ("tc", 40, 100), ("v2", 9, 164), ("v1", 5, 164)])
-def test_decode_step_vs_oracle(dev, orc, monkeypatch, impl, N, k):
+@pytest.mark.parametrize("impl,N,k,Lr", [("tc", 9, 164, 3), ("tc", 40, 100, 3), ("tc", 100, 164, 24),
+                                         ("v2", 9, 164, 3), ("v2", 100, 164, 24), ("v1", 5, 164, 3)])
+def test_decode_step_vs_oracle(dev, orc, monkeypatch, impl, N, k, Lr):
     """Batched decode (append + attend) == kernels::attend(n_heads=1) per (agent, layer, q-head)
     over [synapse rows of its KV head || private rows] (scheduler.cpp:245-262), 1e-3 rel.
-    impl: tc = tcgen05 synapse GEMMs, v2 = CUDA-core register-tiled, v1 = generic."""
+    impl: tc = tcgen05 synapse GEMMs, v2 = CUDA-core register-tiled, v1 = generic.
+    Lr=24, N=100: 48 (layer, KV head) pairs -> several 18-agent tiles per CTA with a
+    ragged last tile (the cross-tile barrier protocol of decode_tc.cu)."""
     import torch
     monkeypatch.setenv("CX_DECODE", impl)
     gen = torch.Generator(device="cuda").manual_seed(11)
-    Lr, H, Q, dk, Tc = 3, 2, 14, 64, 33
+    H, Q, dk, Tc = 2, 14, 64, 33
     syn_k = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
     syn_v = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
     tk = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
