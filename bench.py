@@ -294,7 +294,7 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
     # roofline of the dominant kernel (greedy selection) against HBM
     bytes_per_launch = COMPRESS_BYTES * keys.shape[0] / G
     achieved = bytes_per_launch / (sel_ms * 1e-3) / 1e9
-    dec = run_decode(args, dev) if rank == 0 or True else None
+    dec = run_decode(args, dev, rank, world)
     e2e = run_e2e(args, dev) if rank == 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": "compressions/s", "n_gpus": world, "steps": args.steps,
@@ -306,7 +306,8 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
                    "l2": "flushed (256 MB write) between timed steps"},
         "roofline": {"kernel": "select_kernel (greedy max-min selection)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_source": peak_kind, "traffic": None,
+                     "peak_source": peak_kind, "traffic": ncu_traffic("select64_kernel"),
+                     "traffic_unit": "bytes per launch (ncu --set full, profiles/r1_ncu_full_summary.json)",
                      "note": "selection is fp64/FMA-issue + barrier-latency bound (SURVEY.md §8(d)); "
                              "HBM fraction reported as required"},
         "select_ms": sel_ms,
@@ -330,14 +331,43 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
         print(json.dumps(line), flush=True)
 
 
-def run_decode(args, dev):
+def ncu_traffic(kernel_substr):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes, one launch) of a kernel
+    from the committed `ncu --set full` summary (profiles/r1_ncu_full_summary.json,
+    made by tools/ncu_summary.py from `ncu ... python tools/prof_step.py`), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            rows = json.load(f)
+    except (OSError, ValueError):
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows:
+        if kernel_substr in r.get("Kernel Name", ""):
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v, _, u = r.get(k, "").partition(" ")
+                tot += float(v) * scale.get(u, 1.0)
+            return tot
+    return None
+
+
+def run_decode(args, dev, rank=0, world=1):
+    """Decode leg: N agents x 24 layers (append + attend against the shared synapse).
+    N > 1 GPUs: agents are sharded, each rank holds a synapse
+    replica and its agents' private rows; no per-step exchange.  The step time is
+    the max over ranks; agent-steps/s counts all N agents."""
     import torch
+    import torch.distributed as dist
 
     from paper_2601_01298_b200 import device as cxd
+    from paper_2601_01298_b200.parallel import shard_range
     out = {}
     hbm, _ = load_peaks()
-    for n in sorted({args.n_agents, 1000}):
-        gen = torch.Generator(device=dev).manual_seed(99)
+    for n_total in sorted({args.n_agents, 1000}):
+        ab, ae = shard_range(n_total, rank, world)
+        n = ae - ab
+        gen = torch.Generator(device=dev).manual_seed(99 + rank)
         syn_k = torch.randn(N_LAYERS, N_KV, K, D, device=dev, generator=gen)
         syn_v = torch.randn(N_LAYERS, N_KV, K, D, device=dev, generator=gen)
         tk = torch.randn(n, N_LAYERS, N_KV, T_PRIV + 1, D, device=dev, generator=gen)
@@ -358,10 +388,16 @@ def run_decode(args, dev):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        b = decode_bytes(n)
-        out[f"N{n}"] = {"agent_steps_per_s": n / (ms * 1e-3), "ms_per_step": ms,
-                        "roofline": {"bound": "hbm", "achieved": b / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                                     "frac": b / (ms * 1e-3) / 1e9 / hbm, "bytes": b}}
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t[0])
+        b = decode_bytes(n)  # this rank's bytes (synapse replica + its agents)
+        out[f"N{n_total}"] = {"agent_steps_per_s": n_total / (ms * 1e-3), "ms_per_step": ms,
+                              "agents_per_gpu": n, "kernel": "decode_tc_kernel (tcgen05 synapse + CUDA-core private rows)",
+                              "roofline": {"bound": "hbm", "achieved": b / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                           "frac": b / (ms * 1e-3) / 1e9 / hbm, "bytes": b,
+                                           "traffic": ncu_traffic("decode_tc_kernel") if n == 1000 else None}}
     return out
 
 
