@@ -43,8 +43,8 @@ constexpr int TTAIL = 64;       // max private rows
 constexpr int SWARPS = 4;       // synapse warps (TMEM lanes 0-127)
 constexpr int PWARPS = 12;      // private-row warps (13+ warps allocate registers like 16)
 constexpr int TTHREADS = 32 * (SWARPS + PWARPS);
-constexpr int TPCH = 96;        // synapse keys per P.V chunk
 constexpr int OPS = TD + 4;     // O_priv row stride (floats; conflict-free float4 rows)
+constexpr bool PREFETCH_NEXT = true;  // L2 bulk prefetch of each warp's next agent (net win: -18 us, though ~25% of it is evicted)
 constexpr int SST = TTAIL + 4;  // private score row stride (16-B aligned, conflict-free stores)
 
 
@@ -74,6 +74,20 @@ __device__ __forceinline__ void mma_bf16(uint32_t dtmem, uint64_t ad, uint64_t b
         "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(dtmem),
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
         : "memory");
+}
+
+// A operand from tensor memory (packed bf16x2, row = lane), B from shared memory
+__device__ __forceinline__ void mma_bf16_ts(uint32_t dtmem, uint32_t atmem, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(dtmem),
+        "r"(atmem), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* mbar) {
@@ -113,6 +127,11 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return *reinterpret_cast<float2*>(&d);
 }
 
+// bulk prefetch of a contiguous block into L2 (no registers, no shared memory)
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // long waits (a role waiting for the other): back off instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* m, uint32_t parity) {
     uint32_t ok = 0;
@@ -124,6 +143,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* m, uint32_t parity) {
         if (ok) break;
         __nanosleep(128);
     }
+    __syncwarp();
+}
+
+// private warps: wait until at least `n` tile epilogues have completed
+__device__ __forceinline__ void wait_epilogues(volatile int* epi_done, int n) {
+    if (n > 0)
+        while (*epi_done < n) __nanosleep(64);
+    __threadfence_block();
     __syncwarp();
 }
 
@@ -178,7 +205,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 struct TcLayout {
-    size_t kh, kl, vh, vl, qo, ph, pl, sw, mp, lp, mbar, tbase, total;
+    size_t kh, kl, vh, vl, qo, op, sw, mp, lp, mbar, tbase, total;
     int ns;  // padded synapse keys
 };
 
@@ -187,21 +214,19 @@ __host__ __device__ inline TcLayout tc_layout(int k_syn, int qpg) {
     L.ns = ((k_syn + 15) / 16) * 16;
     const size_t kv = (size_t)L.ns * TD * 2;  // one bf16 operand
     const size_t q2 = (size_t)2 * TM * TD * 2, op = sizeof(float) * (size_t)TM * OPS;
-    const size_t pp = (size_t)TM * TPCH * 2;
     const size_t pw = sizeof(float) * (size_t)PWARPS * qpg * SST;
     size_t o = 0;
     L.kh = o; o += kv;
     L.kl = o; o += kv;
     L.vh = o; o += kv;
     L.vl = o; o += kv;
-    L.qo = o; o += q2 > op ? q2 : op;  // Q hi|lo, then O_priv [TM][OPS] once the score MMAs are done
-    L.ph = o; o += pp;
-    L.pl = o; o += pp;
+    L.qo = o; o += q2;                 // Q hi | lo (A operand of the score MMAs)
+    L.op = o; o += 2 * op;             // O_priv [2][TM][OPS], double-buffered by tile parity
     L.sw = o; o += pw;                 // per private warp: scores / weights [qpg][SST]
     L.mp = o; o += sizeof(float) * 2 * TM;  // private (m, l) per row, double-buffered by tile parity
     L.lp = o; o += sizeof(float) * 2 * TM;
     L.mbar = o; o += 32;
-    L.tbase = o; o += 16;
+    L.tbase = o; o += 16;              // TMEM base address, then the epilogue counter
     L.total = (o + 127) & ~(size_t)127;
     return L;
 }
@@ -223,19 +248,52 @@ __device__ __forceinline__ unsigned long long gtime() {
 // no reuse).  q lives in registers: lane rl of a row's 8 lanes holds dims
 // [4 rl, 4 rl + 4) and [32 + 4 rl, 32 + 4 rl + 4) of every head.
 
-// scores of rows [r0, r0 + 4 NG): 8 lanes per row, 4 rows per warp load (4 x 128
-// contiguous bytes), packed FMAs, reduce-scatter so that the 8 lanes of a row end
-// up with one head each; rows at or beyond nt are masked when PRED.
-template <int QPG, int NG, bool PRED>
-__device__ __forceinline__ void score_rows(const float* tk, int r0, int nt, const float4 (&qa)[QPG],
-                                           const float4 (&qb)[QPG], float* Sw, int lane, float scale) {
+// score of one row per 8-lane group (row t of lane group lane / 8, whose lanes hold
+// its dims [4 rl, 4 rl + 4) in ka and [32 + 4 rl, ...) in kb): packed FMAs, then a
+// reduce-scatter so that the 8 lanes end up with one head each; stored when `valid`
+template <int QPG>
+__device__ __forceinline__ void score_group(const float4& ka, const float4& kb, int t, bool valid,
+                                            const float4 (&qa)[QPG], const float4 (&qb)[QPG], float* Sw, int lane,
+                                            float scale) {
     constexpr int NV = QPG <= 1 ? 1 : QPG <= 2 ? 2 : QPG <= 4 ? 4 : 8;
     constexpr int RB = 8 / NV;
-    const int rl = lane & 7, rg = lane >> 3;
     int hown = 0;
 #pragma unroll
     for (int w = NV / 2, bit = 4; w >= 1; w >>= 1, bit >>= 1)
         if (lane & bit) hown += w;
+    float v[NV];
+#pragma unroll
+    for (int h = 0; h < NV; ++h) {
+        v[h] = 0.f;
+        if (h < QPG) {
+            float2 acc = ffma2(make_float2(qa[h].x, qa[h].y), make_float2(ka.x, ka.y), make_float2(0.f, 0.f));
+            acc = ffma2(make_float2(qa[h].z, qa[h].w), make_float2(ka.z, ka.w), acc);
+            acc = ffma2(make_float2(qb[h].x, qb[h].y), make_float2(kb.x, kb.y), acc);
+            acc = ffma2(make_float2(qb[h].z, qb[h].w), make_float2(kb.z, kb.w), acc);
+            v[h] = acc.x + acc.y;
+        }
+    }
+#pragma unroll
+    for (int w = NV / 2, bit = 4; w >= 1; w >>= 1, bit >>= 1) {
+        const bool up = lane & bit;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const float send = up ? v[i] : v[i + w];
+            const float keep = up ? v[i + w] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+        }
+    }
+#pragma unroll
+    for (int bit = RB / 2; bit >= 1; bit >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], bit);
+    if ((lane & (RB - 1)) == 0 && hown < QPG && valid) Sw[hown * SST + t] = v[0] * scale;
+}
+
+// scores of rows [r0, r0 + 4 NG): 8 lanes per row, 4 rows per warp load (4 x 128
+// contiguous bytes); rows at or beyond nt are masked when PRED.
+template <int QPG, int NG, bool PRED>
+__device__ __forceinline__ void score_rows(const float* tk, int r0, int nt, const float4 (&qa)[QPG],
+                                           const float4 (&qb)[QPG], float* Sw, int lane, float scale) {
+    const int rl = lane & 7, rg = lane >> 3;
     float4 ka[NG], kb[NG];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
@@ -250,32 +308,8 @@ __device__ __forceinline__ void score_rows(const float* tk, int r0, int nt, cons
     }
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-        float v[NV];
-#pragma unroll
-        for (int h = 0; h < NV; ++h) {
-            v[h] = 0.f;
-            if (h < QPG) {
-                float2 acc = ffma2(make_float2(qa[h].x, qa[h].y), make_float2(ka[j].x, ka[j].y), make_float2(0.f, 0.f));
-                acc = ffma2(make_float2(qa[h].z, qa[h].w), make_float2(ka[j].z, ka[j].w), acc);
-                acc = ffma2(make_float2(qb[h].x, qb[h].y), make_float2(kb[j].x, kb[j].y), acc);
-                acc = ffma2(make_float2(qb[h].z, qb[h].w), make_float2(kb[j].z, kb[j].w), acc);
-                v[h] = acc.x + acc.y;
-            }
-        }
-#pragma unroll
-        for (int w = NV / 2, bit = 4; w >= 1; w >>= 1, bit >>= 1) {
-            const bool up = lane & bit;
-#pragma unroll
-            for (int i = 0; i < w; ++i) {
-                const float send = up ? v[i] : v[i + w];
-                const float keep = up ? v[i + w] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
-            }
-        }
-#pragma unroll
-        for (int bit = RB / 2; bit >= 1; bit >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], bit);
         const int t = r0 + 4 * j + rg;
-        if ((lane & (RB - 1)) == 0 && hown < QPG && (!PRED || t < nt)) Sw[hown * SST + t] = v[0] * scale;
+        score_group<QPG>(ka[j], kb[j], t, !PRED || t < nt, qa, qb, Sw, lane, scale);
     }
 }
 
@@ -315,13 +349,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     unsigned char* Vl = smem + lay.vl;
     unsigned char* Qh = smem + lay.qo;
     unsigned char* Ql = smem + lay.qo + (size_t)TM * TD * 2;
-    float* Op = reinterpret_cast<float*>(smem + lay.qo);
-    unsigned char* Ph = smem + lay.ph;
-    unsigned char* Pl = smem + lay.pl;
+    float* Op = reinterpret_cast<float*>(smem + lay.op);
     float* Mp = reinterpret_cast<float*>(smem + lay.mp);
     float* Lp = reinterpret_cast<float*>(smem + lay.lp);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     uint32_t* tbase_s = reinterpret_cast<uint32_t*>(smem + lay.tbase);
+    volatile int* epi_done = reinterpret_cast<volatile int*>(smem + lay.tbase + 8);  // epilogues completed
 
     const int lh = blockIdx.x;
     const int l = lh / b.n_kv, g = lh % b.n_kv;
@@ -332,14 +365,16 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
 
     // ---- one-time: TMEM (S: NS cols, O: 64 cols), mbarriers, K_syn / V_syn^T ----
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tbase_s)), "r"(256));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tbase_s)), "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar[1])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mbar[2])), "r"(PWARPS));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mbar[3])), "r"(PWARPS));
         asm volatile("fence.mbarrier_init.release.cluster;");
+        *epi_done = 0;
     }
     {
         const float* sk = b.syn_keys + (size_t)lh * ks * TD;
@@ -384,56 +419,48 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0) TC_TRACE(1000);
-    const uint32_t tS = *tbase_s, tO = tS + (uint32_t)NS;
+    // TMEM columns: S [0, NS), O [NS, NS + 64), P hi [256, 256 + NS/2), P lo [256 + NS/2, 256 + NS)
+    const uint32_t tS = *tbase_s, tO = tS + (uint32_t)NS, tPh = tS + 256u, tPl = tPh + (uint32_t)(NS / 2);
     const int n_tiles = (b.n_agents + AT - 1) / AT;
-    uint32_t tpar = 0;  // mbar[0] completes once per tile (score MMAs)
+    uint32_t tpar = 0;  // tile parity: mbar[0] / mbar[2] phases, double-buffered O_priv / (m, l)
 
     if (warp < SWARPS) {
         // ======================= synapse warps =======================
         const uint32_t idS = idesc_bf16_f32(TM, NS), idO = idesc_bf16_f32(TM, TD);
         const uint32_t trow = tS + ((uint32_t)(warp * 32) << 16);
+        const uint32_t trow_ph = tPh + ((uint32_t)(warp * 32) << 16), trow_pl = tPl + ((uint32_t)(warp * 32) << 16);
         const int r_own = warp * 32 + lane;
         uint32_t ph1 = 0;
-        int ti = 0;
-        for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
-            if (tid == 0) TC_TRACE(ti * 16 + 0);
-            const int a0 = tile * AT;
-            const int rows = min(AT, b.n_agents - a0) * QPG;
-            if (skip & 1) {  // debugging only (CX_TC_SKIP): keep the hand-off protocol, skip the math
-                if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[0])) : "memory");
-                mbar_wait_parity(&mbar[0], tpar);
-                mbar_wait_sleep(&mbar[2], tpar);
-                bar_sync(1, SWARPS * 32);
-                tpar ^= 1u;
-                continue;
+        // Q tile -> bf16 hi/lo; lane -> (row rb + lane%8, chunk cb + lane/8): 4 lanes read
+        // 128 contiguous bytes of a row, 8 lanes store 128 contiguous bytes
+        auto stage_q = [&](int tile_q) {
+            const int a0q = tile_q * AT;
+            const int rows_q = min(AT, b.n_agents - a0q) * QPG;
+            float4 xa[8], xb[8];
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
+                xa[it] = xb[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r < rows_q) {
+                    const int a = a0q + r / QPG, hh = r % QPG;
+                    const float4* src = reinterpret_cast<const float4*>(
+                        b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD + 8 * c);
+                    xa[it] = __ldg(src);
+                    xb[it] = __ldg(src + 1);
+                }
             }
-            // 1. Q tile -> bf16 hi/lo; lane -> (row rb + lane%8, chunk cb + lane/8):
-            //    4 lanes read 128 contiguous bytes of a row, 8 lanes store 128 contiguous bytes
-            {
-                float4 xa[8], xb[8];
 #pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
-                    xa[it] = xb[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (r < rows) {
-                        const int a = a0 + r / QPG, hh = r % QPG;
-                        const float4* src = reinterpret_cast<const float4*>(
-                            b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD + 8 * c);
-                        xa[it] = __ldg(src);
-                        xb[it] = __ldg(src + 1);
-                    }
-                }
-#pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
-                    const float x[8] = {xa[it].x, xa[it].y, xa[it].z, xa[it].w, xb[it].x, xb[it].y, xb[it].z, xb[it].w};
-                    split8_store(x, Qh, Ql, cm_off(r, 8 * c, TM));
-                }
+            for (int it = 0; it < 8; ++it) {
+                const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
+                const float x[8] = {xa[it].x, xa[it].y, xa[it].z, xa[it].w, xb[it].x, xb[it].y, xb[it].z, xb[it].w};
+                split8_store(x, Qh, Ql, cm_off(r, 8 * c, TM));
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             bar_sync(1, SWARPS * 32);
-            if (tid == 0) TC_TRACE(ti * 16 + 1);
-            // 2. S = Q K^T on the tensor cores (3 MMAs per 16-wide k-step)
+        };
+        // S = Q K^T on the tensor cores (3 MMAs per 16-wide k-step), completion on mbar[0]
+        auto issue_s = [&]() {
             if (tid == 0) {
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t qlbo = (TM / 8) * 128, klbo = (uint32_t)(NS / 8) * 128;
@@ -448,10 +475,29 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 }
                 mma_commit(&mbar[0]);
             }
-            mbar_wait_parity(&mbar[0], tpar);
+        };
+        // the first tile's scores are issued before the loop; tile i+1's while tile i's P.V runs
+        if (!(skip & 1) && (int)blockIdx.y < n_tiles) {
+            stage_q(blockIdx.y);
+            issue_s();
+        }
+        int ti = 0;
+        for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
+            if (tid == 0) TC_TRACE(ti * 16 + 0);
+            const int a0 = tile * AT;
+            const int rows = min(AT, b.n_agents - a0) * QPG;
+            const int next = tile + (int)gridDim.y;
+            if (skip & 1) {  // debugging only (CX_TC_SKIP): keep the hand-off protocol, skip the math
+                mbar_wait_sleep(&mbar[2 + tpar], (uint32_t)(ti >> 1) & 1u);
+                bar_sync(1, SWARPS * 32);
+                if (tid == 0) *epi_done = ti + 1;
+                tpar ^= 1u;
+                continue;
+            }
+            mbar_wait_parity(&mbar[0], tpar);  // S of this tile (issued one tile ahead)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (tid == 0) TC_TRACE(ti * 16 + 2);
-            // 3. softmax over the synapse keys, thread per row
+            // softmax over the synapse keys, thread per row
             const bool live = r_own < rows;
             float mx = -INFINITY, l_s = 0.f;
             for (int c0 = 0; c0 < NS; c0 += 16) {
@@ -470,49 +516,64 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             const float c2 = scale * 1.4426950408889634f;   // e^{(s - mx) scale} = 2^{s c2 - mx c2}
             const float m2 = live ? mx * c2 : INFINITY;     // padding rows: all weights 0
             if (tid == 0) TC_TRACE(ti * 16 + 3);
-            for (int k0 = 0; k0 < NS; k0 += TPCH) {
-                const int kn = min(TPCH, NS - k0);
-                for (int c0 = 0; c0 < kn; c0 += 16) {
-                    float v[16];
-                    tmem_ld16(trow + (uint32_t)(k0 + c0), v);
-                    float p[16];
-                    if (k0 + c0 + 16 <= ks) {
+            // unnormalised P -> TMEM as packed bf16x2 hi / lo (row = lane, 2 keys per column):
+            // the A operand of O = P V_syn, so no shared-memory round trip and one MMA pass
+            for (int c0 = 0; c0 < NS; c0 += 16) {
+                float v[16];
+                tmem_ld16(trow + (uint32_t)c0, v);
+                float p[16];
+                if (c0 + 16 <= ks) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) p[j] = ex2(fmaf(v[j], c2, -m2));
-                    } else {
+                    for (int j = 0; j < 16; ++j) p[j] = ex2(fmaf(v[j], c2, -m2));
+                } else {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) p[j] = k0 + c0 + j < ks ? ex2(fmaf(v[j], c2, -m2)) : 0.f;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) l_s += p[j];
-                    split8_store(p, Ph, Pl, cm_off(r_own, c0, TM));
-                    split8_store(p + 8, Ph, Pl, cm_off(r_own, c0 + 8, TM));
+                    for (int j = 0; j < 16; ++j) p[j] = c0 + j < ks ? ex2(fmaf(v[j], c2, -m2)) : 0.f;
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                bar_sync(1, SWARPS * 32);
-                if (tid == 0) {
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t plbo = (TM / 8) * 128, vlbo = (TD / 8) * 128;
-                    for (int kk = 0; kk < kn / 16; ++kk) {
-                        const uint32_t po = kk * 2 * plbo, vo = ((k0 >> 3) + kk * 2) * vlbo;
-                        const uint64_t ph = sdesc(su32(Ph) + po, plbo, 128), pl = sdesc(su32(Pl) + po, plbo, 128);
-                        const uint64_t vh = sdesc(su32(Vh) + vo, vlbo, 128), vl = sdesc(su32(Vl) + vo, vlbo, 128);
-                        mma_bf16(tO, pl, vh, idO, (k0 > 0 || kk > 0) ? 1u : 0u);
-                        mma_bf16(tO, ph, vl, idO, 1u);
-                        mma_bf16(tO, ph, vh, idO, 1u);
-                    }
-                    mma_commit(&mbar[1]);
+                uint32_t hv[8], lv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    l_s += p[2 * u] + p[2 * u + 1];
+                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(p[2 * u], p[2 * u + 1]);
+                    const float2 hf = __bfloat1622float2(h2);
+                    const __nv_bfloat162 l2 = __floats2bfloat162_rn(p[2 * u] - hf.x, p[2 * u + 1] - hf.y);
+                    hv[u] = *reinterpret_cast<const uint32_t*>(&h2);
+                    lv[u] = *reinterpret_cast<const uint32_t*>(&l2);
                 }
-                mbar_wait_parity(&mbar[1], ph1);  // P chunk consumed (and O complete after the last)
-                ph1 ^= 1u;
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                tmem_st8(trow_ph + (uint32_t)(c0 / 2), hv);
+                tmem_st8(trow_pl + (uint32_t)(c0 / 2), lv);
             }
-            // 5. epilogue: wait for the private partials, merge, store
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            bar_sync(1, SWARPS * 32);  // S of this tile fully read; P in TMEM
+            if (tid == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t vlbo = (TD / 8) * 128;
+                for (int kk = 0; kk < NS / 16; ++kk) {
+                    const uint32_t vo = kk * 2 * vlbo;
+                    const uint64_t vh = sdesc(su32(Vh) + vo, vlbo, 128), vl = sdesc(su32(Vl) + vo, vlbo, 128);
+                    mma_bf16_ts(tO, tPl + (uint32_t)(kk * 8), vh, idO, kk > 0 ? 1u : 0u);
+                    mma_bf16_ts(tO, tPh + (uint32_t)(kk * 8), vl, idO, 1u);
+                    mma_bf16_ts(tO, tPh + (uint32_t)(kk * 8), vh, idO, 1u);
+                }
+                mma_commit(&mbar[1]);
+            }
+            // next tile: its Q (the score MMAs of this tile are done with the buffer) and S
+            // (this tile's S is dead) while this tile's P.V runs
+            if (next < n_tiles) {
+                stage_q(next);
+                issue_s();
+            }
+            mbar_wait_parity(&mbar[1], ph1);  // O = P V_syn complete
+            ph1 ^= 1u;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // epilogue: wait for the private partials, merge, store
             if (tid == 0) TC_TRACE(ti * 16 + 4);
-            mbar_wait_sleep(&mbar[2], tpar);  // every private warp has published this tile
+            // every private warp has published this tile.  Private warps may run one tile
+            // ahead, so even / odd tiles use separate barriers (no parity aliasing)
+            mbar_wait_sleep(&mbar[2 + tpar], (uint32_t)(ti >> 1) & 1u);
             if (tid == 0) TC_TRACE(ti * 16 + 5);
             {
+                const float* Opt = Op + (size_t)tpar * TM * OPS;
                 float v[TD];
                 const uint32_t trow_o = tO + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
@@ -525,19 +586,23 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     const float inv = 1.0f / (l_s * as + l_p * ap);
                     const float cs = as * inv, cp = ap * inv;
                     float* out = b.out + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD;
-                    const float4* op = reinterpret_cast<const float4*>(Op + r_own * OPS);
+                    const float4* op = reinterpret_cast<const float4*>(Opt + r_own * OPS);
 #pragma unroll
                     for (int c4 = 0; c4 < TD / 4; ++c4) {
-                        const float4 p = op[c4];
+                        const float4 pp = op[c4];
                         reinterpret_cast<float4*>(out)[c4] =
-                            make_float4(v[4 * c4] * cs + p.x * cp, v[4 * c4 + 1] * cs + p.y * cp,
-                                        v[4 * c4 + 2] * cs + p.z * cp, v[4 * c4 + 3] * cs + p.w * cp);
+                            make_float4(v[4 * c4] * cs + pp.x * cp, v[4 * c4 + 1] * cs + pp.y * cp,
+                                        v[4 * c4 + 2] * cs + pp.z * cp, v[4 * c4 + 3] * cs + pp.w * cp);
                     }
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            bar_sync(1, SWARPS * 32);  // Op / TMEM reuse by the next tile
-            if (tid == 0) TC_TRACE(ti * 16 + 6);
+            bar_sync(1, SWARPS * 32);  // O / this tile's O_priv buffer fully read
+            if (tid == 0) {
+                __threadfence_block();
+                *epi_done = ti + 1;    // private warps may now overwrite this parity's buffers
+                TC_TRACE(ti * 16 + 6);
+            }
             tpar ^= 1u;
         }
     } else {
@@ -551,12 +616,11 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             const int na = min(AT, b.n_agents - a0);
             bool published = false;
             if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + 8);
-            for (int ai = pw; ai < na; ai += PWARPS) {
-                if (skip & 2) {  // debugging only (CX_TC_SKIP)
-                    if (!published) mbar_wait_sleep(&mbar[0], tpar);
-                    published = true;
-                    continue;
-                }
+            // agents are dealt round-robin over the CTA's whole agent sequence, not per
+            // tile: with 18 agents per tile and 12 warps no warp takes 2 every tile
+            const int first = (pw - (ti * AT) % PWARPS + PWARPS) % PWARPS;
+            for (int ai = first; ai < na; ai += PWARPS) {
+                if (skip & 2) continue;  // debugging only (CX_TC_SKIP)
                 const int a = a0 + ai;
                 const int len = min(b.tail_len[a], b.t_cap - (app ? 1 : 0));
                 const int nt = len + (app ? 1 : 0);
@@ -565,26 +629,55 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 const float* tk = b.tail_keys + toff;
                 const float* tv = b.tail_values + toff;
                 const float* qrow = b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG) * TD;
-                if (app && lane < 16) {  // append the new row (fused); read back below like any other row
-                    reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[lane] =
-                        __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + lane);
-                    reinterpret_cast<float4*>(b.tail_values + toff + (size_t)len * TD)[lane] =
-                        __ldg(reinterpret_cast<const float4*>(b.new_values + noff) + lane);
+                if (lane == 0 && PREFETCH_NEXT) {  // this warp's next agent -> L2, one agent ahead
+                    int na_t = ai + PWARPS, nt_tile = tile;
+                    if (na_t >= na) {
+                        na_t = (pw - ((ti + 1) * AT) % PWARPS + PWARPS) % PWARPS;
+                        nt_tile = tile + (int)gridDim.y;
+                    }
+                    const int an = nt_tile * AT + na_t;
+                    if (nt_tile < n_tiles && an < b.n_agents && na_t < AT) {
+                        const size_t off = ((((size_t)an * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
+                        const uint32_t bytes = (uint32_t)min(b.tail_len[an] + (app ? 1 : 0), b.t_cap) * TD * 4;
+                        if (bytes) {
+                            l2_prefetch(b.tail_keys + off, bytes);
+                            l2_prefetch(b.tail_values + off, bytes);
+                        }
+                    }
                 }
+                // q, the new token's K/V row (it is row `len`) and the first K batch are all in
+                // flight together; the new row is used from registers and appended (fused).
                 float4 qa[QPG], qb[QPG];
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) {
                     qa[h] = __ldg(reinterpret_cast<const float4*>(qrow + (size_t)h * TD) + (lane & 7));
                     qb[h] = __ldg(reinterpret_cast<const float4*>(qrow + (size_t)h * TD) + 8 + (lane & 7));
                 }
-                // The warp barrier orders the appended row before the warp's own reads of it.
-                __syncwarp();
-                // ---- scores: 16-row batches, then 4-row groups ----
+                float4 nka = make_float4(0.f, 0.f, 0.f, 0.f), nkb = nka;
+                float2 nvv = make_float2(0.f, 0.f);
+                if (app) {
+                    nka = __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + (lane & 7));
+                    nkb = __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + 8 + (lane & 7));
+                    nvv = __ldg(reinterpret_cast<const float2*>(b.new_values + noff) + lane);
+                    if (lane < 8) {
+                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[lane] = nka;
+                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[8 + lane] = nkb;
+                    }
+                    reinterpret_cast<float2*>(b.tail_values + toff + (size_t)len * TD)[lane] = nvv;
+                }
+                // ---- scores of the stored rows [0, len): 16-row batches, then 4-row groups ----
                 int r0 = 0;
-                for (; r0 + 16 <= nt; r0 += 16) score_rows<QPG, 4, false>(tk, r0, nt, qa, qb, Sw, lane, scale);
-                for (; r0 < nt; r0 += 4) score_rows<QPG, 1, true>(tk, r0, nt, qa, qb, Sw, lane, scale);
-                if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == 0 ? 9 : 12));
+                for (; r0 + 16 <= len; r0 += 16) score_rows<QPG, 4, false>(tk, r0, len, qa, qb, Sw, lane, scale);
+                for (; r0 < len; r0 += 4) score_rows<QPG, 1, true>(tk, r0, len, qa, qb, Sw, lane, scale);
+                if (app) score_group<QPG>(nka, nkb, len, lane < 8, qa, qb, Sw, lane, scale);
+                if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == first ? 9 : 12));
                 __syncwarp();
+                // this tile's (Mp, Lp, O_priv) buffers were last read by the epilogue two
+                // tiles back: wait for it before the first write of the tile
+                if (!published) {
+                    wait_epilogues(epi_done, ti - 1);
+                    published = true;
+                }
                 // softmax per q-head over the private rows (weights 0 up to TTAIL)
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) {
@@ -607,34 +700,36 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) o[h] = make_float2(0.f, 0.f);
                 r0 = 0;
-                for (; r0 + 16 <= nt; r0 += 16) mix_rows<QPG, 16, false>(tv, r0, nt, Sw, o, lane);
-                for (; r0 < nt; r0 += 4) mix_rows<QPG, 4, true>(tv, r0, nt, Sw, o, lane);
-                if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == 0 ? 10 : 13));
-                // publish into the (dead) Q tile once this tile's score MMAs are complete
-                if (!published) {
-                    mbar_wait_sleep(&mbar[0], tpar);
-                    published = true;
-                }
+                for (; r0 + 16 <= len; r0 += 16) mix_rows<QPG, 16, false>(tv, r0, len, Sw, o, lane);
+                for (; r0 < len; r0 += 4) mix_rows<QPG, 4, true>(tv, r0, len, Sw, o, lane);
+                if (app)
+#pragma unroll
+                    for (int h = 0; h < QPG; ++h) {
+                        const float p = Sw[h * SST + len];
+                        o[h].x = fmaf(p, nvv.x, o[h].x);
+                        o[h].y = fmaf(p, nvv.y, o[h].y);
+                    }
+                if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == first ? 10 : 13));
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) {
                     const int r = ai * QPG + h;
-                    reinterpret_cast<float2*>(Op + r * OPS)[lane] = o[h];
+                    reinterpret_cast<float2*>(Op + ((size_t)tpar * TM + r) * OPS)[lane] = o[h];
                 }
                 __syncwarp();  // Sw reuse
             }
-            // Arrive only after this tile's score phase, even with no agents: a warp
-            // must never arrive for tile i+1 before barrier 2 of tile i has completed.
-            if (!published) mbar_wait_sleep(&mbar[0], tpar);
+            // Arrive only once the epilogue two tiles back is done, even with no agents: the
+            // barrier of this tile's parity then never runs a phase ahead of the synapse warps.
+            if (!published) wait_epilogues(epi_done, ti - 1);
             if (lane == 0 && pw == 0) TC_TRACE(ti * 16 + 11);
             if (lane == 0 && pw == PWARPS - 1) TC_TRACE(ti * 16 + 14);
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[2])) : "memory");
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[2 + tpar])) : "memory");
             tpar ^= 1u;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tbase_s), "r"(256));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tbase_s), "r"(512));
 }
 
 }  // namespace

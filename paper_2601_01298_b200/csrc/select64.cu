@@ -619,6 +619,14 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
             break;
         }
     }
+    if (const char* force = getenv("CX_SEL_C")) {  // debugging / tuning: force a cluster size
+        const int c = atoi(force);
+        const int s_ = (int)((g.L + c - 1) / c);
+        const int rs = std::max(0, s_ - NT);
+        if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT && sel64_layout(rs, true).total <= budget) {
+            C = c; S = s_; Rs = rs;
+        }
+    }
     if (C == 0) {  // too large for one cluster on chip: rows beyond 512 stay in L2
         C = MAXC;
         S = (int)((g.L + C - 1) / C);
@@ -665,6 +673,11 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (getenv("CX_SEL_OCC")) {  // debugging: co-resident clusters for this configuration
+        int ncl = 0;
+        cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+        fprintf(stderr, "select64: C=%d S=%d Rs=%d smem=%zu max active clusters=%d groups=%d\n", C, S, Rs, smem, ncl, g.G);
+    }
     CX_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
     count_launch();
     const char* dump = getenv("CX_SEL_DUMP");
