@@ -296,6 +296,8 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
     achieved = bytes_per_launch / (sel_ms * 1e-3) / 1e9
     dec = run_decode(args, dev, rank, world)
     e2e = run_e2e(args, dev) if rank == 0 else None
+    cfg5 = run_cfg5(args, dev) if rank == 0 else None
+    cfg4 = run_cfg4(args, dev, rank, world)
     line = {
         "metric": METRIC, "value": value, "unit": "compressions/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -318,6 +320,9 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
         line["decode"] = dec
     if e2e is not None:
         line["e2e"] = e2e
+    if cfg5 is not None:
+        line["cfg5"] = cfg5
+    line["cfg4"] = cfg4
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         try:
@@ -399,6 +404,157 @@ def run_decode(args, dev, rank=0, world=1):
                                            "frac": b / (ms * 1e-3) / 1e9 / hbm, "bytes": b,
                                            "traffic": ncu_traffic("decode_tc_kernel") if n == 1000 else None}}
     return out
+
+
+def run_cfg5(args, dev, tokens=600, n_agents=100, inj_every=10, push_every=10, t_inj=16):
+    """BASELINE configs[4]: River + 100 Stream agents, Referential Injection every
+    10 tokens, River and Stream work on priority CUDA streams.
+
+    River lane (highest priority): every `inj_every` agent tokens, inject a
+    16-token thought block into the river's device KvCache (cx_inject_dev,
+    injector.cpp:136-160); every `push_every` tokens, if the previous push has
+    landed, re-compress the river's L=8192 context rows (48 (layer, KV-head)
+    groups, k=164) into the back synapse buffer -- the push (scheduler.cpp:
+    158-165).  Stream lane (medium priority): N agents x 24 layers decode one
+    token per step against the FRONT synapse (append + attend, decode_tc).  A
+    push is published to the agents when its CUDA event has completed (a
+    non-blocking query: SynapseBuffer::read_latest semantics, synapse.hpp:
+    115-135); the agent lane then waits on that event.  The host stays at most
+    `inj_every` tokens ahead of the agent lane, so "landed" is judged at device
+    time, not at launch time.
+    River forward_step / encode_thought (the projections) are out of scope
+    (SURVEY.md §8(f) row 1): the river work is its injections and pushes."""
+    import torch
+
+    from paper_2601_01298_b200 import device as cxd
+    from paper_2601_01298_b200.injector import inject_dev
+    from paper_2601_01298_b200.model import KvCache, ModelConfig
+    river_lane, agent_lane = cxd.lane_stream("river"), cxd.lane_stream("stream")
+    dm = N_KV * D
+    n_inj = tokens // inj_every + 1
+    cfg = ModelConfig(n_layers=N_LAYERS, n_heads=N_KV, d_model=dm, d_k=D, max_positions=L + 4096 + n_inj * t_inj)
+    river = KvCache(cfg, capacity=L + n_inj * t_inj + 16)  # pre-sized: views stay valid
+    gen = torch.Generator(device=dev).manual_seed(5)
+    qpg = N_Q // N_KV
+    with torch.cuda.stream(river_lane):
+        pre_k = torch.randn(N_LAYERS, L, dm, device=dev, generator=gen)
+        pre_v = torch.randn(N_LAYERS, L, dm, device=dev, generator=gen)
+        river.append_context_dev(pre_k.data_ptr(), pre_v.data_ptr(), 0, L, river_lane.cuda_stream)
+        th_k = torch.randn(N_LAYERS, t_inj, dm, device=dev, generator=gen)
+        th_v = torch.randn(N_LAYERS, t_inj, dm, device=dev, generator=gen)
+        rq = [torch.randn(N_LAYERS, qpg, D, device=dev, generator=gen) for _ in range(N_KV)]
+        heads = [(cxd.kvcache_head_view(river, h, L), cxd.kvcache_head_view(river, h, L, values=True))
+                 for h in range(N_KV)]
+        syn = torch.empty(2, 2, N_LAYERS, N_KV, K, D, device=dev)  # [buffer][K|V][layer][kv][k][d]
+        outs = [(torch.empty(N_LAYERS, K, dtype=torch.int64, device=dev),
+                 torch.empty(N_LAYERS, K, dtype=torch.float64, device=dev),
+                 torch.empty(N_LAYERS, K, D, device=dev), torch.empty(N_LAYERS, K, D, device=dev))
+                for _ in range(N_KV)]
+
+    def push(buf):  # river lane: one synapse compression of all 48 groups into syn[buf]
+        for h in range(N_KV):
+            kh, vh = heads[h]
+            cxd.compress_grouped(kh, vh, rq[h], K, LAM, out=outs[h])
+            syn[buf, 0, :, h].copy_(outs[h][2])
+            syn[buf, 1, :, h].copy_(outs[h][3])
+
+    with torch.cuda.stream(river_lane):
+        push(0)
+    torch.cuda.synchronize()
+    gen2 = torch.Generator(device=dev).manual_seed(6)
+    tk = torch.randn(n_agents, N_LAYERS, N_KV, T_PRIV + 1, D, device=dev, generator=gen2)
+    tv = torch.randn_like(tk)
+    tl = torch.full((n_agents,), T_PRIV, dtype=torch.int32, device=dev)
+    nk = torch.randn(n_agents, N_LAYERS, N_KV, D, device=dev, generator=gen2)
+    nv = torch.randn_like(nk)
+    q = torch.randn(n_agents, N_LAYERS, N_Q, D, device=dev, generator=gen2)
+    o = torch.empty_like(q)
+    front, inflight, pushes, injections = 0, None, 0, 0
+    push_ms, vbase = [], L + 1024
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev0.record(agent_lane)
+    river_lane.wait_event(ev0)
+    tok_ev = []
+    for t in range(tokens):
+        if t >= inj_every:
+            tok_ev[t - inj_every].synchronize()
+        if inflight is not None and inflight[0].query():  # the push landed: publish it
+            agent_lane.wait_event(inflight[0])
+            front = inflight[1]
+            push_ms.append(inflight[2].elapsed_time(inflight[0]))
+            pushes += 1
+            inflight = None
+        if t % inj_every == 0:
+            with torch.cuda.stream(river_lane):
+                inject_dev(river, th_k.data_ptr(), th_v.data_ptr(), vbase + injections * t_inj, t_inj, N_LAYERS, dm,
+                           injections, t, river_lane.cuda_stream)
+            injections += 1
+        if t % push_every == 0 and inflight is None:
+            with torch.cuda.stream(river_lane):
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(river_lane)
+                push(1 - front)
+                s1.record(river_lane)
+            inflight = (s1, 1 - front, s0)
+        with torch.cuda.stream(agent_lane):
+            cxd.decode_step(syn[front, 0], syn[front, 1], tk, tv, tl, q, o, nk, nv)
+        ev = torch.cuda.Event()
+        ev.record(agent_lane)
+        tok_ev.append(ev)
+    e_ag, e_rv = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_ag.record(agent_lane)
+    e_rv.record(river_lane)
+    torch.cuda.synchronize()
+    if inflight is not None:
+        push_ms.append(inflight[2].elapsed_time(inflight[0]))
+        pushes += 1
+    ag_ms = ev0.elapsed_time(e_ag)
+    return {"workload": f"cfg5 (BASELINE configs[4]): river KvCache L={L} context rows, {n_agents} stream agents x "
+                        f"{tokens} tokens, injection of {t_inj} tokens every {inj_every}, synapse push every "
+                        f"{push_every} tokens when the previous one has landed",
+            "agent_steps_per_s": n_agents * tokens / (ag_ms * 1e-3), "agent_ms": ag_ms,
+            "river_ms": ev0.elapsed_time(e_rv), "pushes": pushes, "injections": injections,
+            "push_ms_mean": statistics.mean(push_ms) if push_ms else None,
+            "lanes": {"river_priority": river_lane.cx_priority, "stream_priority": agent_lane.cx_priority},
+            "river_entries": river.size(), "river_context_count": river.context_count()}
+
+
+def run_cfg4(args, dev, rank=0, world=1, steps=3):
+    """BASELINE configs[3]: long context L=32768 -> k=656 (98%), 48 groups sharded
+    by (layer, head) over the ranks, synapse all-gathered (NCCL) when N > 1."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_01298_b200 import device as cxd
+    from paper_2601_01298_b200.parallel import all_gather_groups, shard_range
+    l4, k4 = 32768, 656
+    gb, ge = shard_range(G, rank, world)
+    gen = torch.Generator(device=dev).manual_seed(77 + rank)
+    keys = torch.randn(ge - gb, l4, D, device=dev, generator=gen)
+    values = torch.randn(ge - gb, l4, D, device=dev, generator=gen)
+    queries = torch.randn(ge - gb, N_Q // N_KV, D, device=dev, generator=gen)
+    out = (torch.empty(ge - gb, k4, dtype=torch.int64, device=dev), torch.empty(ge - gb, k4, dtype=torch.float64, device=dev),
+           torch.empty(ge - gb, k4, D, device=dev), torch.empty(ge - gb, k4, D, device=dev))
+    cxd.compress_grouped(keys, values, queries, k4, LAM, out=out)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cxd.compress_grouped(keys, values, queries, k4, LAM, out=out)
+        if world > 1:
+            all_gather_groups(list(out), G)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    del keys, values
+    return {"workload": "cfg4 (BASELINE configs[3]): 48 groups, L=32768 -> k=656, lambda=0.5",
+            "compressions_per_s": 1000.0 / ms, "ms_per_step": ms, "groups_per_gpu": ge - gb}
 
 
 def run_e2e(args, dev):

@@ -101,6 +101,13 @@ typedef struct cx_ctx cx_ctx; /* device workspace + default stream; one per host
 cx_status cx_ctx_create(int device, cx_ctx** out);
 cx_status cx_ctx_destroy(cx_ctx* ctx);
 
+/* Priority lanes (SURVEY.md §8(b) threading row): the River's
+ * work (injection appends, synapse pushes) goes on the highest-priority stream,
+ * Stream agents' decode on a medium-priority one.  Replaces the reference's
+ * river thread / per-agent std::threads (scheduler.cpp:63-113, 198). */
+typedef enum cx_lane { CX_LANE_RIVER = 0, CX_LANE_STREAM = 1 } cx_lane;
+cx_status cx_ctx_lane_stream(cx_ctx* ctx, int lane, void** stream, int* priority);
+
 /* A batch of G independent selection groups.  Group g's cloud row i, column c
  * is clouds[g * group_stride + i * row_stride + c] (fp32, device).  Queries:
  * queries[(g * n_pass + p) * d_k + c].  Pass p scores columns
@@ -194,6 +201,12 @@ cx_status cx_kvcache_write_layer(cx_kvcache* c, int layer, const float* key, con
 cx_status cx_kvcache_end_entry(cx_kvcache* c);                                        /* model.cpp:154-159 */
 cx_status cx_kvcache_append_entry(cx_kvcache* c, int64_t position, cx_origin origin,
                                   const float* keys, const float* values);            /* model.cpp:161-173 */
+/* Bulk device append of `count` context entries at positions base..base+count-1
+ * from a device block [n_layers][count][d_model] (a river prefill), stream-ordered.
+ * Same per-entry checks and partial-append behaviour as count append_entry calls
+ * (model.cpp:124-173): entries before the first failing one stay appended. */
+cx_status cx_kvcache_append_context_dev(cx_kvcache* c, const float* keys, const float* values,
+                                        int64_t base_position, int64_t count, void* stream);
 /* copy rows [first, first+n) of one layer to host */
 cx_status cx_kvcache_read(const cx_kvcache* c, int layer, int64_t first, int64_t n,
                           float* keys_out, float* values_out);

@@ -76,6 +76,7 @@ _SIGS = [
     ("cx_attend", C.c_int, [c_f32p, c_f32p, c_f32p, C.c_int64, C.c_int, C.c_int, c_f32p]),
     ("cx_ctx_create", C.c_int, [C.c_int, C.POINTER(c_vp)]),
     ("cx_ctx_destroy", C.c_int, [c_vp]),
+    ("cx_ctx_lane_stream", C.c_int, [c_vp, C.c_int, C.POINTER(c_vp), C.POINTER(C.c_int)]),
     ("cx_attention_grouped_dev", C.c_int, [c_vp, C.POINTER(CxGroups), c_vp, c_vp]),
     ("cx_select_grouped_dev", C.c_int,
      [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp]),
@@ -99,6 +100,7 @@ _SIGS = [
     ("cx_kvcache_end_entry", C.c_int, [c_vp]),
     ("cx_kvcache_append_entry", C.c_int, [c_vp, C.c_int64, C.c_int, c_f32p, c_f32p]),
     ("cx_kvcache_read", C.c_int, [c_vp, C.c_int, C.c_int64, C.c_int64, c_f32p, c_f32p]),
+    ("cx_kvcache_append_context_dev", C.c_int, [c_vp, c_vp, c_vp, C.c_int64, C.c_int64, c_vp]),
     ("cx_inject_host", C.c_int,
      [c_vp, c_f32p, c_f32p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_int64,
       C.POINTER(CxInjectionRecord)]),

@@ -36,6 +36,11 @@ void ctx_init(cx_ctx* c, int device) {
     CX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CX_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CX_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    // priority lanes: lo is the least urgent value, hi the most (numerically smaller)
+    c->lane_prio[CX_LANE_RIVER] = hi;
+    c->lane_prio[CX_LANE_STREAM] = (lo + hi) / 2 == hi && lo != hi ? hi + 1 : (lo + hi) / 2;
+    CX_CUDA(cudaStreamCreateWithPriority(&c->lane[CX_LANE_RIVER], cudaStreamNonBlocking, c->lane_prio[CX_LANE_RIVER]));
+    CX_CUDA(cudaStreamCreateWithPriority(&c->lane[CX_LANE_STREAM], cudaStreamNonBlocking, c->lane_prio[CX_LANE_STREAM]));
     CX_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CX_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
@@ -155,9 +160,22 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
         if (c->d_flag) cudaFree(c->d_flag);
         cudaEventDestroy(c->ev_fork);
         cudaEventDestroy(c->ev_join);
+        for (cudaStream_t& l : c->lane) {
+            cudaStreamSynchronize(l);
+            cudaStreamDestroy(l);
+        }
         cudaStreamDestroy(c->side);
         cudaStreamDestroy(c->stream);
         delete c;
+    });
+}
+
+extern "C" cx_status cx_ctx_lane_stream(cx_ctx* c, int lane, void** stream, int* priority) {
+    return guard([&] {
+        if (!c || !stream) fail(CX_INVALID_ARGUMENT, "null pointer");
+        if (lane != CX_LANE_RIVER && lane != CX_LANE_STREAM) fail(CX_INVALID_ARGUMENT, "unknown lane");
+        *stream = (void*)c->lane[lane];
+        if (priority) *priority = c->lane_prio[lane];
     });
 }
 
@@ -676,6 +694,64 @@ extern "C" cx_status cx_kvcache_append_entry(cx_kvcache* c, int64_t position, cx
         CX_CUDA(cudaStreamSynchronize(c->stream));
         c->layers_written = c->n_layers;
         c->entry_open = false;
+    });
+}
+
+extern "C" cx_status cx_kvcache_append_context_dev(cx_kvcache* c, const float* keys, const float* values,
+                                                    int64_t base_position, int64_t count, void* stream) {
+    return guard([&] {
+        if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
+        if (count < 0) fail(CX_INVALID_ARGUMENT, "negative count");
+        if (count == 0) return;
+        if (!keys || !values) fail(CX_INVALID_ARGUMENT, "null block");
+        // the checks begin_entry would make for each entry in turn (model.cpp:124-140)
+        cx_status err = CX_OK;
+        std::string msg;
+        int64_t n_ok = 0;
+        if (c->entry_open) {
+            err = CX_SEQUENCING_ERROR;
+            msg = "cache entry already open";
+        } else {
+            int64_t last = c->last_context_position;
+            for (; n_ok < count; ++n_ok) {
+                const int64_t p = base_position + n_ok;
+                if (p < 0 || p >= c->max_positions) {
+                    err = CX_CAPACITY_ERROR;
+                    msg = "position " + std::to_string(p) + " outside max_positions " + std::to_string(c->max_positions);
+                    break;
+                }
+                if (p <= last) {
+                    err = CX_PRECONDITION_ERROR;
+                    msg = "context positions must be strictly increasing";
+                    break;
+                }
+                last = p;
+            }
+        }
+        if (n_ok > 0) {
+            cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+            const int64_t row0 = (int64_t)c->positions.size();
+            kv_grow(c, row0 + n_ok);
+            if (s != c->stream) {  // order after the cache's own pending work (e.g. a regrow)
+                cudaEvent_t ev;
+                CX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CX_CUDA(cudaEventRecord(ev, c->stream));
+                CX_CUDA(cudaStreamWaitEvent(s, ev, 0));
+                cudaEventDestroy(ev);
+            }
+            for (int l = 0; l < c->n_layers; ++l)
+                kv_append_rows(c->keys + (size_t)l * c->capacity * c->d_model,
+                               c->values + (size_t)l * c->capacity * c->d_model, c->capacity, 1, c->d_model,
+                               keys + (size_t)l * count * c->d_model, values + (size_t)l * count * c->d_model, n_ok,
+                               row0, s);
+            for (int64_t t = 0; t < n_ok; ++t) {
+                c->positions.push_back(base_position + t);
+                c->origins.push_back((uint8_t)CX_ORIGIN_CONTEXT);
+            }
+            c->last_context_position = base_position + n_ok - 1;
+            c->context_count += n_ok;
+        }
+        if (err != CX_OK) fail(err, msg);
     });
 }
 

@@ -99,6 +99,8 @@ struct cx_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;  // used by the host-pointer (reference-shaped) calls
     cudaStream_t side = nullptr;    // fork target (centroid alongside attention)
+    cudaStream_t lane[2] = {nullptr, nullptr};  // CX_LANE_RIVER (highest priority), CX_LANE_STREAM (medium)
+    int lane_prio[2] = {0, 0};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cx::Arena arena;                // device scratch
     int* d_flag = nullptr;          // device-side error flag (softmax non-finite, ...)

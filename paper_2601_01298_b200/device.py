@@ -38,6 +38,50 @@ def ctx(device: int | None = None) -> int:
     return h
 
 
+LANE_RIVER, LANE_STREAM = 0, 1
+_lanes = {}
+
+
+def lane_stream(lane: str, device: int | None = None) -> torch.cuda.ExternalStream:
+    """The context's priority lane as a torch stream: "river" (highest priority:
+    injection appends, synapse pushes) or "stream" (medium: agent decode).
+    The reference runs these as a river thread and per-agent std::threads
+    (scheduler.cpp:63-113, 198); here they are CUDA stream priorities."""
+    if device is None:
+        device = torch.cuda.current_device()
+    code = {"river": LANE_RIVER, "stream": LANE_STREAM}[lane]
+    key = (threading.get_ident(), device, code)
+    s = _lanes.get(key)
+    if s is None:
+        p, prio = c_vp(), C.c_int()
+        check(lib.cx_ctx_lane_stream(ctx(device), code, C.byref(p), C.byref(prio)), "ctx_lane_stream")
+        s = _lanes[key] = torch.cuda.ExternalStream(p.value, device=torch.device("cuda", device))
+        s.cx_priority = prio.value
+    return s
+
+
+class _DevView:
+    """__cuda_array_interface__ over memory owned by the library (zero copy)."""
+
+    def __init__(self, ptr: int, shape, strides_elems, owner):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                         "strides": tuple(4 * s for s in strides_elems), "version": 3}
+        self._owner = owner
+
+
+def kvcache_head_view(cache, kv_head: int, count: int | None = None, values: bool = False) -> torch.Tensor:
+    """Zero-copy [n_layers, count, d_k] view of one KV head of a device KvCache
+    (layout [layer][capacity][d_model], model.hpp:100-103): the per-(layer, KV
+    head) selection groups of the river's context rows (count defaults to the
+    cache size)."""
+    cfg = cache.config()
+    cap = cache.capacity()
+    n = cache.size() if count is None else int(count)
+    base = cache.values_dev() if values else cache.keys_dev()
+    v = _DevView(base + 4 * kv_head * cfg.d_k, (cfg.n_layers, n, cfg.d_k), (cap * cfg.d_model, cfg.d_model, 1), cache)
+    return torch.as_tensor(v, device=torch.device("cuda", torch.cuda.current_device()))
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 

@@ -151,6 +151,14 @@ class KvCache:
         check(lib.cx_kvcache_append_entry(self._h, int(position), int(origin), ptr(k, c_f32p), ptr(v, c_f32p)),
               "append_entry")
 
+    def append_context_dev(self, keys_dev: int, values_dev: int, base_position: int, count: int,
+                           stream: int = 0) -> None:
+        """Bulk device append of `count` context entries (a river prefill) from a
+        device block [n_layers][count][d_model]; same checks as `count`
+        append_entry calls (model.cpp:124-173), stream-ordered."""
+        check(lib.cx_kvcache_append_context_dev(self._h, keys_dev, values_dev, int(base_position), int(count),
+                                                stream or None), "kvcache_append_context_dev")
+
     def keys_dev(self) -> int:
         return int(lib.cx_kvcache_keys_dev(self._h) or 0)
 

@@ -1,0 +1,112 @@
+"""River / Stream priority lanes, the bulk river prefill and compression through a
+zero-copy KvCache view (cfg5 plumbing, BASELINE configs[4]).
+
+The reference runs the river and each stream agent as std::threads
+(scheduler.cpp:63-113, 198); the B200 path runs their device work on CUDA
+streams of different priority from one context (SURVEY.md §8(b) threading row).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cx():
+    import torch
+    torch.cuda.set_device(0)
+    import paper_2601_01298_b200 as m
+    return m
+
+
+def test_priority_lanes(cx):
+    import torch
+    from paper_2601_01298_b200 import device
+    river, stream = device.lane_stream("river"), device.lane_stream("stream")
+    assert river.cuda_stream != stream.cuda_stream
+    # CUDA priorities: numerically smaller = more urgent; the river lane takes the
+    # device's greatest priority (torch's own range is a clamped subset of it)
+    _, torch_hi = torch.cuda.Stream.priority_range()
+    assert river.cx_priority <= torch_hi, "the river lane must have the highest priority"
+    assert river.cx_priority < stream.cx_priority <= 0, "stream agents run below the river"
+    assert device.lane_stream("river") is river  # one lane object per (thread, device)
+    x = torch.ones(1 << 20, device="cuda")
+    with torch.cuda.stream(river):
+        a = x * 2
+    with torch.cuda.stream(stream):
+        b = x * 3
+    torch.cuda.synchronize()
+    assert float(a.sum()) == 2 * (1 << 20) and float(b.sum()) == 3 * (1 << 20)
+    with pytest.raises(KeyError):
+        device.lane_stream("nope")
+
+
+def test_append_context_dev(cx):
+    """Same checks and partial-append behaviour as repeated append_entry calls
+    (model.cpp:124-173)."""
+    import torch
+    cfg = cx.ModelConfig(n_layers=3, n_heads=2, d_model=8, d_k=4, max_positions=20)
+    c = cx.KvCache(cfg, capacity=4)  # grows on the way
+    g = torch.Generator(device="cuda").manual_seed(3)
+    k = torch.randn(3, 6, 8, device="cuda", generator=g)
+    v = torch.randn(3, 6, 8, device="cuda", generator=g)
+    c.append_context_dev(k.data_ptr(), v.data_ptr(), 2, 6)
+    torch.cuda.synchronize()
+    assert c.size() == 6 and c.context_count() == 6 and c.last_context_position() == 7
+    assert list(c.positions()) == list(range(2, 8))
+    assert all(c.origin(i) == cx.Origin.context for i in range(6))
+    for l in range(3):
+        assert np.array_equal(c.layer_keys(l).reshape(6, 8), k[l].cpu().numpy())
+        assert np.array_equal(c.layer_values(l).reshape(6, 8), v[l].cpu().numpy())
+    # non-increasing context position: nothing appended
+    with pytest.raises(cx.errors.precondition_error):
+        c.append_context_dev(k.data_ptr(), v.data_ptr(), 7, 2)
+    assert c.size() == 6
+    # runs past max_positions: the entries before the first bad one stay (reference order)
+    with pytest.raises(cx.errors.capacity_error):
+        c.append_context_dev(k.data_ptr(), v.data_ptr(), 17, 6)
+    torch.cuda.synchronize()
+    assert c.size() == 9 and list(c.positions()[6:]) == [17, 18, 19]
+    assert np.array_equal(c.key(1, 8), k[1, 2].cpu().numpy())
+    c2 = cx.KvCache(cfg)
+    c2.begin_entry(0, cx.Origin.context)
+    with pytest.raises(cx.errors.sequencing_error):
+        c2.append_context_dev(k.data_ptr(), v.data_ptr(), 1, 2)
+    c.append_context_dev(0, 0, 40, 0)  # empty append is a no-op
+
+
+def test_compress_through_kvcache_view_and_lanes(cx):
+    """A river push: per-KV-head compression of the river cache's context rows
+    through the zero-copy [n_layers, L, d_k] view, on the river lane, while an
+    injection lands on the same lane -- identical to compressing a contiguous
+    copy of the same rows."""
+    import torch
+    from paper_2601_01298_b200 import device
+    from paper_2601_01298_b200.injector import inject_dev
+    n_layers, n_kv, dk, L, k = 3, 2, 64, 700, 40
+    cfg = cx.ModelConfig(n_layers=n_layers, n_heads=n_kv, d_model=n_kv * dk, d_k=dk, max_positions=4096)
+    river = cx.KvCache(cfg, capacity=L + 64)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    pk = torch.randn(n_layers, L, n_kv * dk, device="cuda", generator=g)
+    pv = torch.randn(n_layers, L, n_kv * dk, device="cuda", generator=g)
+    rl = device.lane_stream("river")
+    with torch.cuda.stream(rl):
+        river.append_context_dev(pk.data_ptr(), pv.data_ptr(), 0, L, rl.cuda_stream)
+        tk = torch.randn(n_layers, 16, n_kv * dk, device="cuda", generator=g)
+        inject_dev(river, tk.data_ptr(), tk.data_ptr(), 2048, 16, n_layers, n_kv * dk, 1, 5, rl.cuda_stream)
+        q = torch.randn(n_layers, 7, dk, device="cuda", generator=g)
+        res = []
+        for h in range(n_kv):
+            kh = device.kvcache_head_view(river, h, L)
+            vh = device.kvcache_head_view(river, h, L, values=True)
+            assert kh.shape == (n_layers, L, dk) and kh.stride() == ((L + 64) * n_kv * dk, n_kv * dk, 1)
+            res.append(device.compress_grouped(kh, vh, q, k, 0.5))
+    torch.cuda.synchronize()
+    assert river.size() == L + 16 and river.context_count() == L
+    for h in range(n_kv):
+        kc = pk[:, :, h * dk:(h + 1) * dk].contiguous()
+        vc = pv[:, :, h * dk:(h + 1) * dk].contiguous()
+        rows, scores, sk, sv = device.compress_grouped(kc, vc, q, k, 0.5)
+        torch.cuda.synchronize()
+        assert torch.equal(rows, res[h][0]) and torch.equal(scores, res[h][1])
+        assert torch.equal(sk, res[h][2]) and torch.equal(sv, res[h][3])
