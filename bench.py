@@ -566,23 +566,12 @@ def run_e2e(args, dev):
     hk = torch.randn(G, L, D).pin_memory()
     hv = torch.randn(G, L, D).pin_memory()
     hq = torch.randn(G, N_Q // N_KV, D).pin_memory()
-    dk = torch.empty(G, L, D, device=dev)
-    dv = torch.empty(G, L, D, device=dev)
-    dq = torch.empty(G, N_Q // N_KV, D, device=dev)
-    outs = (torch.empty(G, K, dtype=torch.int64, device=dev), torch.empty(G, K, dtype=torch.float64, device=dev),
-            torch.empty(G, K, D, device=dev), torch.empty(G, K, D, device=dev))
-    h_rows = torch.empty(G, K, dtype=torch.int64).pin_memory()
-    h_sk = torch.empty(G, K, D).pin_memory()
-    h_sv = torch.empty(G, K, D).pin_memory()
+    h_out = (torch.empty(G, K, dtype=torch.int64).pin_memory(), torch.empty(G, K, dtype=torch.float64).pin_memory(),
+             torch.empty(G, K, D).pin_memory(), torch.empty(G, K, D).pin_memory())
+    h_rows, h_sk, h_sv = h_out[0], h_out[2], h_out[3]
 
-    def step():
-        dk.copy_(hk, non_blocking=True)
-        dv.copy_(hv, non_blocking=True)
-        dq.copy_(hq, non_blocking=True)
-        cxd.compress_grouped(dk, dv, dq, K, LAM, out=outs)
-        h_rows.copy_(outs[0], non_blocking=True)
-        h_sk.copy_(outs[2], non_blocking=True)
-        h_sv.copy_(outs[3], non_blocking=True)
+    def step():  # ONE C-ABI call (cx_compress_grouped_host): chunked uploads overlap the compressions
+        cxd.compress_grouped_host(hk, hv, hq, K, LAM, out=h_out)
 
     for _ in range(2):
         step()
@@ -596,7 +585,7 @@ def run_e2e(args, dev):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     h2d = (hk.numel() + hv.numel() + hq.numel()) * 4
-    d2h = h_rows.numel() * 8 + (h_sk.numel() + h_sv.numel()) * 4
+    d2h = h_rows.numel() * 8 + h_out[1].numel() * 8 + (h_sk.numel() + h_sv.numel()) * 4
     return {"value": 1000.0 / ms, "unit": "compressions/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms}
 

@@ -153,6 +153,19 @@ cx_status cx_compress_grouped_dev(cx_ctx* ctx, const cx_groups* g, const float* 
                                   int64_t* out_rows, double* out_scores,
                                   float* syn_keys, float* syn_values, void* stream);
 
+/* One synapse compression from HOST buffers (the end-to-end call): dense
+ * keys/values [G][count][dim], queries [G][n_pass][d_k] (n_pass/d_k/col_step as
+ * in cx_groups); outputs (host): rows/scores [G][take], syn_keys/syn_values
+ * [G][take][dim], take = min(k, count).  Groups are uploaded in chunks on a copy
+ * stream so the upload of chunk i+1 overlaps the compression of chunk i (true
+ * overlap needs pinned host memory).  Synchronous: returns with outputs written.
+ * Same checks, in the same order, as cx_compress_grouped_dev. */
+cx_status cx_compress_grouped_host(cx_ctx* ctx, int n_groups, int64_t count, int dim,
+                                   const float* keys, const float* values, const float* queries,
+                                   int n_pass, int d_k, int col_step, int k, double lambda,
+                                   unsigned flags, int64_t* out_rows, double* out_scores,
+                                   float* syn_keys, float* syn_values);
+
 /* ======================================================================
  * Batched decode attention of N agents against the shared synapse
  * (kernels.cpp:103-142 per (agent, layer, q-head), fp32 accumulate).

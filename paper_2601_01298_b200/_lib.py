@@ -77,6 +77,9 @@ _SIGS = [
     ("cx_ctx_create", C.c_int, [C.c_int, C.POINTER(c_vp)]),
     ("cx_ctx_destroy", C.c_int, [c_vp]),
     ("cx_ctx_lane_stream", C.c_int, [c_vp, C.c_int, C.POINTER(c_vp), C.POINTER(C.c_int)]),
+    ("cx_compress_grouped_host", C.c_int,
+     [c_vp, C.c_int, C.c_int64, C.c_int, c_vp, c_vp, c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+      C.c_uint, c_vp, c_vp, c_vp, c_vp]),
     ("cx_attention_grouped_dev", C.c_int, [c_vp, C.POINTER(CxGroups), c_vp, c_vp]),
     ("cx_select_grouped_dev", C.c_int,
      [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp]),

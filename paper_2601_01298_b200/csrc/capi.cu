@@ -41,6 +41,7 @@ void ctx_init(cx_ctx* c, int device) {
     c->lane_prio[CX_LANE_STREAM] = (lo + hi) / 2 == hi && lo != hi ? hi + 1 : (lo + hi) / 2;
     CX_CUDA(cudaStreamCreateWithPriority(&c->lane[CX_LANE_RIVER], cudaStreamNonBlocking, c->lane_prio[CX_LANE_RIVER]));
     CX_CUDA(cudaStreamCreateWithPriority(&c->lane[CX_LANE_STREAM], cudaStreamNonBlocking, c->lane_prio[CX_LANE_STREAM]));
+    CX_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     CX_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CX_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
@@ -160,6 +161,10 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
         if (c->d_flag) cudaFree(c->d_flag);
         cudaEventDestroy(c->ev_fork);
         cudaEventDestroy(c->ev_join);
+        cudaStreamSynchronize(c->copy);
+        cudaStreamDestroy(c->copy);
+        for (cudaEvent_t e : c->hev) cudaEventDestroy(e);
+        if (c->hbuf) cudaFree(c->hbuf);
         for (cudaStream_t& l : c->lane) {
             cudaStreamSynchronize(l);
             cudaStreamDestroy(l);
@@ -479,15 +484,12 @@ extern "C" cx_status cx_gather_grouped_dev(cx_ctx* c, const cx_groups* gr, const
     });
 }
 
-extern "C" cx_status cx_compress_grouped_dev(cx_ctx* c, const cx_groups* gr, const float* values, int k, double lambda,
-                                             unsigned flags, int64_t* out_rows, double* out_scores, float* syn_keys,
-                                             float* syn_values, void* stream) {
-    return guard([&] {
-        if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
-        if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
-        if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
-        validate_groups(gr, true);
-        if (!out_rows || !out_scores) fail(CX_INVALID_ARGUMENT, "null outputs");
+namespace {
+
+// attention || centroid, selection, landmark gather for the groups of `gr` (validated)
+void compress_impl(cx_ctx* c, const cx_groups* gr, const float* values, int k, double lambda, unsigned flags,
+                   int64_t* out_rows, double* out_scores, float* syn_keys, float* syn_values, void* stream) {
+    {
         GroupView g = view_of(gr);
         const int take = (int)std::min<int64_t>(k, g.L);
         ArenaPlan pl;
@@ -513,6 +515,111 @@ extern "C" cx_status cx_compress_grouped_dev(cx_ctx* c, const cx_groups* gr, con
         select_grouped(c, g, attn, k, lambda, flags, out_rows, out_scores, s, cen);
         if (syn_keys) gather_rows(g, g.X, out_rows, take, syn_keys, s);
         if (syn_values && values) gather_rows(g, values, out_rows, take, syn_values, s);
+    }
+}
+
+}  // namespace
+
+extern "C" cx_status cx_compress_grouped_dev(cx_ctx* c, const cx_groups* gr, const float* values, int k, double lambda,
+                                             unsigned flags, int64_t* out_rows, double* out_scores, float* syn_keys,
+                                             float* syn_values, void* stream) {
+    return guard([&] {
+        if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
+        if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
+        if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
+        validate_groups(gr, true);
+        if (!out_rows || !out_scores) fail(CX_INVALID_ARGUMENT, "null outputs");
+        compress_impl(c, gr, values, k, lambda, flags, out_rows, out_scores, syn_keys, syn_values, stream);
+    });
+}
+
+extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t count, int dim, const float* keys,
+                                              const float* values, const float* queries, int n_pass, int d_k,
+                                              int col_step, int k, double lambda, unsigned flags, int64_t* out_rows,
+                                              double* out_scores, float* syn_keys, float* syn_values) {
+    return guard([&] {
+        if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
+        if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
+        if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
+        cx_groups all{};
+        all.n_groups = n_groups;
+        all.count = count;
+        all.dim = dim;
+        all.clouds = keys;
+        all.group_stride = count * dim;
+        all.row_stride = dim;
+        all.queries = queries;
+        all.n_pass = n_pass;
+        all.d_k = d_k;
+        all.col_step = col_step;
+        validate_groups(&all, true);
+        if (!out_rows || !out_scores || !values) fail(CX_INVALID_ARGUMENT, "null pointer");
+        if (n_groups == 0) return;
+        const int take = (int)std::min<int64_t>(k, count);
+        const size_t in_g = (size_t)count * dim, q_g = (size_t)n_pass * d_k, o_g = (size_t)take * dim;
+        // device staging: keys | values | queries | rows | scores | syn_k | syn_v (256-B aligned slices)
+        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t b_k = al(sizeof(float) * in_g * n_groups), b_q = al(sizeof(float) * q_g * n_groups);
+        const size_t b_r = al(sizeof(int64_t) * take * n_groups), b_s = al(sizeof(double) * take * n_groups);
+        const size_t b_o = al(sizeof(float) * o_g * n_groups);
+        const size_t need = 2 * b_k + b_q + b_r + b_s + 2 * b_o;
+        if (need > c->hcap) {
+            if (c->hbuf) {
+                CX_CUDA(cudaStreamSynchronize(c->stream));
+                cudaFree(c->hbuf);
+            }
+            c->hbuf = nullptr;
+            c->hcap = 0;
+            CX_CUDA(cudaMalloc(&c->hbuf, need));
+            c->hcap = need;
+        }
+        char* p = c->hbuf;
+        float* dk = reinterpret_cast<float*>(p); p += b_k;
+        float* dv = reinterpret_cast<float*>(p); p += b_k;
+        float* dq = reinterpret_cast<float*>(p); p += b_q;
+        int64_t* dr = reinterpret_cast<int64_t*>(p); p += b_r;
+        double* ds = reinterpret_cast<double*>(p); p += b_s;
+        float* dsk = reinterpret_cast<float*>(p); p += b_o;
+        float* dsv = reinterpret_cast<float*>(p);
+        // Chunks of groups, one selection wave each (15 co-resident 8-CTA clusters on
+        // B200), so chunking costs no compute; the remainder goes FIRST so that the
+        // only exposed upload is the smallest one.
+        constexpr int WAVE = 15;
+        std::vector<int> start;
+        for (int g0 = 0, first = n_groups % WAVE ? n_groups % WAVE : WAVE; g0 < n_groups; g0 += (g0 ? WAVE : first))
+            start.push_back(g0);
+        const int nch = (int)start.size();
+        start.push_back(n_groups);
+        while ((int)c->hev.size() < nch) {
+            cudaEvent_t e;
+            CX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->hev.push_back(e);
+        }
+        CX_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        for (int i = 0; i < nch; ++i) {  // all uploads queued on the copy stream
+            const int g0 = start[i], ng = start[i + 1] - g0;
+            CX_CUDA(cudaMemcpyAsync(dk + g0 * in_g, keys + g0 * in_g, sizeof(float) * in_g * ng, cudaMemcpyHostToDevice, c->copy));
+            CX_CUDA(cudaMemcpyAsync(dv + g0 * in_g, values + g0 * in_g, sizeof(float) * in_g * ng, cudaMemcpyHostToDevice, c->copy));
+            CX_CUDA(cudaMemcpyAsync(dq + g0 * q_g, queries + g0 * q_g, sizeof(float) * q_g * ng, cudaMemcpyHostToDevice, c->copy));
+            CX_CUDA(cudaEventRecord(c->hev[i], c->copy));
+        }
+        for (int i = 0; i < nch; ++i) {  // chunk i computes as soon as its upload lands
+            const int g0 = start[i], ng = start[i + 1] - g0;
+            CX_CUDA(cudaStreamWaitEvent(c->stream, c->hev[i], 0));
+            cx_groups gi = all;
+            gi.n_groups = ng;
+            gi.clouds = dk + g0 * in_g;
+            gi.queries = dq + g0 * q_g;
+            compress_impl(c, &gi, dv + g0 * in_g, k, lambda, flags, dr + (size_t)g0 * take, ds + (size_t)g0 * take,
+                          dsk + g0 * o_g, dsv + g0 * o_g, c->stream);
+        }
+        CX_CUDA(cudaMemcpyAsync(out_rows, dr, sizeof(int64_t) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));
+        CX_CUDA(cudaMemcpyAsync(out_scores, ds, sizeof(double) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));
+        if (syn_keys)
+            CX_CUDA(cudaMemcpyAsync(syn_keys, dsk, sizeof(float) * o_g * n_groups, cudaMemcpyDeviceToHost, c->stream));
+        if (syn_values)
+            CX_CUDA(cudaMemcpyAsync(syn_values, dsv, sizeof(float) * o_g * n_groups, cudaMemcpyDeviceToHost, c->stream));
+        check_flag_and_sync(c);  // non-finite attention input -> precondition_error (kernels.cpp:70)
     });
 }
 

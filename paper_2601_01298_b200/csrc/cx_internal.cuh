@@ -101,6 +101,10 @@ struct cx_ctx {
     cudaStream_t side = nullptr;    // fork target (centroid alongside attention)
     cudaStream_t lane[2] = {nullptr, nullptr};  // CX_LANE_RIVER (highest priority), CX_LANE_STREAM (medium)
     int lane_prio[2] = {0, 0};
+    cudaStream_t copy = nullptr;    // host-path uploads (cx_compress_grouped_host)
+    char* hbuf = nullptr;           // host-path device staging (grow-only, separate from the arena)
+    size_t hcap = 0;
+    std::vector<cudaEvent_t> hev;   // per-chunk upload events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cx::Arena arena;                // device scratch
     int* d_flag = nullptr;          // device-side error flag (softmax non-finite, ...)

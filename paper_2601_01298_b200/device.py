@@ -157,6 +157,34 @@ def compress_grouped(keys: torch.Tensor, values: torch.Tensor, queries: torch.Te
     return out
 
 
+def compress_grouped_host(keys: torch.Tensor, values: torch.Tensor, queries: torch.Tensor, k: int, lam: float,
+                          mode: str = "gqa", flags: int = 0, out=None, device: int | None = None):
+    """The end-to-end compression from HOST tensors (use pinned memory for overlap):
+    keys/values [G, L, d], queries [G, P, d_k] (contiguous, CPU) -> host (rows,
+    scores, syn_keys, syn_values).  Uploads are chunked and overlap the per-chunk
+    compressions inside the library (cx_compress_grouped_host)."""
+    for t in (keys, values, queries):
+        if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+            raise TypeError("host path: contiguous CPU float32 tensors")
+    G, L, d = keys.shape
+    if values.shape != keys.shape or queries.shape[0] != G:
+        raise ValueError("keys/values/queries shape mismatch")
+    P, dk = queries.shape[1], queries.shape[2]
+    take = min(k, L)
+    if out is None:
+        pin = keys.is_pinned()
+        out = (torch.empty((G, take), dtype=torch.int64, pin_memory=pin),
+               torch.empty((G, take), dtype=torch.float64, pin_memory=pin),
+               torch.empty((G, take, d), dtype=torch.float32, pin_memory=pin),
+               torch.empty((G, take, d), dtype=torch.float32, pin_memory=pin))
+    rows, scores, sk, sv = out
+    check(lib.cx_compress_grouped_host(ctx(device), G, L, d, keys.data_ptr(), values.data_ptr(), queries.data_ptr(),
+                                       P, dk, dk if mode == "mha" else 0, int(k), float(lam), int(flags),
+                                       rows.data_ptr(), scores.data_ptr(), sk.data_ptr(), sv.data_ptr()),
+          "compress_grouped_host")
+    return out
+
+
 def decode_step(syn_keys: torch.Tensor, syn_values: torch.Tensor, tail_keys: torch.Tensor,
                 tail_values: torch.Tensor, tail_len: torch.Tensor, q: torch.Tensor, out: torch.Tensor,
                 new_keys: torch.Tensor | None = None, new_values: torch.Tensor | None = None) -> torch.Tensor:

@@ -110,3 +110,26 @@ def test_compress_through_kvcache_view_and_lanes(cx):
         torch.cuda.synchronize()
         assert torch.equal(rows, res[h][0]) and torch.equal(scores, res[h][1])
         assert torch.equal(sk, res[h][2]) and torch.equal(sv, res[h][3])
+
+
+@pytest.mark.parametrize("G,pinned", [(13, True), (3, False)])
+def test_compress_grouped_host_matches_device(cx, G, pinned):
+    """cx_compress_grouped_host (chunked uploads overlapping the per-chunk
+    compressions) == cx_compress_grouped_dev on the same data, bit for bit,
+    including a ragged last chunk and pageable host memory."""
+    import torch
+    from paper_2601_01298_b200 import device
+    L, d, P, k = 1500, 64, 7, 60
+    gen = torch.Generator().manual_seed(21 + G)
+    hk = torch.randn(G, L, d, generator=gen)
+    hv = torch.randn(G, L, d, generator=gen)
+    hq = torch.randn(G, P, d, generator=gen)
+    if pinned:
+        hk, hv, hq = hk.pin_memory(), hv.pin_memory(), hq.pin_memory()
+    rows, scores, sk, sv = device.compress_grouped_host(hk, hv, hq, k, 0.5)
+    dr, ds, dsk, dsv = device.compress_grouped(hk.cuda(), hv.cuda(), hq.cuda(), k, 0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(rows, dr.cpu()) and torch.equal(scores, ds.cpu())
+    assert torch.equal(sk, dsk.cpu()) and torch.equal(sv, dsv.cpu())
+    with pytest.raises(cx.errors.config_error):
+        device.compress_grouped_host(hk, hv, hq, 0, 0.5)
