@@ -106,15 +106,12 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* m, uint32_t parity) {
     __syncwarp();
 }
 
-// Named barriers count whole warps (.aligned): reconverge first -- lanes leave the
-// mbarrier spin loops at different iterations, and a diverged warp would arrive twice.
+// Named barrier among the synapse warps.  Named barriers count whole warps
+// (.aligned): reconverge first -- lanes leave the mbarrier spin loops at different
+// iterations.  (Cross-role hand-offs use mbarriers, not bar.arrive.)
 __device__ __forceinline__ void bar_sync(int id, int n) {
     __syncwarp();
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-    __syncwarp();
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // packed fp32x2 FMA (sm_100): two independent fp32 FMAs per instruction
@@ -164,12 +161,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* out) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int j = 0; j < 16; ++j) out[j] = __uint_as_float(v[j]);
-}
-
-// split x into bf16 hi + lo (x - hi - lo ~ 2^-17 |x|)
-__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
-    hi = __float2bfloat16_rn(x);
-    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
 // 8 floats -> one 16-byte core-matrix row chunk of hi and of lo (packed bf16x2 conversions)

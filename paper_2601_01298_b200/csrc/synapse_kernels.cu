@@ -20,7 +20,6 @@ namespace cx {
 
 namespace {
 
-constexpr int kWarp = 32;
 constexpr int kMaxCluster = 16;
 
 __device__ __forceinline__ double dmin_std(double a, double b) { return (b < a) ? b : a; }  // std::min
