@@ -487,12 +487,14 @@ static bool launch_decode_v2(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t
 
 void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int qpg = b.n_q / b.n_kv;
-    // CX_DECODE=tc|v2|v1 pins an implementation (testing); default: the tcgen05
-    // kernel (decode_tc.cu), then v2 (CUDA cores), then the generic v1.
+    // CX_DECODE=tc|v2|v1 pins an implementation (testing; a pinned kernel that does
+    // not apply to the shape is an error, not a silent fallback).  Default: the
+    // tcgen05 kernel (decode_tc.cu), then v2 (CUDA cores), then the generic v1.
     const char* pin = getenv("CX_DECODE");
     const bool allow_tc = !pin || !strcmp(pin, "tc");
-    const bool allow_v2 = !pin || !strcmp(pin, "tc") || !strcmp(pin, "v2");
+    const bool allow_v2 = !pin || !strcmp(pin, "v2");
     if (allow_tc && decode_tc_launch(ctx, b, s)) return;
+    if (pin && !strcmp(pin, "tc")) fail(CX_PRECONDITION_ERROR, "decode_step: CX_DECODE=tc does not apply to this shape");
     if (allow_v2 && b.d_k == DV2_DK && b.k_syn <= 32 * DV2_KPL && b.t_cap <= 64) {
         bool done = false;
         switch (qpg) {
@@ -505,6 +507,7 @@ void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
         }
         if (done) return;
     }
+    if (pin && !strcmp(pin, "v2")) fail(CX_PRECONDITION_ERROR, "decode_step: CX_DECODE=v2 does not apply to this shape");
     int apb = std::max(1, 8 / qpg);
     const int warps = apb * qpg;
     const int t_rows = b.t_cap + 1;

@@ -369,9 +369,12 @@ def test_synapse_buffer(cx):
     assert b4.wait_nonempty(5000) is None
 
 
-@pytest.mark.parametrize("impl,N,k,Lr", [("tc", 9, 164, 3), ("tc", 40, 100, 3), ("tc", 100, 164, 24),
-                                         ("v2", 9, 164, 3), ("v2", 100, 164, 24), ("v1", 5, 164, 3)])
-def test_decode_step_vs_oracle(dev, orc, monkeypatch, impl, N, k, Lr):
+@pytest.mark.parametrize("impl,N,k,Lr,H,Q,Tc", [
+    ("tc", 9, 164, 3, 2, 14, 33), ("tc", 40, 100, 3, 2, 14, 33), ("tc", 100, 164, 24, 2, 14, 33),
+    # every q-heads-per-KV-head instantiation (reduce-scatter widths 1, 2, 4, 8), t_cap / k_syn edges
+    ("tc", 7, 17, 2, 2, 2, 5), ("tc", 11, 1, 2, 2, 4, 64), ("tc", 30, 176, 2, 1, 4, 20), ("tc", 5, 64, 2, 2, 16, 33),
+    ("v2", 9, 164, 3, 2, 14, 33), ("v2", 100, 164, 24, 2, 14, 33), ("v1", 5, 164, 3, 2, 14, 33)])
+def test_decode_step_vs_oracle(dev, orc, monkeypatch, impl, N, k, Lr, H, Q, Tc):
     """Batched decode (append + attend) == kernels::attend(n_heads=1) per (agent, layer, q-head)
     over [synapse rows of its KV head || private rows] (scheduler.cpp:245-262), 1e-3 rel.
     impl: tc = tcgen05 synapse GEMMs, v2 = CUDA-core register-tiled, v1 = generic.
@@ -380,7 +383,7 @@ def test_decode_step_vs_oracle(dev, orc, monkeypatch, impl, N, k, Lr):
     import torch
     monkeypatch.setenv("CX_DECODE", impl)
     gen = torch.Generator(device="cuda").manual_seed(11)
-    H, Q, dk, Tc = 2, 14, 64, 33
+    dk = 64
     syn_k = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
     syn_v = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
     tk = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
