@@ -45,7 +45,10 @@ constexpr int PWARPS = 12;      // private-row warps (13+ warps allocate registe
 constexpr int TTHREADS = 32 * (SWARPS + PWARPS);
 constexpr int OPS = TD + 4;     // O_priv row stride (floats; conflict-free float4 rows)
 constexpr bool PREFETCH_NEXT = true;  // L2 bulk prefetch of each warp's next agent (net win: -18 us, though ~25% of it is evicted)
-constexpr int SST = TTAIL + 4;  // private score row stride (16-B aligned, conflict-free stores)
+constexpr int SST = TTAIL + 4;
+// O_priv buffers: 2 lets the private warps publish a tile before the previous tile's
+// epilogue; 1 saves 35 KB of shared memory, i.e. leaves L1 room for the private stream
+constexpr int OP_BUFS = 1;  // private score row stride (16-B aligned, conflict-free stores)
 
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -212,7 +215,7 @@ __host__ __device__ inline TcLayout tc_layout(int k_syn, int qpg) {
     L.vh = o; o += kv;
     L.vl = o; o += kv;
     L.qo = o; o += q2;                 // Q hi | lo (A operand of the score MMAs)
-    L.op = o; o += 2 * op;             // O_priv [2][TM][OPS], double-buffered by tile parity
+    L.op = o; o += OP_BUFS * op;       // O_priv [OP_BUFS][TM][OPS]
     L.sw = o; o += pw;                 // per private warp: scores / weights [qpg][SST]
     L.mp = o; o += sizeof(float) * 2 * TM;  // private (m, l) per row, double-buffered by tile parity
     L.lp = o; o += sizeof(float) * 2 * TM;
@@ -235,6 +238,17 @@ __device__ __forceinline__ unsigned long long gtime() {
     } while (0)
 
 // ---- private-row helpers (warp per agent) ----
+// L1PF: private rows go through L1 (ld.global.nc) and each 16-row batch is
+// prefetched into L1 one batch ahead (prefetch.global.L1: no registers, no shared
+// memory); otherwise they are streamed with ld.global.cg (L2 only).
+constexpr bool L1PF = true;
+template <class T>
+__device__ __forceinline__ T ldrow(const T* p) { return L1PF ? __ldg(p) : __ldcg(p); }
+// the 32 lines of 16 private rows starting at row r0 (row = 256 B), one per lane
+__device__ __forceinline__ void prefetch_rows16_l1(const float* base, int r0, int nrows, int lane) {
+    if (L1PF && r0 + (lane >> 1) < nrows)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(base + (size_t)r0 * TD + lane * 32));
+}
 // Private rows are read with ld.global.cg (L2-coherent, no L1 allocation: they have
 // no reuse).  q lives in registers: lane rl of a row's 8 lanes holds dims
 // [4 rl, 4 rl + 4) and [32 + 4 rl, 32 + 4 rl + 4) of every head.
@@ -291,8 +305,8 @@ __device__ __forceinline__ void score_rows(const float* tk, int r0, int nt, cons
         const int t = r0 + 4 * j + rg;
         const float4* kp = reinterpret_cast<const float4*>(tk + (size_t)t * TD);
         if (!PRED || t < nt) {
-            ka[j] = __ldcg(kp + rl);
-            kb[j] = __ldcg(kp + 8 + rl);
+            ka[j] = ldrow(kp + rl);
+            kb[j] = ldrow(kp + 8 + rl);
         } else {
             ka[j] = kb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -310,7 +324,7 @@ __device__ __forceinline__ void mix_rows(const float* tv, int r0, int nt, const 
     float2 v[NR];
 #pragma unroll
     for (int t = 0; t < NR; ++t)
-        v[t] = (!PRED || r0 + t < nt) ? __ldcg(reinterpret_cast<const float2*>(tv + (size_t)(r0 + t) * TD) + lane)
+        v[t] = (!PRED || r0 + t < nt) ? ldrow(reinterpret_cast<const float2*>(tv + (size_t)(r0 + t) * TD) + lane)
                                       : make_float2(0.f, 0.f);
 #pragma unroll
     for (int t4 = 0; t4 < NR / 4; ++t4)
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             mbar_wait_sleep(&mbar[2 + tpar], (uint32_t)(ti >> 1) & 1u);
             if (tid == 0) TC_TRACE(ti * 16 + 5);
             {
-                const float* Opt = Op + (size_t)tpar * TM * OPS;
+                const float* Opt = Op + (size_t)(OP_BUFS == 2 ? tpar : 0) * TM * OPS;
                 float v[TD];
                 const uint32_t trow_o = tO + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
@@ -605,7 +619,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
         for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
             const int a0 = tile * AT;
             const int na = min(AT, b.n_agents - a0);
-            bool published = false;
+            bool published = false, op_free = false;
             if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + 8);
             // agents are dealt round-robin over the CTA's whole agent sequence, not per
             // tile: with 18 agents per tile and 12 warps no warp takes 2 every tile
@@ -620,7 +634,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 const float* tk = b.tail_keys + toff;
                 const float* tv = b.tail_values + toff;
                 const float* qrow = b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG) * TD;
-                if (lane == 0 && PREFETCH_NEXT) {  // this warp's next agent -> L2, one agent ahead
+                // this warp's next agent: its private rows -> L2 now (bulk prefetch)
+                {
                     int na_t = ai + PWARPS, nt_tile = tile;
                     if (na_t >= na) {
                         na_t = (pw - ((ti + 1) * AT) % PWARPS + PWARPS) % PWARPS;
@@ -629,8 +644,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     const int an = nt_tile * AT + na_t;
                     if (nt_tile < n_tiles && an < b.n_agents && na_t < AT) {
                         const size_t off = ((((size_t)an * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
-                        const uint32_t bytes = (uint32_t)min(b.tail_len[an] + (app ? 1 : 0), b.t_cap) * TD * 4;
-                        if (bytes) {
+                        const int nx_len = min(b.tail_len[an], b.t_cap - (app ? 1 : 0));
+                        const uint32_t bytes = (uint32_t)min(nx_len + (app ? 1 : 0), b.t_cap) * TD * 4;
+                        if (lane == 0 && PREFETCH_NEXT && bytes) {
                             l2_prefetch(b.tail_keys + off, bytes);
                             l2_prefetch(b.tail_values + off, bytes);
                         }
@@ -658,7 +674,11 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 }
                 // ---- scores of the stored rows [0, len): 16-row batches, then 4-row groups ----
                 int r0 = 0;
-                for (; r0 + 16 <= len; r0 += 16) score_rows<QPG, 4, false>(tk, r0, len, qa, qb, Sw, lane, scale);
+                prefetch_rows16_l1(tv, 0, len, lane);  // V batch 0 lands in L1 during the scores
+                for (; r0 + 16 <= len; r0 += 16) {
+                    prefetch_rows16_l1(tk, r0 + 16, len, lane);
+                    score_rows<QPG, 4, false>(tk, r0, len, qa, qb, Sw, lane, scale);
+                }
                 for (; r0 < len; r0 += 4) score_rows<QPG, 1, true>(tk, r0, len, qa, qb, Sw, lane, scale);
                 if (app) score_group<QPG>(nka, nkb, len, lane < 8, qa, qb, Sw, lane, scale);
                 if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == first ? 9 : 12));
@@ -691,7 +711,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) o[h] = make_float2(0.f, 0.f);
                 r0 = 0;
-                for (; r0 + 16 <= len; r0 += 16) mix_rows<QPG, 16, false>(tv, r0, len, Sw, o, lane);
+                for (; r0 + 16 <= len; r0 += 16) {
+                    prefetch_rows16_l1(tv, r0 + 16, len, lane);
+                    mix_rows<QPG, 16, false>(tv, r0, len, Sw, o, lane);
+                }
                 for (; r0 < len; r0 += 4) mix_rows<QPG, 4, true>(tv, r0, len, Sw, o, lane);
                 if (app)
 #pragma unroll
@@ -701,10 +724,14 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                         o[h].y = fmaf(p, nvv.y, o[h].y);
                     }
                 if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == first ? 10 : 13));
+                if (OP_BUFS == 1 && !op_free) {  // single O_priv buffer: last tile's epilogue must be done
+                    wait_epilogues(epi_done, ti);
+                    op_free = true;
+                }
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) {
                     const int r = ai * QPG + h;
-                    reinterpret_cast<float2*>(Op + ((size_t)tpar * TM + r) * OPS)[lane] = o[h];
+                    reinterpret_cast<float2*>(Op + ((size_t)(OP_BUFS == 2 ? tpar : 0) * TM + r) * OPS)[lane] = o[h];
                 }
                 __syncwarp();  // Sw reuse
             }
