@@ -44,7 +44,7 @@ constexpr int SWARPS = 4;       // synapse warps (TMEM lanes 0-127)
 constexpr int PWARPS = 12;      // private-row warps (13+ warps allocate registers like 16)
 constexpr int TTHREADS = 32 * (SWARPS + PWARPS);
 constexpr int OPS = TD + 4;     // O_priv row stride (floats; conflict-free float4 rows)
-constexpr bool PREFETCH_NEXT = true;  // L2 bulk prefetch of each warp's next agent (net win: -18 us, though ~25% of it is evicted)
+constexpr bool PREFETCH_NEXT = false;  // L2 bulk prefetch of the next agent: superseded by the L1 batch prefetch (it added ~25% DRAM re-reads)
 constexpr int SST = TTAIL + 4;
 // O_priv buffers: 2 lets the private warps publish a tile before the previous tile's
 // epilogue; 1 saves 35 KB of shared memory, i.e. leaves L1 room for the private stream
