@@ -23,6 +23,9 @@
 // reference.
 #include <cooperative_groups.h>
 
+#include <map>
+#include <mutex>
+
 #include "cx_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -594,6 +597,38 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
 
 // Host side: choose the cluster size and residency, launch.  Returns false
 // when the dim-64 kernel does not apply (caller uses the generic kernel).
+// co-resident clusters of size C for the on-chip (shared-memory rows) kernel, cached
+static int active_clusters(int C, int Rs, int S) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;
+    const size_t smem = sel64_layout(Rs, true).total;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(C, (int)smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    const int rpt = (S + NT - 1) / NT;
+    void (*kern)(Sel64Params) = rpt <= 1 ? select64_kernel<1, true> : rpt <= 2 ? select64_kernel<2, true> : select64_kernel<4, true>;
+    int n = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess) {
+        if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)C, 1, 1);
+        cfg.blockDim = dim3(NT, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    }
+    cudaGetLastError();  // an unsupported query leaves no sticky error behind
+    cache[key] = n;
+    return n;
+}
+
 bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                      cudaStream_t s) {
@@ -626,6 +661,27 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
         if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT && sel64_layout(rs, true).total <= budget) {
             C = c; S = s_; Rs = rs;
         }
+    }
+    // Among the on-chip cluster sizes, pick the one minimising waves x per-round cost.
+    // Per-round cost was measured to be ~3.6 us + 0.0037 us per row per CTA on B200
+    // (C=8: 7.4 us, C=9: 7.2 us, C=16: 5.5 us at L=8192); waves = ceil(G / co-resident
+    // clusters), queried once per configuration.  cfg2 (G=48): C=9 (4 waves, 4.71 vs
+    // 4.86 ms at C=8); G <= 7 (one group, or cfg2 over 8 GPUs): C=16.
+    if (C > 0 && !getenv("CX_SEL_C")) {
+        double best = 1e300;
+        int bc = C, bs = S, brs = Rs;
+        for (int c = C; c <= MAXC; ++c) {
+            const int s_ = (int)((g.L + c - 1) / c), rs = std::max(0, s_ - NT);
+            if (s_ > MAXRPT_ALL * NT || sel64_layout(rs, true).total > budget) continue;
+            const int act = active_clusters(c, rs, s_);
+            if (act <= 0) continue;
+            const double cost = (double)((g.G + act - 1) / act) * (3.6 + 0.0037 * s_);
+            if (cost < best * (1.0 - 1e-9)) {
+                best = cost;
+                bc = c; bs = s_; brs = rs;
+            }
+        }
+        C = bc; S = bs; Rs = brs;
     }
     if (C == 0) {  // too large for one cluster on chip: rows beyond 512 stay in L2
         C = MAXC;
