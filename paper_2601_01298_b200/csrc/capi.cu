@@ -846,11 +846,15 @@ extern "C" cx_status cx_kvcache_append_context_dev(cx_kvcache* c, const float* k
                 CX_CUDA(cudaStreamWaitEvent(s, ev, 0));
                 cudaEventDestroy(ev);
             }
-            for (int l = 0; l < c->n_layers; ++l)
-                kv_append_rows(c->keys + (size_t)l * c->capacity * c->d_model,
-                               c->values + (size_t)l * c->capacity * c->d_model, c->capacity, 1, c->d_model,
-                               keys + (size_t)l * count * c->d_model, values + (size_t)l * count * c->d_model, n_ok,
-                               row0, s);
+            if (n_ok == count) {  // the whole block: one launch for all layers
+                kv_append_rows(c->keys, c->values, c->capacity, c->n_layers, c->d_model, keys, values, n_ok, row0, s);
+            } else {
+                for (int l = 0; l < c->n_layers; ++l)
+                    kv_append_rows(c->keys + (size_t)l * c->capacity * c->d_model,
+                                   c->values + (size_t)l * c->capacity * c->d_model, c->capacity, 1, c->d_model,
+                                   keys + (size_t)l * count * c->d_model, values + (size_t)l * count * c->d_model,
+                                   n_ok, row0, s);
+            }
             for (int64_t t = 0; t < n_ok; ++t) {
                 c->positions.push_back(base_position + t);
                 c->origins.push_back((uint8_t)CX_ORIGIN_CONTEXT);

@@ -13,7 +13,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--groups", type=int, default=48)
 ap.add_argument("--agents", type=int, default=1000)
 ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--what", default="both")
+ap.add_argument("--what", default="both")  # both = compress + decode + inject
 a = ap.parse_args()
 torch.cuda.set_device(0)
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -37,5 +37,17 @@ if a.what in ("both", "decode"):
     o = torch.empty_like(qq)
     for _ in range(a.reps):
         cxd.decode_step(sk, sv, tk, tv, tl, qq, o, nk, nv)
+    torch.cuda.synchronize()
+if a.what in ("both", "inject"):  # Referential Injection append (cfg5: 16-token block into the river cache)
+    from paper_2601_01298_b200.injector import inject_dev
+    from paper_2601_01298_b200.model import KvCache, ModelConfig
+    cfg = ModelConfig(n_layers=24, n_heads=2, d_model=128, d_k=64, max_positions=16384)
+    river = KvCache(cfg, capacity=8192 + 64)
+    pk = torch.randn(24, 8192, 128, device="cuda", generator=g)
+    river.append_context_dev(pk.data_ptr(), pk.data_ptr(), 0, 8192, torch.cuda.current_stream().cuda_stream)
+    tk = torch.randn(24, 16, 128, device="cuda", generator=g)
+    for r in range(a.reps):
+        inject_dev(river, tk.data_ptr(), tk.data_ptr(), 9000 + 16 * r, 16, 24, 128, r, 0,
+                   torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
 print("ok")
