@@ -629,6 +629,28 @@ static int active_clusters(int C, int Rs, int S) {
     return n;
 }
 
+// Among the on-chip cluster sizes >= c_min, the one minimising waves x per-round cost
+// for G groups.  Per-round cost was measured to be ~3.6 us + 0.0037 us per row per CTA
+// on B200 (C=8: 7.4 us, C=9: 7.2 us, C=16: 5.5 us at L=8192); waves = ceil(G /
+// co-resident clusters).  cfg2 (G=48): C=9 (4.71 vs 4.86 ms at C=8); G <= 7 (one
+// group, or cfg2 over 8 GPUs): C=16.  Returns the estimated cost (us per round).
+static double best_cluster(int G, int64_t L, int c_min, size_t budget, int* C, int* S, int* Rs, int* act_out) {
+    double best = 1e300;
+    for (int c = c_min; c <= MAXC; ++c) {
+        const int s_ = (int)((L + c - 1) / c), rs = std::max(0, s_ - NT);
+        if (s_ > MAXRPT_ALL * NT || sel64_layout(rs, true).total > budget) continue;
+        const int act = active_clusters(c, rs, s_);
+        if (act <= 0) continue;
+        const double cost = (double)((G + act - 1) / act) * (3.6 + 0.0037 * s_);
+        if (cost < best * (1.0 - 1e-9)) {
+            best = cost;
+            *C = c; *S = s_; *Rs = rs;
+            *act_out = act;
+        }
+    }
+    return best;
+}
+
 bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                      cudaStream_t s) {
@@ -662,26 +684,29 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
             C = c; S = s_; Rs = rs;
         }
     }
-    // Among the on-chip cluster sizes, pick the one minimising waves x per-round cost.
-    // Per-round cost was measured to be ~3.6 us + 0.0037 us per row per CTA on B200
-    // (C=8: 7.4 us, C=9: 7.2 us, C=16: 5.5 us at L=8192); waves = ceil(G / co-resident
-    // clusters), queried once per configuration.  cfg2 (G=48): C=9 (4 waves, 4.71 vs
-    // 4.86 ms at C=8); G <= 7 (one group, or cfg2 over 8 GPUs): C=16.
+    // cluster size by the cost model (best_cluster)
+    // A partial last wave (cfg2: 48 = 15 + 15 + 15 + 3 clusters) runs as its own launch
+    // with the cluster size best for that many groups (3 groups: C=16, all rows in
+    // registers, ~25% cheaper per round), after the full waves.
     if (C > 0 && !getenv("CX_SEL_C")) {
-        double best = 1e300;
-        int bc = C, bs = S, brs = Rs;
-        for (int c = C; c <= MAXC; ++c) {
-            const int s_ = (int)((g.L + c - 1) / c), rs = std::max(0, s_ - NT);
-            if (s_ > MAXRPT_ALL * NT || sel64_layout(rs, true).total > budget) continue;
-            const int act = active_clusters(c, rs, s_);
-            if (act <= 0) continue;
-            const double cost = (double)((g.G + act - 1) / act) * (3.6 + 0.0037 * s_);
-            if (cost < best * (1.0 - 1e-9)) {
-                best = cost;
-                bc = c; bs = s_; brs = rs;
+        int act = 0;
+        const double cost = best_cluster(g.G, g.L, C, budget, &C, &S, &Rs, &act);
+        const int full = act > 0 ? (g.G / act) * act : 0, rem = g.G - full;
+        if (full > 0 && rem > 0) {
+            int c2, s2, r2, a2, c1, s1, r1, a1;
+            const double cost2 = best_cluster(full, g.L, C, budget, &c1, &s1, &r1, &a1) +
+                                 best_cluster(rem, g.L, C, budget, &c2, &s2, &r2, &a2);
+            if (cost2 < cost * 0.98) {
+                GroupView ga = g, gb = g;
+                ga.G = full;
+                gb.G = rem;
+                gb.X = g.X + (int64_t)full * g.gstride;
+                const int64_t o = (int64_t)full * take;
+                return select64_launch(ga, attn, cen, take, lambda, flags, pick_rows, pick_scores, rows, scores, s) &&
+                       select64_launch(gb, attn + (int64_t)full * g.L, cen + (int64_t)full * D, take, lambda, flags,
+                                       pick_rows + o, pick_scores + o, rows + o, scores + o, s);
             }
         }
-        C = bc; S = bs; Rs = brs;
     }
     if (C == 0) {  // too large for one cluster on chip: rows beyond 512 stay in L2
         C = MAXC;
