@@ -346,6 +346,7 @@ template <int QPG>
 __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch b, float scale,
                                                                  unsigned long long* trc, int skip) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    if (threadIdx.x == 0) TC_TRACE(1001);  // kernel start (debugging only)
     const TcLayout lay = tc_layout(b.k_syn, QPG);
     const int NS = lay.ns;
     unsigned char* Kh = smem + lay.kh;
@@ -381,49 +382,55 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
         asm volatile("fence.mbarrier_init.release.cluster;");
         *epi_done = 0;
     }
-    {
-        const float* sk = b.syn_keys + (size_t)lh * ks * TD;
-        const float* sv = b.syn_values + (size_t)lh * ks * TD;
-        constexpr int IT = (TNS_MAX * 8 + TTHREADS - 1) / TTHREADS;
-        // K: item = (key j, 8-dim chunk c): two float4 loads, one hi and one lo store
-        float4 ka[IT], kb[IT];
-#pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            const int it = tid + k * TTHREADS, j = it >> 3, c = it & 7;
-            ka[k] = kb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (j < ks) {
-                ka[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c));
-                kb[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c) + 1);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            const int it = tid + k * TTHREADS, j = it >> 3, c = it & 7;
-            if (j < NS) {
-                const float x[8] = {ka[k].x, ka[k].y, ka[k].z, ka[k].w, kb[k].x, kb[k].y, kb[k].z, kb[k].w};
-                split8_store(x, Kh, Kl, cm_off(j, 8 * c, NS));  // B of S = Q K^T: N = keys, K = dims
-            }
-        }
-        // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
-#pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            const int it = tid + k * TTHREADS, c = it & (TD - 1), jc = it >> 6;
-            if (jc < NS / 8) {
-                float x[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int j = 8 * jc + u;
-                    x[u] = j < ks ? __ldg(sv + (size_t)j * TD + c) : 0.f;
-                }
-                split8_store(x, Vh, Vl, cm_off(c, 8 * jc, TD));  // B of O = P V: N = dims, K = keys
-            }
-        }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // barriers / TMEM base visible to all; the private warps start streaming right away
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (tid == 0) TC_TRACE(1000);
+    if (warp < SWARPS) {  // K_syn / V_syn^T staging: synapse warps only (the private rows never read them)
+        const float* sk = b.syn_keys + (size_t)lh * ks * TD;
+        const float* sv = b.syn_values + (size_t)lh * ks * TD;
+        constexpr int ST = SWARPS * 32, IT = 4;  // items per pass per thread (loads in flight)
+        // K: item = (key j, 8-dim chunk c): two float4 loads, one hi and one lo store
+        for (int base = 0; base < NS * 8; base += IT * ST) {
+            float4 ka[IT], kb[IT];
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int it = base + tid + k * ST, j = it >> 3, c = it & 7;
+                ka[k] = kb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (j < ks) {
+                    ka[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c));
+                    kb[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c) + 1);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int it = base + tid + k * ST, j = it >> 3, c = it & 7;
+                if (j < NS) {
+                    const float x[8] = {ka[k].x, ka[k].y, ka[k].z, ka[k].w, kb[k].x, kb[k].y, kb[k].z, kb[k].w};
+                    split8_store(x, Kh, Kl, cm_off(j, 8 * c, NS));  // B of S = Q K^T: N = keys, K = dims
+                }
+            }
+        }
+        // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
+        for (int base = 0; base < TD * (NS / 8); base += 2 * ST) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
+                if (jc < NS / 8) {
+                    float x[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = 8 * jc + u;
+                        x[u] = j < ks ? __ldg(sv + (size_t)j * TD + c) : 0.f;
+                    }
+                    split8_store(x, Vh, Vl, cm_off(c, 8 * jc, TD));  // B of O = P V: N = dims, K = keys
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_sync(1, SWARPS * 32);
+        if (tid == 0) TC_TRACE(1000);
+    }
     // TMEM columns: S [0, NS), O [NS, NS + 64), P hi [256, 256 + NS/2), P lo [256 + NS/2, 256 + NS)
     const uint32_t tS = *tbase_s, tO = tS + (uint32_t)NS, tPh = tS + 256u, tPl = tPh + (uint32_t)(NS / 2);
     const int n_tiles = (b.n_agents + AT - 1) / AT;
@@ -794,7 +801,8 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
         CX_CUDA(cudaStreamSynchronize(s));
         CX_CUDA(cudaMemcpy(h.data(), trc, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost));
         const double t0 = (double)h[1000];
-        fprintf(stderr, "decode_tc trace: grid %d x %d\n", n_lh, per_lh);
+        fprintf(stderr, "decode_tc trace: grid %d x %d, K/V_syn staging %.2f us\n", n_lh, per_lh,
+                (h[1000] - h[1001]) / 1e3);
         for (int ti = 0; ti < 62 && h[ti * 16]; ++ti) {
             fprintf(stderr, "tile %2d syn:", ti);
             for (int k = 0; k < 7; ++k) fprintf(stderr, " %7.2f", (h[ti * 16 + k] - t0) / 1e3);
