@@ -164,6 +164,8 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
         cudaStreamSynchronize(c->copy);
         cudaStreamDestroy(c->copy);
         for (cudaEvent_t e : c->hev) cudaEventDestroy(e);
+        for (cudaEvent_t e : c->pev) cudaEventDestroy(e);
+        if (c->aux) cx_ctx_destroy(c->aux);
         if (c->hbuf) cudaFree(c->hbuf);
         for (cudaStream_t& l : c->lane) {
             cudaStreamSynchronize(l);
@@ -562,7 +564,8 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         const size_t b_k = al(sizeof(float) * in_g * n_groups), b_q = al(sizeof(float) * q_g * n_groups);
         const size_t b_r = al(sizeof(int64_t) * take * n_groups), b_s = al(sizeof(double) * take * n_groups);
         const size_t b_o = al(sizeof(float) * o_g * n_groups);
-        const size_t need = 2 * b_k + b_q + b_r + b_s + 2 * b_o;
+        const size_t b_a = al(sizeof(double) * (size_t)count * n_groups), b_c = al(sizeof(double) * dim * n_groups);
+        const size_t need = 2 * b_k + b_q + b_r + b_s + 2 * b_o + b_a + b_c;
         if (need > c->hcap) {
             if (c->hbuf) {
                 CX_CUDA(cudaStreamSynchronize(c->stream));
@@ -580,7 +583,9 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         int64_t* dr = reinterpret_cast<int64_t*>(p); p += b_r;
         double* ds = reinterpret_cast<double*>(p); p += b_s;
         float* dsk = reinterpret_cast<float*>(p); p += b_o;
-        float* dsv = reinterpret_cast<float*>(p);
+        float* dsv = reinterpret_cast<float*>(p); p += b_o;
+        double* dattn = reinterpret_cast<double*>(p); p += b_a;
+        double* dcen = reinterpret_cast<double*>(p);
         // Chunks of groups, one selection wave each (15 co-resident 8-CTA clusters on
         // B200), so chunking costs no compute; the remainder goes FIRST so that the
         // only exposed upload is the smallest one.
@@ -591,10 +596,41 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         const int nch = (int)start.size();
         start.push_back(n_groups);
         while ((int)c->hev.size() < nch) {
-            cudaEvent_t e;
+            cudaEvent_t e, f;
             CX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CX_CUDA(cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
             c->hev.push_back(e);
+            c->pev.push_back(f);
         }
+        // The prologue of each chunk (centroid + attention mass: latency-bound, few SMs)
+        // runs on a second context while the previous chunk's selection holds the rest
+        // of the GPU; scratch is sized once for the largest chunk.
+        if (!c->aux) {
+            auto* a = new cx_ctx();
+            try {
+                ctx_init(a, c->device);
+            } catch (...) {
+                delete a;
+                throw;
+            }
+            c->aux = a;
+        }
+        cx_ctx* x = c->aux;
+        {
+            int maxg = 0;
+            for (int i = 0; i < nch; ++i) maxg = std::max(maxg, start[i + 1] - start[i]);
+            cx_groups gm = all;
+            gm.n_groups = maxg;
+            GroupView vm = view_of(&gm);
+            ArenaPlan pa, ps;
+            plan_attention(pa, vm);
+            plan_select(ps, vm, k);
+            CX_CUDA(cudaStreamSynchronize(x->stream));
+            x->arena.reserve(pa.used);
+            CX_CUDA(cudaStreamSynchronize(c->stream));
+            c->arena.reserve(ps.used);
+        }
+        CX_CUDA(cudaMemsetAsync(x->d_flag, 0, sizeof(int), x->stream));
         CX_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
         for (int i = 0; i < nch; ++i) {  // all uploads queued on the copy stream
             const int g0 = start[i], ng = start[i + 1] - g0;
@@ -603,15 +639,32 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
             CX_CUDA(cudaMemcpyAsync(dq + g0 * q_g, queries + g0 * q_g, sizeof(float) * q_g * ng, cudaMemcpyHostToDevice, c->copy));
             CX_CUDA(cudaEventRecord(c->hev[i], c->copy));
         }
-        for (int i = 0; i < nch; ++i) {  // chunk i computes as soon as its upload lands
+        for (int i = 0; i < nch; ++i) {  // prologues: as soon as each upload lands
             const int g0 = start[i], ng = start[i + 1] - g0;
-            CX_CUDA(cudaStreamWaitEvent(c->stream, c->hev[i], 0));
+            CX_CUDA(cudaStreamWaitEvent(x->stream, c->hev[i], 0));
             cx_groups gi = all;
             gi.n_groups = ng;
             gi.clouds = dk + g0 * in_g;
             gi.queries = dq + g0 * q_g;
-            compress_impl(c, &gi, dv + g0 * in_g, k, lambda, flags, dr + (size_t)g0 * take, ds + (size_t)g0 * take,
-                          dsk + g0 * o_g, dsv + g0 * o_g, c->stream);
+            const GroupView g = view_of(&gi);
+            centroid_launch(g, dcen + (size_t)g0 * dim, x->stream);
+            x->arena.reset();
+            attention_grouped(x, g, dattn + (size_t)g0 * count, x->stream);
+            CX_CUDA(cudaEventRecord(c->pev[i], x->stream));
+        }
+        for (int i = 0; i < nch; ++i) {  // selection + gather of chunk i after its prologue
+            const int g0 = start[i], ng = start[i + 1] - g0;
+            CX_CUDA(cudaStreamWaitEvent(c->stream, c->pev[i], 0));
+            cx_groups gi = all;
+            gi.n_groups = ng;
+            gi.clouds = dk + g0 * in_g;
+            gi.queries = dq + g0 * q_g;
+            const GroupView g = view_of(&gi);
+            c->arena.reset();
+            select_grouped(c, g, dattn + (size_t)g0 * count, k, lambda, flags, dr + (size_t)g0 * take,
+                           ds + (size_t)g0 * take, c->stream, dcen + (size_t)g0 * dim);
+            gather_rows(g, g.X, dr + (size_t)g0 * take, take, dsk + g0 * o_g, c->stream);
+            gather_rows(g, dv + g0 * in_g, dr + (size_t)g0 * take, take, dsv + g0 * o_g, c->stream);
         }
         CX_CUDA(cudaMemcpyAsync(out_rows, dr, sizeof(int64_t) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));
         CX_CUDA(cudaMemcpyAsync(out_scores, ds, sizeof(double) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));
@@ -619,7 +672,8 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
             CX_CUDA(cudaMemcpyAsync(syn_keys, dsk, sizeof(float) * o_g * n_groups, cudaMemcpyDeviceToHost, c->stream));
         if (syn_values)
             CX_CUDA(cudaMemcpyAsync(syn_values, dsv, sizeof(float) * o_g * n_groups, cudaMemcpyDeviceToHost, c->stream));
-        check_flag_and_sync(c);  // non-finite attention input -> precondition_error (kernels.cpp:70)
+        check_flag_and_sync(x);  // non-finite attention input -> precondition_error (kernels.cpp:70)
+        check_flag_and_sync(c);
     });
 }
 

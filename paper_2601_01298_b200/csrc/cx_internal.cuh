@@ -105,6 +105,8 @@ struct cx_ctx {
     char* hbuf = nullptr;           // host-path device staging (grow-only, separate from the arena)
     size_t hcap = 0;
     std::vector<cudaEvent_t> hev;   // per-chunk upload events
+    std::vector<cudaEvent_t> pev;   // per-chunk prologue (centroid + attention) events
+    cx_ctx* aux = nullptr;          // host path: prologue context (own stream, arena, flag)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cx::Arena arena;                // device scratch
     int* d_flag = nullptr;          // device-side error flag (softmax non-finite, ...)
