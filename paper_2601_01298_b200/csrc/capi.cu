@@ -685,8 +685,9 @@ extern "C" cx_status cx_decode_step_dev(cx_ctx* c, const cx_decode_batch* b, voi
             fail(CX_PRECONDITION_ERROR, "decode_step: bad shape");
         if (b->n_q / b->n_kv > 8) fail(CX_PRECONDITION_ERROR, "decode_step: more than 8 q-heads per KV head");
         if (b->n_agents == 0) return;
-        if (!b->syn_keys || !b->syn_values || !b->tail_keys || !b->tail_values || !b->tail_len || !b->q || !b->out)
-            fail(CX_INVALID_ARGUMENT, "null pointer");
+        if ((b->k_syn > 0 && (!b->syn_keys || !b->syn_values)) || !b->tail_keys || !b->tail_values || !b->tail_len ||
+            !b->q || !b->out)
+            fail(CX_INVALID_ARGUMENT, "null pointer");  // an empty synapse (k_syn = 0) may pass NULL
         if ((b->new_keys == nullptr) != (b->new_values == nullptr))
             fail(CX_INVALID_ARGUMENT, "new_keys/new_values must both be set or both NULL");
         decode_step(c, *b, (cudaStream_t)stream);

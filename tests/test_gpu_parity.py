@@ -444,3 +444,38 @@ def test_bench_landmarks_on_b200(cx, orc):
         rnd = orc.random_subset(r, 256, 16)
         wins += cx.hausdorff_to_subset(cloud, hyb) <= cx.hausdorff_to_subset(cloud, rnd)
     assert wins / 100 == exp["hybrid_win_rate"] and wins >= 90
+
+
+@pytest.mark.parametrize("k,Tc", [(0, 33), (20, 80), (164, 33)])
+def test_decode_default_dispatch_edges(dev, orc, k, Tc):
+    """No pin: the default dispatch (tcgen05 -> v2 -> v1) on shapes the tcgen05
+    kernel declines -- an empty synapse (k_syn = 0: a snapshot before the river has
+    context) and more private rows than it stages (t_cap > 64) -- plus the common case."""
+    import torch
+    gen = torch.Generator(device="cuda").manual_seed(5 + k + Tc)
+    N, Lr, H, Q, dk = 6, 2, 2, 14, 64
+    syn_k = torch.randn(Lr, H, max(k, 1), dk, device="cuda", generator=gen)[:, :, :k].contiguous()
+    syn_v = torch.randn(Lr, H, max(k, 1), dk, device="cuda", generator=gen)[:, :, :k].contiguous()
+    tk = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
+    tv = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
+    tl = torch.randint(0, Tc, (N,), device="cuda", generator=gen).to(torch.int32)
+    nk = torch.randn(N, Lr, H, dk, device="cuda", generator=gen)
+    nv = torch.randn(N, Lr, H, dk, device="cuda", generator=gen)
+    q = torch.randn(N, Lr, Q, dk, device="cuda", generator=gen)
+    out = torch.empty_like(q)
+    dev.decode_step(syn_k, syn_v, tk, tv, tl, q, out, nk, nv)
+    torch.cuda.synchronize()
+    o, tkn, tvn, tln = out.cpu().numpy(), tk.cpu().numpy(), tv.cpu().numpy(), tl.cpu().numpy()
+    sk, sv, qn = syn_k.cpu().numpy(), syn_v.cpu().numpy(), q.cpu().numpy()
+    worst = 0.0
+    for a in range(N):
+        n_t = int(tln[a]) + 1
+        for l in range(Lr):
+            for g in range(H):
+                kk = np.concatenate([sk[l, g], tkn[a, l, g, :n_t]])
+                vv = np.concatenate([sv[l, g], tvn[a, l, g, :n_t]])
+                for hh in range(Q // H):
+                    h = g * (Q // H) + hh
+                    exp = orc.attend(qn[a, l, h], kk, vv, k + n_t, 1, dk)
+                    worst = max(worst, float(np.max(np.abs(o[a, l, h] - exp) / np.maximum(1.0, np.abs(exp)))))
+    assert worst <= 1e-3, worst
