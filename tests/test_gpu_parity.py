@@ -479,3 +479,32 @@ def test_decode_default_dispatch_edges(dev, orc, k, Tc):
                     exp = orc.attend(qn[a, l, h], kk, vv, k + n_t, 1, dk)
                     worst = max(worst, float(np.max(np.abs(o[a, l, h] - exp) / np.maximum(1.0, np.abs(exp)))))
     assert worst <= 1e-3, worst
+
+
+@pytest.mark.parametrize("G,L,k,lam,flags", [
+    (3, 30, 40, 0.5, 0),     # k > L: every row is taken (synapse.cpp take = min(k, L))
+    (2, 1, 5, 0.5, 0),       # a single row
+    (3, 513, 513, 0.3, 0),   # k = L, just past one register row per thread
+    (4, 1000, 1, 0.5, 0),    # one pick
+    (2, 4100, 50, 0.0, 0),   # lambda = 0: pure attention order
+    (2, 4100, 50, 1.0, 0),   # lambda = 1: pure coverage
+    (5, 2048, 40, 0.5, 2),   # the generic kernel on cfg1-sized groups
+])
+def test_grouped_compress_edge_shapes(dev, orc, G, L, k, lam, flags):
+    """Grouped compression on edge shapes == the reference per group (rows bitwise,
+    gathered K/V bitwise)."""
+    import torch
+    ks, vs, qs = zip(*[oracle.synthetic_group(orc, 900 + 13 * gi + L, L, 64, 7) for gi in range(G)])
+    kt = torch.from_numpy(np.stack(ks)).cuda()
+    vt = torch.from_numpy(np.stack(vs)).cuda()
+    qt = torch.from_numpy(np.stack(qs)).cuda()
+    rows, scores, sk, sv = dev.compress_grouped(kt, vt, qt, k, lam, flags=flags)
+    torch.cuda.synchronize()
+    take = min(k, L)
+    assert rows.shape == (G, take)
+    rows, sk, sv = rows.cpu().numpy(), sk.cpu().numpy(), sv.cpu().numpy()
+    for gi in range(G):
+        a = oracle.group_attention(orc, ks[gi], qs[gi])
+        idx, _ = orc.select_landmarks_points(ks[gi], a, k, lam)
+        assert np.array_equal(rows[gi], idx), (gi, rows[gi][:8], idx[:8])
+        assert np.array_equal(sk[gi], ks[gi][idx]) and np.array_equal(sv[gi], vs[gi][idx])
