@@ -22,6 +22,7 @@
 // cluster-wide barrier per round).  Every decision is bit-identical to the
 // reference.
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
 
 #include <map>
 #include <mutex>
@@ -38,6 +39,11 @@ constexpr int D = 64;
 constexpr int NT = 512;          // threads per CTA (one register row each)
 constexpr int NW = NT / 32;
 constexpr int QCAP = 160;        // exact-evaluation queue capacity per pass
+constexpr int QCAP_SK = 64;      // ... in sketch mode (leaves room for 1536 sketch rows)
+// Rows beyond the 512 register rows of a CTA live in shared memory as fp32
+// (ROWS_SMEM), or as an fp16 SKETCH there with the exact fp32 rows read from L2
+// by the few exact evaluations (ROWS_SKETCH), or are read from L2 every round.
+enum : int { ROWS_L2 = 0, ROWS_SMEM = 1, ROWS_SKETCH = 2 };
 constexpr int SPITCH = D + 1;    // staged-row pitch (conflict-free column reads)
 constexpr int MAXC = 16;
 constexpr int MAXRPT_ALL = 4;    // rows per thread (S <= 2048)
@@ -131,7 +137,8 @@ struct Sel64Layout {
 
 __host__ __device__ inline size_t al(size_t x, size_t a = 16) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline Sel64Layout sel64_layout(int Rs, bool smem_rows) {
+__host__ __device__ inline Sel64Layout sel64_layout(int Rs, int mode) {
+    const int qcap = mode == ROWS_SKETCH ? QCAP_SK : QCAP;
     Sel64Layout l;
     size_t o = 0;
     l.mbar = o;  o = al(o + 2 * sizeof(uint64_t));
@@ -141,10 +148,11 @@ __host__ __device__ inline Sel64Layout sel64_layout(int Rs, bool smem_rows) {
     l.cand = o;  o = al(o + sizeof(float) * D + sizeof(Hdr)); // this CTA's candidate (coords + header)
     l.hw = o;    o = al(o + sizeof(double) * 4 * NW);         // per-warp partials
     l.misc = o;  o = al(o + sizeof(unsigned long long) * 8);  // counters / atomics
-    l.qown = o;  o = al(o + sizeof(int) * QCAP);
-    l.qres = o;  o = al(o + sizeof(double) * 2 * QCAP);
-    l.stage = o; o = al(o + sizeof(float) * QCAP * SPITCH);
-    l.xs = o;    o = al(o + (smem_rows ? sizeof(float) * (size_t)Rs * D : 0));
+    l.qown = o;  o = al(o + sizeof(int) * qcap);
+    l.qres = o;  o = al(o + sizeof(double) * 2 * qcap);
+    l.stage = o; o = al(o + sizeof(float) * qcap * SPITCH);
+    l.xs = o;    o = al(o + (mode == ROWS_SMEM ? sizeof(float) * (size_t)Rs * D
+                             : mode == ROWS_SKETCH ? sizeof(__half) * (size_t)Rs * D : 0));
     l.total = o;
     return l;
 }
@@ -225,8 +233,21 @@ __device__ __forceinline__ float gram_lower_bound(float nx, float nb, float dot)
     return __fsub_rd(s, e);
 }
 
-template <int RPT, bool SMEM_ROWS>
+// The same bound when x is only known through its fp16 rounding x~ (the sketch):
+// |x_c - x~_c| <= 2^-11 |x_c| + 2^-25 (subnormals), so |2 (x - x~).b| <= 2^-11 (|x|^2 +
+// |b|^2) + 2^-21 |b|, added to the slack.  An fp16 overflow makes the dot inf/NaN,
+// the comparison false, and the row is evaluated exactly.
+__device__ __forceinline__ float gram_lower_bound_sketch(float nx, float nb, float dot) {
+    const float sum = __fadd_rn(nx, nb);
+    const float s = __fsub_rn(sum, __fmul_rn(2.0f, dot));
+    const float e = __fadd_ru(__fmaf_ru(0x1p-18f + 0x1p-11f, sum, 0x1p-100f), __fmul_ru(0x1p-21f, __fsqrt_ru(nb)));
+    return __fsub_rd(s, e);
+}
+
+template <int RPT, int ROWMODE>
 __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
+    constexpr bool SMEM_ROWS = ROWMODE == ROWS_SMEM;
+    constexpr int qcap = ROWMODE == ROWS_SKETCH ? QCAP_SK : QCAP;
     constexpr int MAXRPT = RPT;  // rows per thread of this instantiation
     cg::cluster_group cluster = cg::this_cluster();
     const uint32_t C = cluster.num_blocks();
@@ -240,7 +261,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
     int round = -1;  // for STAMP outside the loop
 
     extern __shared__ __align__(16) unsigned char smem[];
-    const Sel64Layout lay = sel64_layout(p.Rs, SMEM_ROWS);
+    const Sel64Layout lay = sel64_layout(p.Rs, ROWMODE);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     double* mm = reinterpret_cast<double*>(smem + lay.mm);
     Hdr* hdr = reinterpret_cast<Hdr*>(smem + lay.hdr);
@@ -253,6 +274,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
     double* qres = reinterpret_cast<double*>(smem + lay.qres);
     float* stage = reinterpret_cast<float*>(smem + lay.stage);
     float4* xs4 = reinterpret_cast<float4*>(smem + lay.xs);  // [D/4][Rs] float4
+    uint4* xh8 = reinterpret_cast<uint4*>(smem + lay.xs);    // sketch: [D/8][Rs] x 8 halves
     int* qn = reinterpret_cast<int*>(&misc[0]);              // queue length
     unsigned long long* hkey = &misc[1];                      // max exact score bits
     unsigned long long* hrow = &misc[2];                      // min row among ties
@@ -279,6 +301,35 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
             xs4[(size_t)c4 * p.Rs + j] = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)(NT + j) * p.rstride) + c4);
         }
     }
+    if (ROWMODE == ROWS_SKETCH) {
+        for (int e = tid; e < nsm * (D / 8); e += NT) {
+            const int j = e / (D / 8), c8 = e % (D / 8);
+            const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)(NT + j) * p.rstride) + 2 * c8;
+            const float4 u = __ldg(src), v = __ldg(src + 1);
+            const __half2 h0 = __floats2half2_rn(u.x, u.y), h1 = __floats2half2_rn(u.z, u.w);
+            const __half2 h2 = __floats2half2_rn(v.x, v.y), h3 = __floats2half2_rn(v.z, v.w);
+            xh8[(size_t)c8 * p.Rs + j] = make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                                                    *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
+        }
+    }
+    // x~ . b over the fp16 sketch of row NT + j
+    auto sketch_dot = [&](int j, const float* b) {
+        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int c8 = 0; c8 < D / 8; ++c8) {
+            const uint4 u = xh8[(size_t)c8 * p.Rs + j];
+            const float4 w0 = reinterpret_cast<const float4*>(b)[2 * c8], w1 = reinterpret_cast<const float4*>(b)[2 * c8 + 1];
+            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+            const float2 f3 = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+            s0 = ffma2(f0, make_float2(w0.x, w0.y), s0);
+            s1 = ffma2(f1, make_float2(w0.z, w0.w), s1);
+            s0 = ffma2(f2, make_float2(w1.x, w1.y), s0);
+            s1 = ffma2(f3, make_float2(w1.z, w1.w), s1);
+        }
+        return (s0.x + s0.y) + (s1.x + s1.y);
+    };
     auto reg4 = [&](int c4) { return make_float4(xr[4 * c4], xr[4 * c4 + 1], xr[4 * c4 + 2], xr[4 * c4 + 3]); };
     auto far4 = [&](int j) {  // row NT + j
         return [&, j](int c4) -> float4 {
@@ -350,12 +401,16 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                 if (assign || !p.filter) {
                     need = true;
                 } else {
-                    const float dt = (k == 0) ? dot_f32x2(reg4, bw) : dot_f32x2<4>(far4(tid + k * NT - NT), bw);
-                    need = !(gram_lower_bound(nx[k], nbw, dt) > th[k]);
+                    if (ROWMODE == ROWS_SKETCH && k > 0) {
+                        need = !(gram_lower_bound_sketch(nx[k], nbw, sketch_dot(tid + k * NT - NT, bw)) > th[k]);
+                    } else {
+                        const float dt = (k == 0) ? dot_f32x2(reg4, bw) : dot_f32x2<4>(far4(tid + k * NT - NT), bw);
+                        need = !(gram_lower_bound(nx[k], nbw, dt) > th[k]);
+                    }
                 }
                 if (!need) continue;
                 const int sl = atomicAdd(qn, 1);
-                if (sl < QCAP) {
+                if (sl < qcap) {
                     slot[k] = sl;
                     qown[sl] = tid;
                     float* st = stage + sl * SPITCH;
@@ -374,7 +429,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                 }
             }
             __syncthreads();
-            const int nq = min(qn[0], QCAP);
+            const int nq = min(qn[0], qcap);
             if (tid < nq) {
                 const float* st = stage + tid * SPITCH;
                 const double d2 = exact_sq<2>([&](int c4) {
@@ -601,13 +656,13 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
 static int active_clusters(int C, int Rs, int S) {
     static std::mutex mu;
     static std::map<std::pair<int, int>, int> cache;
-    const size_t smem = sel64_layout(Rs, true).total;
+    const size_t smem = sel64_layout(Rs, ROWS_SMEM).total;
     std::lock_guard<std::mutex> lk(mu);
     const auto key = std::make_pair(C, (int)smem);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     const int rpt = (S + NT - 1) / NT;
-    void (*kern)(Sel64Params) = rpt <= 1 ? select64_kernel<1, true> : rpt <= 2 ? select64_kernel<2, true> : select64_kernel<4, true>;
+    void (*kern)(Sel64Params) = rpt <= 1 ? select64_kernel<1, ROWS_SMEM> : rpt <= 2 ? select64_kernel<2, ROWS_SMEM> : select64_kernel<4, ROWS_SMEM>;
     int n = 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess) {
         if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -638,7 +693,7 @@ static double best_cluster(int G, int64_t L, int c_min, size_t budget, int* C, i
     double best = 1e300;
     for (int c = c_min; c <= MAXC; ++c) {
         const int s_ = (int)((L + c - 1) / c), rs = std::max(0, s_ - NT);
-        if (s_ > MAXRPT_ALL * NT || sel64_layout(rs, true).total > budget) continue;
+        if (s_ > MAXRPT_ALL * NT || sel64_layout(rs, ROWS_SMEM).total > budget) continue;
         const int act = active_clusters(c, rs, s_);
         if (act <= 0) continue;
         const double cost = (double)((G + act - 1) / act) * (3.6 + 0.0037 * s_);
@@ -667,11 +722,10 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
     const size_t budget = (size_t)max_optin - 2048;
     // smallest cluster whose slice fits on chip (512 register rows + shared rows)
     int C = 0, S = 0, Rs = 0;
-    bool smem_rows = true;
     for (int c = 1; c <= MAXC; c *= 2) {
         const int s_ = (int)((g.L + c - 1) / c);
         const int rs = std::max(0, s_ - NT);
-        if (s_ <= MAXRPT_ALL * NT && sel64_layout(rs, true).total <= budget) {
+        if (s_ <= MAXRPT_ALL * NT && sel64_layout(rs, ROWS_SMEM).total <= budget) {
             C = c; S = s_; Rs = rs;
             break;
         }
@@ -680,7 +734,7 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
         const int c = atoi(force);
         const int s_ = (int)((g.L + c - 1) / c);
         const int rs = std::max(0, s_ - NT);
-        if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT && sel64_layout(rs, true).total <= budget) {
+        if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT && sel64_layout(rs, ROWS_SMEM).total <= budget) {
             C = c; S = s_; Rs = rs;
         }
     }
@@ -708,12 +762,13 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
             }
         }
     }
-    if (C == 0) {  // too large for one cluster on chip: rows beyond 512 stay in L2
+    int mode = ROWS_SMEM;
+    if (C == 0) {  // too large for one cluster on chip: an fp16 sketch of the rows beyond 512, or L2
         C = MAXC;
         S = (int)((g.L + C - 1) / C);
         Rs = std::max(0, S - NT);
-        smem_rows = false;
         if (S > MAXRPT_ALL * NT) return false;
+        mode = (sel64_layout(Rs, ROWS_SKETCH).total <= budget && !getenv("CX_SEL_NOSKETCH")) ? ROWS_SKETCH : ROWS_L2;
     }
     Sel64Params prm;
     prm.X = g.X;
@@ -735,11 +790,15 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 8 * 4096));
     if (tr && tr[0] == 'p') prm.trace = (long long*)1;
-    const size_t smem = sel64_layout(Rs, smem_rows).total;
+    const size_t smem = sel64_layout(Rs, mode).total;
     const int rpt = (S + NT - 1) / NT;
     void (*kern)(Sel64Params) = nullptr;
-    if (smem_rows) kern = rpt <= 1 ? select64_kernel<1, true> : rpt <= 2 ? select64_kernel<2, true> : select64_kernel<4, true>;
-    else kern = rpt <= 1 ? select64_kernel<1, false> : rpt <= 2 ? select64_kernel<2, false> : select64_kernel<4, false>;
+    if (mode == ROWS_SMEM)
+        kern = rpt <= 1 ? select64_kernel<1, ROWS_SMEM> : rpt <= 2 ? select64_kernel<2, ROWS_SMEM> : select64_kernel<4, ROWS_SMEM>;
+    else if (mode == ROWS_SKETCH)
+        kern = rpt <= 1 ? select64_kernel<1, ROWS_SKETCH> : rpt <= 2 ? select64_kernel<2, ROWS_SKETCH> : select64_kernel<4, ROWS_SKETCH>;
+    else
+        kern = rpt <= 1 ? select64_kernel<1, ROWS_L2> : rpt <= 2 ? select64_kernel<2, ROWS_L2> : select64_kernel<4, ROWS_L2>;
     CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (C > 8) CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
@@ -780,9 +839,9 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
             acc[5] += (double)(prm.trace[(r + 1) * 8] - t[0]);
         }
         if (n > 0)
-            fprintf(stderr, "select64 C=%d S=%d Rs=%d smem_rows=%d cycles/round: U=%.0f X1send=%.0f X1wait=%.0f "
+            fprintf(stderr, "select64 C=%d S=%d Rs=%d rows=%d cycles/round: U=%.0f X1send=%.0f X1wait=%.0f "
                             "H=%.0f X2=%.0f total=%.0f\n",
-                    C, S, Rs, (int)smem_rows, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
+                    C, S, Rs, mode, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
         cudaFree(prm.trace);
     }
     return true;
