@@ -653,16 +653,25 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
 // Host side: choose the cluster size and residency, launch.  Returns false
 // when the dim-64 kernel does not apply (caller uses the generic kernel).
 // co-resident clusters of size C for the on-chip (shared-memory rows) kernel, cached
-static int active_clusters(int C, int Rs, int S) {
+static void (*sel64_kernel_for(int rpt, int mode))(Sel64Params) {
+    if (mode == ROWS_SMEM)
+        return rpt <= 1 ? select64_kernel<1, ROWS_SMEM> : rpt <= 2 ? select64_kernel<2, ROWS_SMEM> : select64_kernel<4, ROWS_SMEM>;
+    if (mode == ROWS_SKETCH)
+        return rpt <= 1 ? select64_kernel<1, ROWS_SKETCH> : rpt <= 2 ? select64_kernel<2, ROWS_SKETCH>
+                                                              : select64_kernel<4, ROWS_SKETCH>;
+    return rpt <= 1 ? select64_kernel<1, ROWS_L2> : rpt <= 2 ? select64_kernel<2, ROWS_L2> : select64_kernel<4, ROWS_L2>;
+}
+
+static int active_clusters(int C, int Rs, int S, int mode = ROWS_SMEM) {
     static std::mutex mu;
     static std::map<std::pair<int, int>, int> cache;
-    const size_t smem = sel64_layout(Rs, ROWS_SMEM).total;
+    const size_t smem = sel64_layout(Rs, mode).total;
     std::lock_guard<std::mutex> lk(mu);
-    const auto key = std::make_pair(C, (int)smem);
+    const auto key = std::make_pair(C * 4 + mode, (int)smem);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     const int rpt = (S + NT - 1) / NT;
-    void (*kern)(Sel64Params) = rpt <= 1 ? select64_kernel<1, ROWS_SMEM> : rpt <= 2 ? select64_kernel<2, ROWS_SMEM> : select64_kernel<4, ROWS_SMEM>;
+    void (*kern)(Sel64Params) = sel64_kernel_for(rpt, mode);
     int n = 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess) {
         if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -689,17 +698,27 @@ static int active_clusters(int C, int Rs, int S) {
 // on B200 (C=8: 7.4 us, C=9: 7.2 us, C=16: 5.5 us at L=8192); waves = ceil(G /
 // co-resident clusters).  cfg2 (G=48): C=9 (4.71 vs 4.86 ms at C=8); G <= 7 (one
 // group, or cfg2 over 8 GPUs): C=16.  Returns the estimated cost (us per round).
-static double best_cluster(int G, int64_t L, int c_min, size_t budget, int* C, int* S, int* Rs, int* act_out) {
+static double best_cluster(int G, int64_t L, size_t budget, int* C, int* S, int* Rs, int* mode, int* act_out) {
     double best = 1e300;
-    for (int c = c_min; c <= MAXC; ++c) {
+    const bool sketch_ok = !getenv("CX_SEL_NOSKETCH");
+    for (int c = 1; c <= MAXC; ++c) {
         const int s_ = (int)((L + c - 1) / c), rs = std::max(0, s_ - NT);
-        if (s_ > MAXRPT_ALL * NT || sel64_layout(rs, ROWS_SMEM).total > budget) continue;
-        const int act = active_clusters(c, rs, s_);
+        if (s_ > MAXRPT_ALL * NT) continue;
+        // fp32 rows on chip if they fit, else the fp16 sketch (rows re-read from L2 only
+        // by the exact evaluations); the sketch costs ~3% more per round (measured at S=2048)
+        int md = ROWS_SMEM;
+        double per = 3.6 + 0.0037 * s_;
+        if (sel64_layout(rs, ROWS_SMEM).total > budget) {
+            if (!sketch_ok || sel64_layout(rs, ROWS_SKETCH).total > budget) continue;
+            md = ROWS_SKETCH;
+            per *= 1.03;
+        }
+        const int act = active_clusters(c, rs, s_, md);
         if (act <= 0) continue;
-        const double cost = (double)((G + act - 1) / act) * (3.6 + 0.0037 * s_);
+        const double cost = (double)((G + act - 1) / act) * per;
         if (cost < best * (1.0 - 1e-9)) {
             best = cost;
-            *C = c; *S = s_; *Rs = rs;
+            *C = c; *S = s_; *Rs = rs; *mode = md;
             *act_out = act;
         }
     }
@@ -720,36 +739,26 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
             max_optin = 232448;
     }
     const size_t budget = (size_t)max_optin - 2048;
-    // smallest cluster whose slice fits on chip (512 register rows + shared rows)
-    int C = 0, S = 0, Rs = 0;
-    for (int c = 1; c <= MAXC; c *= 2) {
-        const int s_ = (int)((g.L + c - 1) / c);
-        const int rs = std::max(0, s_ - NT);
-        if (s_ <= MAXRPT_ALL * NT && sel64_layout(rs, ROWS_SMEM).total <= budget) {
-            C = c; S = s_; Rs = rs;
-            break;
-        }
-    }
+    // Cluster size and row mode by the cost model (best_cluster): waves x per-round cost
+    // over every C whose rows fit on chip as fp32 or as the fp16 sketch.  A partial last
+    // wave (e.g. 48 = 15 + 15 + 15 + 3 clusters) runs as its own launch with the
+    // configuration best for that many groups, after the full waves.
+    int C = 0, S = 0, Rs = 0, mode = ROWS_SMEM, act = 0;
     if (const char* force = getenv("CX_SEL_C")) {  // debugging / tuning: force a cluster size
         const int c = atoi(force);
-        const int s_ = (int)((g.L + c - 1) / c);
-        const int rs = std::max(0, s_ - NT);
-        if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT && sel64_layout(rs, ROWS_SMEM).total <= budget) {
+        const int s_ = (int)((g.L + c - 1) / c), rs = std::max(0, s_ - NT);
+        if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT) {
             C = c; S = s_; Rs = rs;
+            mode = sel64_layout(rs, ROWS_SMEM).total <= budget ? ROWS_SMEM
+                   : sel64_layout(rs, ROWS_SKETCH).total <= budget ? ROWS_SKETCH : ROWS_L2;
         }
-    }
-    // cluster size by the cost model (best_cluster)
-    // A partial last wave (cfg2: 48 = 15 + 15 + 15 + 3 clusters) runs as its own launch
-    // with the cluster size best for that many groups (3 groups: C=16, all rows in
-    // registers, ~25% cheaper per round), after the full waves.
-    if (C > 0 && !getenv("CX_SEL_C")) {
-        int act = 0;
-        const double cost = best_cluster(g.G, g.L, C, budget, &C, &S, &Rs, &act);
+    } else {
+        const double cost = best_cluster(g.G, g.L, budget, &C, &S, &Rs, &mode, &act);
         const int full = act > 0 ? (g.G / act) * act : 0, rem = g.G - full;
-        if (full > 0 && rem > 0) {
-            int c2, s2, r2, a2, c1, s1, r1, a1;
-            const double cost2 = best_cluster(full, g.L, C, budget, &c1, &s1, &r1, &a1) +
-                                 best_cluster(rem, g.L, C, budget, &c2, &s2, &r2, &a2);
+        if (C > 0 && full > 0 && rem > 0) {
+            int c1, s1, r1, m1, a1, c2, s2, r2, m2, a2;
+            const double cost2 = best_cluster(full, g.L, budget, &c1, &s1, &r1, &m1, &a1) +
+                                 best_cluster(rem, g.L, budget, &c2, &s2, &r2, &m2, &a2);
             if (cost2 < cost * 0.98) {
                 GroupView ga = g, gb = g;
                 ga.G = full;
@@ -762,13 +771,12 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
             }
         }
     }
-    int mode = ROWS_SMEM;
-    if (C == 0) {  // too large for one cluster on chip: an fp16 sketch of the rows beyond 512, or L2
+    if (C == 0) {  // nothing fits on chip: rows beyond 512 per CTA are read from L2 every round
         C = MAXC;
         S = (int)((g.L + C - 1) / C);
         Rs = std::max(0, S - NT);
         if (S > MAXRPT_ALL * NT) return false;
-        mode = (sel64_layout(Rs, ROWS_SKETCH).total <= budget && !getenv("CX_SEL_NOSKETCH")) ? ROWS_SKETCH : ROWS_L2;
+        mode = ROWS_L2;
     }
     Sel64Params prm;
     prm.X = g.X;
@@ -792,13 +800,7 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
     if (tr && tr[0] == 'p') prm.trace = (long long*)1;
     const size_t smem = sel64_layout(Rs, mode).total;
     const int rpt = (S + NT - 1) / NT;
-    void (*kern)(Sel64Params) = nullptr;
-    if (mode == ROWS_SMEM)
-        kern = rpt <= 1 ? select64_kernel<1, ROWS_SMEM> : rpt <= 2 ? select64_kernel<2, ROWS_SMEM> : select64_kernel<4, ROWS_SMEM>;
-    else if (mode == ROWS_SKETCH)
-        kern = rpt <= 1 ? select64_kernel<1, ROWS_SKETCH> : rpt <= 2 ? select64_kernel<2, ROWS_SKETCH> : select64_kernel<4, ROWS_SKETCH>;
-    else
-        kern = rpt <= 1 ? select64_kernel<1, ROWS_L2> : rpt <= 2 ? select64_kernel<2, ROWS_L2> : select64_kernel<4, ROWS_L2>;
+    void (*kern)(Sel64Params) = sel64_kernel_for(rpt, mode);
     CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (C > 8) CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
