@@ -584,7 +584,9 @@ def run_e2e(args, dev):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    h2d = (hk.numel() + hv.numel() + hq.numel()) * 4
+    # keys and queries are uploaded; values cross PCIe only at the selected rows (the
+    # pinned buffer is read zero-copy by the gather: G x K rows x D floats)
+    h2d = (hk.numel() + hq.numel()) * 4 + G * K * D * 4
     d2h = h_rows.numel() * 8 + h_out[1].numel() * 8 + (h_sk.numel() + h_sv.numel()) * 4
     return {"value": 1000.0 / ms, "unit": "compressions/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms}

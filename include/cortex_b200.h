@@ -158,7 +158,9 @@ cx_status cx_compress_grouped_dev(cx_ctx* ctx, const cx_groups* g, const float* 
  * in cx_groups); outputs (host): rows/scores [G][take], syn_keys/syn_values
  * [G][take][dim], take = min(k, count).  Groups are uploaded in chunks on a copy
  * stream so the upload of chunk i+1 overlaps the compression of chunk i (true
- * overlap needs pinned host memory).  Synchronous: returns with outputs written.
+ * overlap needs pinned host memory).  When `values` is pinned (device-accessible),
+ * only the selected value rows cross PCIe (zero-copy gather); otherwise all of
+ * it is uploaded.  Synchronous: returns with outputs written.
  * Same checks, in the same order, as cx_compress_grouped_dev. */
 cx_status cx_compress_grouped_host(cx_ctx* ctx, int n_groups, int64_t count, int dim,
                                    const float* keys, const float* values, const float* queries,

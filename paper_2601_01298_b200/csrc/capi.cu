@@ -559,6 +559,17 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         if (n_groups == 0) return;
         const int take = (int)std::min<int64_t>(k, count);
         const size_t in_g = (size_t)count * dim, q_g = (size_t)n_pass * d_k, o_g = (size_t)take * dim;
+        // Values are only read at the selected rows (2% at cfg2).  When the caller's buffer is
+        // pinned (device-accessible through UVA) the landmark gather reads those rows straight
+        // from host memory over PCIe instead of uploading every value row.
+        const float* vdev = nullptr;
+        {
+            cudaPointerAttributes pa{};
+            if (cudaPointerGetAttributes(&pa, values) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                pa.devicePointer != nullptr && !getenv("CX_HOST_UPLOAD_VALUES"))
+                vdev = reinterpret_cast<const float*>(pa.devicePointer);
+            cudaGetLastError();
+        }
         // device staging: keys | values | queries | rows | scores | syn_k | syn_v (256-B aligned slices)
         auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
         const size_t b_k = al(sizeof(float) * in_g * n_groups), b_q = al(sizeof(float) * q_g * n_groups);
@@ -586,10 +597,11 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         float* dsv = reinterpret_cast<float*>(p); p += b_o;
         double* dattn = reinterpret_cast<double*>(p); p += b_a;
         double* dcen = reinterpret_cast<double*>(p);
-        // Chunks of groups, one selection wave each (15 co-resident 8-CTA clusters on
-        // B200), so chunking costs no compute; the remainder goes FIRST so that the
-        // only exposed upload is the smallest one.
-        constexpr int WAVE = 15;
+        // Chunks of groups, one selection wave each (the cost model's co-resident clusters:
+        // 22 on B200 at L=8192), so chunking costs no compute; the remainder goes FIRST so
+        // that the only exposed upload is the smallest one.
+        const int w = dim == 64 ? select64_wave(count, n_groups) : 0;
+        const int WAVE = w > 0 ? w : 15;
         std::vector<int> start;
         for (int g0 = 0, first = n_groups % WAVE ? n_groups % WAVE : WAVE; g0 < n_groups; g0 += (g0 ? WAVE : first))
             start.push_back(g0);
@@ -635,7 +647,9 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         for (int i = 0; i < nch; ++i) {  // all uploads queued on the copy stream
             const int g0 = start[i], ng = start[i + 1] - g0;
             CX_CUDA(cudaMemcpyAsync(dk + g0 * in_g, keys + g0 * in_g, sizeof(float) * in_g * ng, cudaMemcpyHostToDevice, c->copy));
-            CX_CUDA(cudaMemcpyAsync(dv + g0 * in_g, values + g0 * in_g, sizeof(float) * in_g * ng, cudaMemcpyHostToDevice, c->copy));
+            if (!vdev)
+                CX_CUDA(cudaMemcpyAsync(dv + g0 * in_g, values + g0 * in_g, sizeof(float) * in_g * ng, cudaMemcpyHostToDevice,
+                                        c->copy));
             CX_CUDA(cudaMemcpyAsync(dq + g0 * q_g, queries + g0 * q_g, sizeof(float) * q_g * ng, cudaMemcpyHostToDevice, c->copy));
             CX_CUDA(cudaEventRecord(c->hev[i], c->copy));
         }
@@ -664,7 +678,7 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
             select_grouped(c, g, dattn + (size_t)g0 * count, k, lambda, flags, dr + (size_t)g0 * take,
                            ds + (size_t)g0 * take, c->stream, dcen + (size_t)g0 * dim);
             gather_rows(g, g.X, dr + (size_t)g0 * take, take, dsk + g0 * o_g, c->stream);
-            gather_rows(g, dv + g0 * in_g, dr + (size_t)g0 * take, take, dsv + g0 * o_g, c->stream);
+            gather_rows(g, (vdev ? vdev : dv) + g0 * in_g, dr + (size_t)g0 * take, take, dsv + g0 * o_g, c->stream);
         }
         CX_CUDA(cudaMemcpyAsync(out_rows, dr, sizeof(int64_t) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));
         CX_CUDA(cudaMemcpyAsync(out_scores, ds, sizeof(double) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));

@@ -142,6 +142,8 @@ void plan_attention(ArenaPlan& p, const GroupView& g);
 void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
                     unsigned flags, int64_t* rows, double* scores, cudaStream_t s,
                     const double* centroids = nullptr /* [G][dim], computed here when null */);
+// groups per selection wave for G groups of L rows (dim 64), 0 if not on chip
+int select64_wave(int64_t L, int G);
 // centroid_of for every group (synapse.cpp:173-181), bit-exact sequential sums
 void centroid_launch(const GroupView& g, double* cen, cudaStream_t s);
 void plan_select(ArenaPlan& p, const GroupView& g, int k);

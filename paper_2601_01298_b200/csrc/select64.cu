@@ -725,6 +725,21 @@ static double best_cluster(int G, int64_t L, size_t budget, int* C, int* S, int*
     return best;
 }
 
+// groups per wave of the configuration the cost model picks for G groups of L rows
+// (0 when the dim-64 kernel would not run on chip)
+int select64_wave(int64_t L, int G) {
+    static int max_optin = -1;
+    if (max_optin < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+            max_optin = 232448;
+    }
+    int C = 0, S = 0, Rs = 0, mode = 0, act = 0;
+    best_cluster(G, L, (size_t)max_optin - 2048, &C, &S, &Rs, &mode, &act);
+    return C > 0 ? act : 0;
+}
+
 bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                      cudaStream_t s) {
