@@ -309,7 +309,7 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
         "roofline": {"kernel": "select_kernel (greedy max-min selection)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_source": peak_kind, "traffic": ncu_traffic("select64_kernel"),
-                     "traffic_unit": "bytes per launch (ncu --set full, profiles/r1_ncu_full_summary.json)",
+                     "traffic_unit": "bytes per step: all select64 launches of one compression (ncu --set full, profiles/r1_ncu_full_summary.json)",
                      "note": "selection is fp64/FMA-issue + barrier-latency bound (SURVEY.md §8(d)); "
                              "HBM fraction reported as required"},
         "select_ms": sel_ms,
@@ -346,15 +346,18 @@ def ncu_traffic(kernel_substr):
             rows = json.load(f)
     except (OSError, ValueError):
         return None
+    # the capture holds one step (tools/prof_step.py --reps 1): every launch of the
+    # kernel in it belongs to that step (the selection runs as one launch per wave
+    # configuration), so their traffic is summed
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot, hit = 0.0, False
     for r in rows:
         if kernel_substr in r.get("Kernel Name", ""):
-            tot = 0.0
+            hit = True
             for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 v, _, u = r.get(k, "").partition(" ")
                 tot += float(v) * scale.get(u, 1.0)
-            return tot
-    return None
+    return tot if hit else None
 
 
 def run_decode(args, dev, rank=0, world=1):
