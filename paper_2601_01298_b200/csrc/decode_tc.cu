@@ -8,18 +8,23 @@
 // owns one (layer, KV head), stages K_syn / V_syn^T once, and loops over tiles
 // of 128 query rows (e.g. 18 agents x 7 q-heads) with two warp roles that run
 // concurrently and meet once per tile:
-//   synapse warps 0-3 (thread per TMEM lane = query row):
+//   synapse warps 0-3 (thread per TMEM lane = query row; they alone stage
+//   K_syn / V_syn^T, the private warps start streaming at kernel start):
 //     1. Q tile -> shared memory as a bf16 hi/lo pair (x = hi + lo to 2^-17);
 //     2. one thread issues S = Qlo Khi + Qhi Klo + Qhi Khi (tcgen05.mma
 //        kind::f16, fp32 accumulate in TMEM);
-//     3. row softmax over the synapse keys (m_s, l_s), unnormalised P as bf16
-//        hi/lo in 96-key chunks, O_syn = P V_syn (3 MMAs per k-step) into TMEM;
+//     3. row softmax over the synapse keys (m_s, l_s); the unnormalised P goes
+//        to TMEM as packed bf16x2 hi / lo (tcgen05.st) and is the A operand of
+//        O_syn = P V_syn (3 TS-MMAs per k-step, one pass);
+//     4. tile i+1's Q and S are issued while tile i's P.V runs (pipelined);
 //     5. epilogue: merge with the private partial (flash-style rescale).
-//   private warps 4-15 (warp per agent, all q-heads of the KV group):
-//     4. append the new token's K/V (fused), stream the private K rows (lane
-//        per row, full-row loads in flight) and V rows (lane per 2 dims), form
-//        scores / softmax (m_p, l_p) / O_priv on CUDA cores, publish to shared
-//        memory (O_priv aliases the Q tile once the score MMAs have read it).
+//   private warps 4-15 (warp per agent, agents dealt round-robin over the CTA's
+//   whole agent sequence): append the new token's K/V (fused, used from
+//   registers), stream the stored private rows in 16-row batches (8 lanes per
+//   row: q fits in registers, one warp load reads 4 rows x 128 B; the next
+//   batch is prefetched into L1), form scores (packed FMAs + reduce-scatter),
+//   softmax (m_p, l_p) and O_priv on CUDA cores, publish to shared memory
+//   (gated by an epilogue counter; two parity-split mbarriers hand tiles over).
 // The merge (m = max(m_s, m_p); O = (O_s e^{m_s-m} + O_p e^{m_p-m}) /
 // (l_s e^{m_s-m} + l_p e^{m_p-m})) is the one-pass softmax of the reference's
 // kernels::attend (kernels.cpp:127-158) over [synapse rows || private rows].

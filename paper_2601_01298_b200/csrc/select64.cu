@@ -4,10 +4,12 @@
 //
 // Layout: one thread-block cluster of C CTAs per group; CTA r owns rows
 // [r*S, r*S+S).  Thread t owns rows t, 512+t, 1024+t, ...; row t lives in 64
-// fp32 REGISTERS, the others in shared memory (float4-interleaved,
-// conflict-free) or, for very long contexts, in place in L2.  All per-row
-// state (running min distance, attention, bound threshold, removed flag) is in
-// the owner's registers.  Per round:
+// fp32 REGISTERS, the others in shared memory as fp32 (float4-interleaved,
+// conflict-free) or as an fp16 SKETCH (the filter reads the sketch, the exact
+// evaluations read the fp32 row from L2), or in L2 only.  C and the row mode
+// come from a measured cost model (waves x per-round cost; a partial last wave
+// is a separate launch).  All per-row state (running min distance, attention,
+// bound threshold, removed flag) is in the owner's registers.  Per round:
 //   U  distance update against the previous pick.  A Gram-form fp32 lower
 //      bound (packed fma.rn.f32x2) rules out rows whose min cannot change;
 //      the rest are queued and evaluated exactly in fp64 in the reference's
