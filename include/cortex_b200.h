@@ -7,7 +7,7 @@
  * entry point per reference function on the path (the citation on each line
  * is the cortex:: declaration it replaces), plain pointers + sizes, no torch
  * or CUDA types (streams are passed as void* = cudaStream_t).  The C++ shim
- * in include/cortex/*.hpp re-exports the exact cortex:: declarations on top
+ * in include/cortex/ (the .hpp headers) re-exports the exact cortex:: declarations on top
  * of these entry points, so code written against the reference links
  * unchanged.
  *

@@ -144,3 +144,18 @@ def test_oracle_is_not_linked_by_the_product(lib):
             if f.endswith((".py", ".cu", ".cpp", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f), errors="replace").read()
                 assert "import oracle" not in txt and "oracle/" not in txt.replace("oracle/_ref", ""), f
+
+
+def test_plain_c_consumer_compiles_and_links(tmp_path):
+    """include/cortex_b200.h is a C ABI: a C11 program (no C++, no torch) compiles
+    warning-free against it and links against libcortex_b200.so.  (Run on the GPU
+    in test_gpu_c_consumer.)"""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2601_01298_b200")
+    exe = tmp_path / "c_smoke"
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "tests", "c_consumer", "smoke.c"), "-L", libdir, "-lcortex_b200",
+                        "-Wl,-rpath," + libdir, "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert exe.exists()
