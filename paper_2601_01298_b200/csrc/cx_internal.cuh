@@ -142,6 +142,11 @@ void plan_attention(ArenaPlan& p, const GroupView& g);
 void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
                     unsigned flags, int64_t* rows, double* scores, cudaStream_t s,
                     const double* centroids = nullptr /* [G][dim], computed here when null */);
+// d = 128 instantiation (select128.cu): the reference-mode cloud of a 2-head MHA cache
+bool select128_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
+                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
+                      cudaStream_t s);
+int select128_wave(int64_t L, int G);
 // groups per selection wave for G groups of L rows (dim 64), 0 if not on chip
 int select64_wave(int64_t L, int G);
 // centroid_of for every group (synapse.cpp:173-181), bit-exact sequential sums

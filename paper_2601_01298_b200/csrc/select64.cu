@@ -1,6 +1,7 @@
 // select64.cu -- the greedy hybrid selection (SURVEY.md §8(a) A4/A6,
 // synapse.cpp:353-421) specialised for d = 64, the per-(layer, KV-head) key
-// width of the 0.5B-class shape.
+// width of the 0.5B-class shape.  select128.cu compiles the same kernel for
+// d = 128 (the head-concatenated reference-mode cloud) with no register rows.
 //
 // Layout: one thread-block cluster of C CTAs per group; CTA r owns rows
 // [r*S, r*S+S).  Thread t owns rows t, 512+t, 1024+t, ...; row t lives in 64
@@ -33,14 +34,26 @@
 
 namespace cg = cooperative_groups;
 
+// entry points of this instantiation: select64_* (d = 64) or select128_* (select128.cu)
+#define SEL_CAT2(a, b, c) a##b##_##c
+#define SEL_CAT(a, b, c) SEL_CAT2(a, b, c)
+#define SEL_FN(name) SEL_CAT(select, SEL_D, name)
+
 namespace cx {
 
 namespace {
 
-constexpr int D = 64;
-constexpr int NT = 512;          // threads per CTA (one register row each)
+#ifndef SEL_D
+#define SEL_D 64
+#endif
+constexpr int D = SEL_D;         // row width of this instantiation (64; 128 via select128.cu)
+constexpr int NT = 512;          // threads per CTA
 constexpr int NW = NT / 32;
-constexpr int QCAP = 160;        // exact-evaluation queue capacity per pass
+// d = 64: thread t keeps row t in 64 registers (RR = 512 register rows per CTA);
+// d = 128 has no register rows: every row is a shared-memory (fp32 / sketch) row
+constexpr bool REG = D == 64;
+constexpr int RR = REG ? NT : 0;
+constexpr int QCAP = D == 64 ? 160 : 96;  // exact-evaluation queue capacity per pass
 constexpr int QCAP_SK = 64;      // ... in sketch mode (leaves room for 1536 sketch rows)
 // Rows beyond the 512 register rows of a CTA live in shared memory as fp32
 // (ROWS_SMEM), or as an fp16 SKETCH there with the exact fp32 rows read from L2
@@ -106,11 +119,11 @@ struct Sel64Params {
     int64_t gstride, rstride;
     int64_t L;
     const double* attn;  // [G][L]
-    const double* cen;   // [G][64]
+    const double* cen;   // [G][D]
     int take;
     double lambda;
     int S;               // rows per CTA
-    int Rs;              // rows per CTA beyond the register rows (S - 512, >= 0)
+    int Rs;              // rows per CTA beyond the register rows (S - RR, >= 0)
     int filter;
     int64_t* pick_rows;
     double* pick_scores;
@@ -227,22 +240,26 @@ __device__ __forceinline__ float dot_f32x2(Get4 get4, const float* b) {
 
 // Lower bound of the fp64 squared distance from the Gram form
 // S = |x|^2 + |b|^2 - 2 x.b: every fp32 rounding above is
-// covered by 64 u (|x|^2 + |b|^2), u = 2^-24, plus an underflow allowance.
+// covered by D u (|x|^2 + |b|^2), u = 2^-24 (64 u at d = 64, 128 u at d = 128),
+// plus an underflow allowance.
+constexpr float GRAM_SLACK = D * 0x1p-24f;
+constexpr float SKETCH_SUB = D <= 64 ? 0x1p-21f : 0x1p-20f;
+static_assert(D <= 128, "sketch subnormal term derived for d <= 128");
 __device__ __forceinline__ float gram_lower_bound(float nx, float nb, float dot) {
     const float sum = __fadd_rn(nx, nb);
     const float s = __fsub_rn(sum, __fmul_rn(2.0f, dot));
-    const float e = __fmaf_ru(0x1p-18f, sum, 0x1p-100f);
+    const float e = __fmaf_ru(GRAM_SLACK, sum, 0x1p-100f);
     return __fsub_rd(s, e);
 }
 
 // The same bound when x is only known through its fp16 rounding x~ (the sketch):
 // |x_c - x~_c| <= 2^-11 |x_c| + 2^-25 (subnormals), so |2 (x - x~).b| <= 2^-11 (|x|^2 +
-// |b|^2) + 2^-21 |b|, added to the slack.  An fp16 overflow makes the dot inf/NaN,
+// |b|^2) + 2^-24 sqrt(D) |b| (<= 2^-21 |b| at d = 64, 2^-20 |b| at d = 128), added to the slack.  An fp16 overflow makes the dot inf/NaN,
 // the comparison false, and the row is evaluated exactly.
 __device__ __forceinline__ float gram_lower_bound_sketch(float nx, float nb, float dot) {
     const float sum = __fadd_rn(nx, nb);
     const float s = __fsub_rn(sum, __fmul_rn(2.0f, dot));
-    const float e = __fadd_ru(__fmaf_ru(0x1p-18f + 0x1p-11f, sum, 0x1p-100f), __fmul_ru(0x1p-21f, __fsqrt_ru(nb)));
+    const float e = __fadd_ru(__fmaf_ru(GRAM_SLACK + 0x1p-11f, sum, 0x1p-100f), __fmul_ru(SKETCH_SUB, __fsqrt_ru(nb)));
     return __fsub_rd(s, e);
 }
 
@@ -285,7 +302,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
 
     // ---- stage rows ---------------------------------------------------------
     float xr[D];
-    if (tid < nrows) {
+    if (REG && tid < nrows) {
         const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)tid * p.rstride);
 #pragma unroll
         for (int c4 = 0; c4 < D / 4; ++c4) {
@@ -296,17 +313,17 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
 #pragma unroll
         for (int c = 0; c < D; ++c) xr[c] = 0.f;
     }
-    const int nsm = max(0, nrows - NT);
+    const int nsm = max(0, nrows - RR);
     if (SMEM_ROWS) {
         for (int e = tid; e < nsm * (D / 4); e += NT) {
             const int j = e / (D / 4), c4 = e % (D / 4);
-            xs4[(size_t)c4 * p.Rs + j] = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)(NT + j) * p.rstride) + c4);
+            xs4[(size_t)c4 * p.Rs + j] = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)(RR + j) * p.rstride) + c4);
         }
     }
     if (ROWMODE == ROWS_SKETCH) {
         for (int e = tid; e < nsm * (D / 8); e += NT) {
             const int j = e / (D / 8), c8 = e % (D / 8);
-            const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)(NT + j) * p.rstride) + 2 * c8;
+            const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)(RR + j) * p.rstride) + 2 * c8;
             const float4 u = __ldg(src), v = __ldg(src + 1);
             const __half2 h0 = __floats2half2_rn(u.x, u.y), h1 = __floats2half2_rn(u.z, u.w);
             const __half2 h2 = __floats2half2_rn(v.x, v.y), h3 = __floats2half2_rn(v.z, v.w);
@@ -314,7 +331,8 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                                                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
         }
     }
-    // x~ . b over the fp16 sketch of row NT + j
+    __syncthreads();  // staged rows are written and read by different threads
+    // x~ . b over the fp16 sketch of row RR + j
     auto sketch_dot = [&](int j, const float* b) {
         float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
 #pragma unroll 4
@@ -333,10 +351,10 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         return (s0.x + s0.y) + (s1.x + s1.y);
     };
     auto reg4 = [&](int c4) { return make_float4(xr[4 * c4], xr[4 * c4 + 1], xr[4 * c4 + 2], xr[4 * c4 + 3]); };
-    auto far4 = [&](int j) {  // row NT + j
+    auto far4 = [&](int j) {  // row RR + j
         return [&, j](int c4) -> float4 {
             if (SMEM_ROWS) return xs4[(size_t)c4 * p.Rs + j];
-            return __ldg(reinterpret_cast<const float4*>(gX + (int64_t)(NT + j) * p.rstride) + c4);
+            return __ldg(reinterpret_cast<const float4*>(gX + (int64_t)(RR + j) * p.rstride) + c4);
         };
     };
 
@@ -354,12 +372,12 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                 const int li = tid + k * NT;
                 a[k] = p.attn[(int64_t)g * p.L + r0 + li];
                 // coverage init: distance to the centroid (synapse.cpp:244-249)
-                if (k == 0) {
+                if (REG && k == 0) {
                     m[k] = __dsqrt_rn(exact_sq_d(reg4, cen));
                     nx[k] = (float)norm2(reg4);
                 } else {
-                    m[k] = __dsqrt_rn(exact_sq_d<2>(far4(li - NT), cen));
-                    nx[k] = (float)norm2<2>(far4(li - NT));
+                    m[k] = __dsqrt_rn(exact_sq_d<2>(far4(li - RR), cen));
+                    nx[k] = (float)norm2<2>(far4(li - RR));
                 }
                 remm |= 1u << k;
             }
@@ -403,10 +421,10 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                 if (assign || !p.filter) {
                     need = true;
                 } else {
-                    if (ROWMODE == ROWS_SKETCH && k > 0) {
-                        need = !(gram_lower_bound_sketch(nx[k], nbw, sketch_dot(tid + k * NT - NT, bw)) > th[k]);
+                    if (ROWMODE == ROWS_SKETCH && !(REG && k == 0)) {
+                        need = !(gram_lower_bound_sketch(nx[k], nbw, sketch_dot(tid + k * NT - RR, bw)) > th[k]);
                     } else {
-                        const float dt = (k == 0) ? dot_f32x2(reg4, bw) : dot_f32x2<4>(far4(tid + k * NT - NT), bw);
+                        const float dt = (REG && k == 0) ? dot_f32x2(reg4, bw) : dot_f32x2<4>(far4(tid + k * NT - RR), bw);
                         need = !(gram_lower_bound(nx[k], nbw, dt) > th[k]);
                     }
                 }
@@ -418,11 +436,11 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                     float* st = stage + sl * SPITCH;
 #pragma unroll
                     for (int c4 = 0; c4 < D / 4; ++c4) {
-                        const float4 v = (k == 0) ? reg4(c4) : far4(tid + k * NT - NT)(c4);
+                        const float4 v = (REG && k == 0) ? reg4(c4) : far4(tid + k * NT - RR)(c4);
                         st[4 * c4] = v.x; st[4 * c4 + 1] = v.y; st[4 * c4 + 2] = v.z; st[4 * c4 + 3] = v.w;
                     }
                 } else {  // queue full: evaluate in place
-                    const double d2 = (k == 0) ? exact_sq(reg4, bw) : exact_sq<2>(far4(tid + k * NT - NT), bw);
+                    const double d2 = (REG && k == 0) ? exact_sq(reg4, bw) : exact_sq<2>(far4(tid + k * NT - RR), bw);
                     const double d = __dsqrt_rn(d2);
                     if (assign || d < m[k]) {
                         m[k] = d;
@@ -567,7 +585,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                    round, tid, a[0], m[0], happ[0], hex[0], amin, amax, cmin, cmax, hmax, kbest, rbest);
         if (rbest != ~0ull) {  // owner of the local winner publishes its coordinates
             const int li = (int)((long long)rbest - r0);
-            if (li < NT) {
+            if (REG && li < NT) {
                 if (tid == li) {
 #pragma unroll
                     for (int c4 = 0; c4 < D / 4; ++c4) reinterpret_cast<float4*>(cand)[c4] = reg4(c4);
@@ -575,11 +593,11 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                 }
             } else if (tid == (li & (NT - 1))) {
                 const int k = li / NT;
-                auto get = far4(li - NT);
+                auto get = far4(li - RR);
 #pragma unroll
                 for (int c4 = 0; c4 < D / 4; ++c4) reinterpret_cast<float4*>(cand)[c4] = get(c4);
 #pragma unroll
-                for (int kk = 1; kk < MAXRPT; ++kk)
+                for (int kk = REG ? 1 : 0; kk < MAXRPT; ++kk)
                     if (kk == k) cand_hdr->nb = (double)nx[kk];
             }
         } else if (tid < D) {
@@ -598,8 +616,8 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
             st_async_v2(dst, __double_as_longlong(sc), (uint64_t)rw, mb);
             st_async_v2(dst + 16, __double_as_longlong(cand_hdr->nb), 0ull, mb);
         }
-        if (tid >= 32 && tid < 32 + (int)C * (D / 4)) {
-            const int e = tid - 32, dst_rank = e / (D / 4), c4 = e % (D / 4);
+        for (int e = tid - 32; tid >= 32 && e < (int)C * (D / 4); e += NT - 32) {
+            const int dst_rank = e / (D / 4), c4 = e % (D / 4);
             const uint32_t dst = mapa(smem_u32(bc + rank * D + 4 * c4), dst_rank);
             st_async_v4(dst, reinterpret_cast<const float4*>(cand)[c4], mapa(smem_u32(&mbar[1]), dst_rank));
         }
@@ -704,7 +722,7 @@ static double best_cluster(int G, int64_t L, size_t budget, int* C, int* S, int*
     double best = 1e300;
     const bool sketch_ok = !getenv("CX_SEL_NOSKETCH");
     for (int c = 1; c <= MAXC; ++c) {
-        const int s_ = (int)((L + c - 1) / c), rs = std::max(0, s_ - NT);
+        const int s_ = (int)((L + c - 1) / c), rs = std::max(0, s_ - RR);
         if (s_ > MAXRPT_ALL * NT) continue;
         // fp32 rows on chip if they fit, else the fp16 sketch (rows re-read from L2 only
         // by the exact evaluations): measured ~15% more per round (C=6: 10.1 us, C=5:
@@ -730,7 +748,7 @@ static double best_cluster(int G, int64_t L, size_t budget, int* C, int* S, int*
 
 // groups per wave of the configuration the cost model picks for G groups of L rows
 // (0 when the dim-64 kernel would not run on chip)
-int select64_wave(int64_t L, int G) {
+int SEL_FN(wave)(int64_t L, int G) {
     static int max_optin = -1;
     if (max_optin < 0) {
         int dev = 0;
@@ -743,7 +761,7 @@ int select64_wave(int64_t L, int G) {
     return C > 0 ? act : 0;
 }
 
-bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
+bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                      cudaStream_t s) {
     if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 ||
@@ -764,7 +782,7 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
     int C = 0, S = 0, Rs = 0, mode = ROWS_SMEM, act = 0;
     if (const char* force = getenv("CX_SEL_C")) {  // debugging / tuning: force a cluster size
         const int c = atoi(force);
-        const int s_ = (int)((g.L + c - 1) / c), rs = std::max(0, s_ - NT);
+        const int s_ = (int)((g.L + c - 1) / c), rs = std::max(0, s_ - RR);
         if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT) {
             C = c; S = s_; Rs = rs;
             mode = sel64_layout(rs, ROWS_SMEM).total <= budget ? ROWS_SMEM
@@ -783,8 +801,8 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
                 gb.G = rem;
                 gb.X = g.X + (int64_t)full * g.gstride;
                 const int64_t o = (int64_t)full * take;
-                return select64_launch(ga, attn, cen, take, lambda, flags, pick_rows, pick_scores, rows, scores, s) &&
-                       select64_launch(gb, attn + (int64_t)full * g.L, cen + (int64_t)full * D, take, lambda, flags,
+                return SEL_FN(launch)(ga, attn, cen, take, lambda, flags, pick_rows, pick_scores, rows, scores, s) &&
+                       SEL_FN(launch)(gb, attn + (int64_t)full * g.L, cen + (int64_t)full * D, take, lambda, flags,
                                        pick_rows + o, pick_scores + o, rows + o, scores + o, s);
             }
         }
@@ -792,7 +810,7 @@ bool select64_launch(const GroupView& g, const double* attn, const double* cen, 
     if (C == 0) {  // nothing fits on chip: rows beyond 512 per CTA are read from L2 every round
         C = MAXC;
         S = (int)((g.L + C - 1) / C);
-        Rs = std::max(0, S - NT);
+        Rs = std::max(0, S - RR);
         if (S > MAXRPT_ALL * NT) return false;
         mode = ROWS_L2;
     }

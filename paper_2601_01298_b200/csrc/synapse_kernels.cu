@@ -751,7 +751,8 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     else centroid_launch(g, cen, s);
 
     if (!(flags & CX_SELECT_GENERIC) &&
-        select64_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, s))
+        (select64_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, s) ||
+         select128_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, s)))
         return;
 
     SelectPlan pl = plan_select_shape(g);

@@ -166,6 +166,41 @@ def test_mha_mode_matches_reference_cloud(dev, orc):
     assert np.array_equal(rows.cpu().numpy()[0], idx)
 
 
+@pytest.mark.parametrize("G,L,k,force", [
+    (3, 1500, 30, None),   # cost-model choice
+    (2, 7168, 96, None),   # reference-mode cfg2 cloud per layer (d_model = 128): fp16 sketch rows
+    (2, 1500, 40, "4"),    # 375 fp32 rows per CTA in shared memory
+    (2, 1500, 40, "2"),    # 750 rows per CTA: the sketch
+    (2, 1500, 40, "1"),    # 1500 rows per CTA: rows re-read from L2
+    (3, 5, 9, None),       # k > L
+])
+def test_select128_matches_reference(dev, orc, monkeypatch, G, L, k, force):
+    """The d = 128 instantiation of the cluster selection (select128.cu) on the
+    head-concatenated cloud of a 2-head MHA cache: rows and scores bit-exact
+    against the reference per group and against the generic kernel."""
+    import torch
+    if force:
+        monkeypatch.setenv("CX_SEL_C", force)
+    dm = 128
+    ks, qs = [], []
+    for gi in range(G):
+        r = orc.rng(300 + 17 * gi + L)
+        ks.append(r.gaussian_f32(L * dm).reshape(L, dm))
+        qs.append(r.gaussian_f32(dm))
+    kt = torch.from_numpy(np.stack(ks)).cuda()
+    qt = torch.from_numpy(np.stack(qs).reshape(G, 2, dm // 2)).cuda()
+    a = dev.attention_grouped(kt, qt, mode="mha")
+    rows, scores = dev.select_grouped(kt, a, k, 0.5)
+    grows, gscores = dev.select_grouped(kt, a, k, 0.5, 2)  # CX_SELECT_GENERIC
+    torch.cuda.synchronize()
+    assert torch.equal(rows, grows) and torch.equal(scores, gscores)
+    a_np = a.cpu().numpy()
+    for gi in range(G):
+        idx, sc = orc.select_landmarks_points(ks[gi], a_np[gi], k, 0.5)
+        assert rows[gi].cpu().numpy().tobytes() == idx.tobytes(), gi
+        assert scores[gi].cpu().numpy().tobytes() == sc.tobytes(), gi
+
+
 def test_full_cfg2_properties(dev):
     """All 48 (layer, KV-head) groups at L=8192, k=164: size-independent
     properties (sorted unique rows in range, gather == source rows)."""
