@@ -26,7 +26,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
     "--expt-relaxed-constexpr",
     "-I" + INCLUDE, "-I" + CSRC,
-]
+] + os.environ.get("CX_NVCC_EXTRA", "").split()  # experiments only (e.g. -DCX_TC_OP_BUFS=2)
 
 
 def _sources():

@@ -49,11 +49,13 @@ constexpr int SWARPS = 4;       // synapse warps (TMEM lanes 0-127)
 constexpr int PWARPS = 12;      // private-row warps (13+ warps allocate registers like 16)
 constexpr int TTHREADS = 32 * (SWARPS + PWARPS);
 constexpr int OPS = TD + 4;     // O_priv row stride (floats; conflict-free float4 rows)
-constexpr bool PREFETCH_NEXT = false;  // L2 bulk prefetch of the next agent: superseded by the L1 batch prefetch (it added ~25% DRAM re-reads)
 constexpr int SST = TTAIL + 4;
 // O_priv buffers: 2 lets the private warps publish a tile before the previous tile's
 // epilogue; 1 saves 35 KB of shared memory, i.e. leaves L1 room for the private stream
-constexpr int OP_BUFS = 1;  // private score row stride (16-B aligned, conflict-free stores)
+#ifndef CX_TC_OP_BUFS
+#define CX_TC_OP_BUFS 1
+#endif
+constexpr int OP_BUFS = CX_TC_OP_BUFS;  // O_priv buffers (2: private warps may run a whole tile ahead)
 
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -130,11 +132,6 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
         : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
           "l"(*reinterpret_cast<uint64_t*>(&c)));
     return *reinterpret_cast<float2*>(&d);
-}
-
-// bulk prefetch of a contiguous block into L2 (no registers, no shared memory)
-__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // long waits (a role waiting for the other): back off instead of spinning on issue slots
@@ -649,24 +646,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 const float* tk = b.tail_keys + toff;
                 const float* tv = b.tail_values + toff;
                 const float* qrow = b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG) * TD;
-                // this warp's next agent: its private rows -> L2 now (bulk prefetch)
-                {
-                    int na_t = ai + PWARPS, nt_tile = tile;
-                    if (na_t >= na) {
-                        na_t = (pw - ((ti + 1) * AT) % PWARPS + PWARPS) % PWARPS;
-                        nt_tile = tile + (int)gridDim.y;
-                    }
-                    const int an = nt_tile * AT + na_t;
-                    if (nt_tile < n_tiles && an < b.n_agents && na_t < AT) {
-                        const size_t off = ((((size_t)an * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
-                        const int nx_len = min(b.tail_len[an], b.t_cap - (app ? 1 : 0));
-                        const uint32_t bytes = (uint32_t)min(nx_len + (app ? 1 : 0), b.t_cap) * TD * 4;
-                        if (lane == 0 && PREFETCH_NEXT && bytes) {
-                            l2_prefetch(b.tail_keys + off, bytes);
-                            l2_prefetch(b.tail_values + off, bytes);
-                        }
-                    }
-                }
                 // q, the new token's K/V row (it is row `len`) and the first K batch are all in
                 // flight together; the new row is used from registers and appended (fused).
                 float4 qa[QPG], qb[QPG];
@@ -681,17 +660,16 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     nka = __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + (lane & 7));
                     nkb = __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + 8 + (lane & 7));
                     nvv = __ldg(reinterpret_cast<const float2*>(b.new_values + noff) + lane);
-                    if (lane < 8) {
-                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[lane] = nka;
-                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[8 + lane] = nkb;
-                    }
-                    reinterpret_cast<float2*>(b.tail_values + toff + (size_t)len * TD)[lane] = nvv;
-                }
+                }  // (appended at the end of the agent: a store here would hold back every load below)
                 // ---- scores of the stored rows [0, len): 16-row batches, then 4-row groups ----
+                // K batch 1 and V batches 0-1 go to L1 now (the whole 32-row tail is in flight
+                // with q and K batch 0); longer tails are prefetched two batches ahead
                 int r0 = 0;
-                prefetch_rows16_l1<PB>(tv, 0, len, lane);  // V batch 0 lands in L1 during the scores
+                prefetch_rows16_l1<PB>(tk, PB, len, lane);
+                prefetch_rows16_l1<PB>(tv, 0, len, lane);
+                prefetch_rows16_l1<PB>(tv, PB, len, lane);
                 for (; r0 + PB <= len; r0 += PB) {
-                    prefetch_rows16_l1<PB>(tk, r0 + PB, len, lane);
+                    prefetch_rows16_l1<PB>(tk, r0 + 2 * PB, len, lane);
                     score_rows<QPG, PB / 4, false>(tk, r0, len, qa, qb, Sw, lane, scale);
                 }
                 for (; r0 < len; r0 += 4) score_rows<QPG, 1, true>(tk, r0, len, qa, qb, Sw, lane, scale);
@@ -726,8 +704,22 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) o[h] = make_float2(0.f, 0.f);
                 r0 = 0;
+                {  // the next agent's q and first K batch land in L1 during this mix
+                    int na_t = ai + PWARPS, nt_tile = tile;
+                    if (na_t >= na) {
+                        na_t = (pw - ((ti + 1) * AT) % PWARPS + PWARPS) % PWARPS;
+                        nt_tile = tile + (int)gridDim.y;
+                    }
+                    const int an = nt_tile * AT + na_t;
+                    if (nt_tile < n_tiles && an < b.n_agents && na_t < AT) {
+                        const size_t off = ((((size_t)an * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
+                        prefetch_rows16_l1<PB>(b.tail_keys + off, 0, b.t_cap, lane);
+                        const float* qn = b.q + (((size_t)an * b.n_layers + l) * b.n_q + (size_t)g * QPG) * TD;
+                        if (lane < 2 * QPG) asm volatile("prefetch.global.L1 [%0];" ::"l"(qn + lane * 32));
+                    }
+                }
                 for (; r0 + PB <= len; r0 += PB) {
-                    prefetch_rows16_l1<PB>(tv, r0 + PB, len, lane);
+                    prefetch_rows16_l1<PB>(tv, r0 + 2 * PB, len, lane);
                     mix_rows<QPG, PB, false>(tv, r0, len, Sw, o, lane);
                 }
                 for (; r0 < len; r0 += 4) mix_rows<QPG, 4, true>(tv, r0, len, Sw, o, lane);
@@ -747,6 +739,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 for (int h = 0; h < QPG; ++h) {
                     const int r = ai * QPG + h;
                     reinterpret_cast<float2*>(Op + ((size_t)(OP_BUFS == 2 ? tpar : 0) * TM + r) * OPS)[lane] = o[h];
+                }
+                if (app) {  // the fused append of the new token's K/V (row len; never read above)
+                    if (lane < 8) {
+                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[lane] = nka;
+                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[8 + lane] = nkb;
+                    }
+                    reinterpret_cast<float2*>(b.tail_values + toff + (size_t)len * TD)[lane] = nvv;
                 }
                 __syncwarp();  // Sw reuse
             }
@@ -793,14 +792,18 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
     // one resident CTA per SM: fill the SMs in a single wave
     const int per_lh = std::max(1, std::min(n_tiles, sms / n_lh));
-    CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    // debugging only (CX_TC_SMEM_PAD=bytes): reserve extra shared memory, i.e. shrink the L1
+    // carveout, to measure how the private-row stream depends on L1 capacity
+    const size_t smem = lay.total + (getenv("CX_TC_SMEM_PAD") ? (size_t)atol(getenv("CX_TC_SMEM_PAD")) : 0);
+    if (smem > (size_t)max_optin) return false;
+    CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     static unsigned long long* trc = nullptr;
     const bool tracing = getenv("CX_TC_TRACE") != nullptr;
     if (tracing && !trc) {
         CX_CUDA(cudaMalloc(&trc, 2048 * sizeof(unsigned long long)));
         CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
     }
-    kern<<<dim3((unsigned)n_lh, (unsigned)per_lh), TTHREADS, lay.total, s>>>(b, (float)(1.0 / std::sqrt((double)b.d_k)),
+    kern<<<dim3((unsigned)n_lh, (unsigned)per_lh), TTHREADS, smem, s>>>(b, (float)(1.0 / std::sqrt((double)b.d_k)),
                                                                              tracing ? trc : nullptr,
                                                                              getenv("CX_TC_SKIP") ? atoi(getenv("CX_TC_SKIP")) : 0);
     check_launch("decode_tc_kernel");
