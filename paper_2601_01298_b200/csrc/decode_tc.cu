@@ -189,16 +189,6 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
 struct TcLayout {
     size_t kh, kl, vh, vl, qo, op, sw, mp, lp, mbar, tbase, total;
@@ -682,21 +672,38 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     wait_epilogues(epi_done, ti - 1);
                     published = true;
                 }
-                // softmax per q-head over the private rows (weights 0 up to TTAIL)
+                // softmax per q-head over the private rows (weights 0 up to TTAIL); the
+                // heads' shuffle reductions are interleaved (independent chains)
+                {
+                    float s0[QPG], s1[QPG], mh[QPG], lh[QPG];
 #pragma unroll
-                for (int h = 0; h < QPG; ++h) {
-                    const float s0 = lane < nt ? Sw[h * SST + lane] : -INFINITY;
-                    const float s1 = lane + 32 < nt ? Sw[h * SST + lane + 32] : -INFINITY;
-                    const float m = warp_max(fmaxf(s0, s1));
-                    const float p0 = lane < nt ? __expf(s0 - m) : 0.f;
-                    const float p1 = lane + 32 < nt ? __expf(s1 - m) : 0.f;
-                    Sw[h * SST + lane] = p0;
-                    Sw[h * SST + lane + 32] = p1;
-                    const float lsum = warp_sum(p0 + p1);
-                    if (lane == 0) {  // this buffer's previous tile was merged two tiles ago
-                        Mp[tpar * TM + ai * QPG + h] = m;
-                        Lp[tpar * TM + ai * QPG + h] = lsum;
+                    for (int h = 0; h < QPG; ++h) {
+                        s0[h] = lane < nt ? Sw[h * SST + lane] : -INFINITY;
+                        s1[h] = lane + 32 < nt ? Sw[h * SST + lane + 32] : -INFINITY;
+                        mh[h] = fmaxf(s0[h], s1[h]);
                     }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1)
+#pragma unroll
+                        for (int h = 0; h < QPG; ++h) mh[h] = fmaxf(mh[h], __shfl_xor_sync(0xffffffffu, mh[h], o));
+#pragma unroll
+                    for (int h = 0; h < QPG; ++h) {
+                        const float p0 = lane < nt ? __expf(s0[h] - mh[h]) : 0.f;
+                        const float p1 = lane + 32 < nt ? __expf(s1[h] - mh[h]) : 0.f;
+                        Sw[h * SST + lane] = p0;
+                        Sw[h * SST + lane + 32] = p1;
+                        lh[h] = p0 + p1;
+                    }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1)
+#pragma unroll
+                        for (int h = 0; h < QPG; ++h) lh[h] += __shfl_xor_sync(0xffffffffu, lh[h], o);
+                    if (lane == 0)  // this buffer's previous tile was merged two tiles ago
+#pragma unroll
+                        for (int h = 0; h < QPG; ++h) {
+                            Mp[tpar * TM + ai * QPG + h] = mh[h];
+                            Lp[tpar * TM + ai * QPG + h] = lh[h];
+                        }
                 }
                 __syncwarp();
                 // ---- O_priv = P V_priv (lane: dims 2 lane, 2 lane + 1) ----
