@@ -15,7 +15,8 @@
 //        kind::f16, fp32 accumulate in TMEM);
 //     3. row softmax over the synapse keys (m_s, l_s); the unnormalised P goes
 //        to TMEM as packed bf16x2 hi / lo (tcgen05.st) and is the A operand of
-//        O_syn = P V_syn (3 TS-MMAs per k-step, one pass);
+//        O_syn = P V_syn: per k-step one N = 128 TS-MMA P_hi [V_hi | V_lo] and one
+//        N = 64 P_lo V_hi (V_hi / V_lo stacked as one 128-row B operand);
 //     4. tile i+1's Q and S are issued while tile i's P.V runs (pipelined);
 //     5. epilogue: merge with the private partial (flash-style rescale).
 //   private warps 4-15 (warp per agent, agents dealt round-robin over the CTA's
@@ -134,6 +135,11 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return *reinterpret_cast<float2*>(&d);
 }
 
+// bulk prefetch of a contiguous block into L2 (no registers, no shared memory)
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // long waits (a role waiting for the other): back off instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* m, uint32_t parity) {
     uint32_t ok = 0;
@@ -204,8 +210,7 @@ __host__ __device__ inline TcLayout tc_layout(int k_syn, int qpg) {
     size_t o = 0;
     L.kh = o; o += kv;
     L.kl = o; o += kv;
-    L.vh = o; o += kv;
-    L.vl = o; o += kv;
+    L.vh = o; o += 2 * kv;             // V^T hi (rows 0-63) | lo (rows 64-127): one N = 128 operand
     L.qo = o; o += q2;                 // Q hi | lo (A operand of the score MMAs)
     L.op = o; o += OP_BUFS * op;       // O_priv [OP_BUFS][TM][OPS]
     L.sw = o; o += pw;                 // per private warp: scores / weights [qpg][SST]
@@ -346,8 +351,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     const int NS = lay.ns;
     unsigned char* Kh = smem + lay.kh;
     unsigned char* Kl = smem + lay.kl;
-    unsigned char* Vh = smem + lay.vh;
-    unsigned char* Vl = smem + lay.vl;
+    unsigned char* Vhl = smem + lay.vh;  // [V_hi^T ; V_lo^T] as 128 N-rows
     unsigned char* Qh = smem + lay.qo;
     unsigned char* Ql = smem + lay.qo + (size_t)TM * TD * 2;
     float* Op = reinterpret_cast<float*>(smem + lay.op);
@@ -382,9 +386,17 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp < SWARPS) {  // K_syn / V_syn^T staging: synapse warps only (the private rows never read them)
+        {  // the first Q tile -> L2 during the staging
+            const int a0q = (int)blockIdx.y * AT;
+            if (tid < min(AT, b.n_agents - a0q))
+                l2_prefetch(b.q + (((size_t)(a0q + tid) * b.n_layers + l) * b.n_q + (size_t)g * QPG) * TD,
+                            (uint32_t)(QPG * TD * sizeof(float)));
+        }
         const float* sk = b.syn_keys + (size_t)lh * ks * TD;
         const float* sv = b.syn_values + (size_t)lh * ks * TD;
-        constexpr int ST = SWARPS * 32, IT = 4;  // items per pass per thread (loads in flight)
+        // items per pass per thread: all NS * 8 = 1408 items (k <= 176) in ONE pass, so the
+        // staging costs two loaded-latency round trips (K, then V) instead of nine
+        constexpr int ST = SWARPS * 32, IT = (TNS_MAX * 8 + ST - 1) / ST;
         // K: item = (key j, 8-dim chunk c): two float4 loads, one hi and one lo store
         for (int base = 0; base < NS * 8; base += IT * ST) {
             float4 ka[IT], kb[IT];
@@ -407,19 +419,22 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             }
         }
         // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
-        for (int base = 0; base < TD * (NS / 8); base += 2 * ST) {
+        for (int base = 0; base < TD * (NS / 8); base += IT * ST) {
+            float xv[IT][8];
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < IT; ++k) {
                 const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
-                if (jc < NS / 8) {
-                    float x[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int j = 8 * jc + u;
-                        x[u] = j < ks ? __ldg(sv + (size_t)j * TD + c) : 0.f;
-                    }
-                    split8_store(x, Vh, Vl, cm_off(c, 8 * jc, TD));  // B of O = P V: N = dims, K = keys
+                for (int u = 0; u < 8; ++u) {
+                    const int j = 8 * jc + u;
+                    xv[k][u] = (jc < NS / 8 && j < ks) ? __ldg(sv + (size_t)j * TD + c) : 0.f;
                 }
+            }
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
+                // B of O = P V (N = dims, K = keys): hi at N-row c, lo at N-row 64 + c (+1024 B)
+                if (jc < NS / 8) split8_store(xv[k], Vhl, Vhl + cm_off(TD, 0, 2 * TD), cm_off(c, 8 * jc, 2 * TD));
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -427,13 +442,15 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
         if (tid == 0) TC_TRACE(1000);
     }
     // TMEM columns: S [0, NS), O [NS, NS + 64), P hi [256, 256 + NS/2), P lo [256 + NS/2, 256 + NS)
-    const uint32_t tS = *tbase_s, tO = tS + (uint32_t)NS, tPh = tS + 256u, tPl = tPh + (uint32_t)(NS / 2);
+    // TMEM columns: S [0, NS), O [NS, NS + 128) (P_hi V_hi + P_lo V_hi | P_hi V_lo), P hi / lo after
+    const uint32_t tS = *tbase_s, tO = tS + (uint32_t)NS, tPh = tS + (uint32_t)max(256, NS + 2 * TD),
+                   tPl = tPh + (uint32_t)(NS / 2);
     const int n_tiles = (b.n_agents + AT - 1) / AT;
     uint32_t tpar = 0;  // tile parity: mbar[0] / mbar[2] phases, double-buffered O_priv / (m, l)
 
     if (warp < SWARPS) {
         // ======================= synapse warps =======================
-        const uint32_t idS = idesc_bf16_f32(TM, NS), idO = idesc_bf16_f32(TM, TD);
+        const uint32_t idS = idesc_bf16_f32(TM, NS), idO = idesc_bf16_f32(TM, TD), idO2 = idesc_bf16_f32(TM, 2 * TD);
         const uint32_t trow = tS + ((uint32_t)(warp * 32) << 16);
         const uint32_t trow_ph = tPh + ((uint32_t)(warp * 32) << 16), trow_pl = tPl + ((uint32_t)(warp * 32) << 16);
         const int r_own = warp * 32 + lane;
@@ -466,6 +483,14 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             bar_sync(1, SWARPS * 32);
         };
+        // a Q tile's agents -> L2 (one bulk prefetch of QPG contiguous rows per agent), a
+        // tile ahead of stage_q: the staging then waits on L2, not on a DRAM round trip
+        auto prefetch_q = [&](int tile_q) {
+            const int a0q = tile_q * AT;
+            if (tile_q < n_tiles && tid < min(AT, b.n_agents - a0q))
+                l2_prefetch(b.q + (((size_t)(a0q + tid) * b.n_layers + l) * b.n_q + (size_t)g * QPG) * TD,
+                            (uint32_t)(QPG * TD * sizeof(float)));
+        };
         // S = Q K^T on the tensor cores (3 MMAs per 16-wide k-step), completion on mbar[0]
         auto issue_s = [&]() {
             if (tid == 0) {
@@ -491,6 +516,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
         int ti = 0;
         for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
             if (tid == 0) TC_TRACE(ti * 16 + 0);
+            prefetch_q(tile + (int)gridDim.y);  // staged during this tile's P.V
             const int a0 = tile * AT;
             const int rows = min(AT, b.n_agents - a0) * QPG;
             const int next = tile + (int)gridDim.y;
@@ -552,17 +578,19 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             bar_sync(1, SWARPS * 32);  // S of this tile fully read; P in TMEM
+            if (tid == 0) TC_TRACE(ti * 16 + 1);
             if (tid == 0) {
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t vlbo = (TD / 8) * 128;
+                const uint32_t vlbo = (2 * TD / 8) * 128;  // K-chunk stride of the 128-row V operand
                 for (int kk = 0; kk < NS / 16; ++kk) {
                     const uint32_t vo = kk * 2 * vlbo;
-                    const uint64_t vh = sdesc(su32(Vh) + vo, vlbo, 128), vl = sdesc(su32(Vl) + vo, vlbo, 128);
-                    mma_bf16_ts(tO, tPl + (uint32_t)(kk * 8), vh, idO, kk > 0 ? 1u : 0u);
-                    mma_bf16_ts(tO, tPh + (uint32_t)(kk * 8), vl, idO, 1u);
-                    mma_bf16_ts(tO, tPh + (uint32_t)(kk * 8), vh, idO, 1u);
+                    // one N = 128 MMA: [P_hi V_hi | P_hi V_lo]; one N = 64: += P_lo V_hi
+                    const uint64_t vhl = sdesc(su32(Vhl) + vo, vlbo, 128);
+                    mma_bf16_ts(tO, tPh + (uint32_t)(kk * 8), vhl, idO2, kk > 0 ? 1u : 0u);
+                    mma_bf16_ts(tO, tPl + (uint32_t)(kk * 8), vhl, idO, 1u);
                 }
                 mma_commit(&mbar[1]);
+                TC_TRACE(ti * 16 + 15);
             }
             // next tile: its Q (the score MMAs of this tile are done with the buffer) and S
             // (this tile's S is dead) while this tile's P.V runs
@@ -570,6 +598,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 stage_q(next);
                 issue_s();
             }
+            if (tid == 0) TC_TRACE(ti * 16 + 7);
             mbar_wait_parity(&mbar[1], ph1);  // O = P V_syn complete
             ph1 ^= 1u;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -584,7 +613,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 float v[TD];
                 const uint32_t trow_o = tO + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
-                for (int c0 = 0; c0 < TD; c0 += 16) tmem_ld16(trow_o + (uint32_t)c0, v + c0);
+                for (int c0 = 0; c0 < TD; c0 += 16) {
+                    float w[16];
+                    tmem_ld16(trow_o + (uint32_t)c0, v + c0);
+                    tmem_ld16(trow_o + (uint32_t)(TD + c0), w);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[c0 + j] += w[j];
+                }
                 if (live) {
                     const int a = a0 + r_own / QPG, hh = r_own % QPG;
                     const float m_p = Mp[tpar * TM + r_own], l_p = Lp[tpar * TM + r_own];
@@ -823,7 +858,8 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
                 (h[1000] - h[1001]) / 1e3);
         for (int ti = 0; ti < 62 && h[ti * 16]; ++ti) {
             fprintf(stderr, "tile %2d syn:", ti);
-            for (int k = 0; k < 7; ++k) fprintf(stderr, " %7.2f", (h[ti * 16 + k] - t0) / 1e3);
+            for (int k = 0; k < 8; ++k) fprintf(stderr, " %7.2f", (h[ti * 16 + k] - t0) / 1e3);
+            fprintf(stderr, " pv-issued %7.2f", (h[ti * 16 + 15] - t0) / 1e3);
             fprintf(stderr, " | priv0:");
             for (int k = 8; k < 15; ++k) fprintf(stderr, " %7.2f", h[ti * 16 + k] ? (h[ti * 16 + k] - t0) / 1e3 : -1.0);
             fprintf(stderr, "\n");
