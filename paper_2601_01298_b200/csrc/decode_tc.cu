@@ -469,8 +469,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     const int a = a0q + r / QPG, hh = r % QPG;
                     const float4* src = reinterpret_cast<const float4*>(
                         b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD + 8 * c);
-                    xa[it] = __ldg(src);
-                    xb[it] = __ldg(src + 1);
+                    xa[it] = __ldcg(src);  // L2 only: no L1 allocation over the private rows' prefetches
+                    xb[it] = __ldcg(src + 1);
                 }
             }
 #pragma unroll

@@ -54,12 +54,17 @@ constexpr int NW = NT / 32;
 constexpr bool REG = D == 64;
 constexpr int RR = REG ? NT : 0;
 constexpr int QCAP = D == 64 ? 160 : 96;  // exact-evaluation queue capacity per pass
-constexpr int QCAP_SK = 64;      // ... in sketch mode (leaves room for 1536 sketch rows)
+#ifndef CX_QCAP_SK
+#define CX_QCAP_SK 64
+#endif
+constexpr int QCAP_SK = CX_QCAP_SK;  // ... in sketch mode (64 leaves room for 1536 sketch rows)
 // Rows beyond the 512 register rows of a CTA live in shared memory as fp32
 // (ROWS_SMEM), or as an fp16 SKETCH there with the exact fp32 rows read from L2
 // by the few exact evaluations (ROWS_SKETCH), or are read from L2 every round.
 enum : int { ROWS_L2 = 0, ROWS_SMEM = 1, ROWS_SKETCH = 2 };
-constexpr int SPITCH = D + 1;    // staged-row pitch (conflict-free column reads)
+// staged-row pitch: 16-byte aligned rows (cp.async / float4 stores); the evaluators'
+// float4 reads (thread t, row t) hit 8 distinct 16-byte slots per quarter warp
+constexpr int SPITCH = D + 4;
 constexpr int MAXC = 16;
 constexpr int MAXRPT_ALL = 4;    // rows per thread (S <= 2048)
 constexpr double HYB_MARGIN = 1e-12;
@@ -91,6 +96,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
             : "r"(a), "r"(parity)
             : "memory");
     } while (!ok);
+}
+// global -> shared 16 bytes without registers (L2 only); completes at cp.async.wait_all
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void st_async_v2(uint32_t raddr, uint64_t a, uint64_t b, uint32_t rmbar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
@@ -135,7 +144,7 @@ struct Sel64Params {
 #define STAMP(k)                                                        \
     do {                                                                \
         if (p.trace && p.trace != (long long*)1 && tid == 0 && rank == 0 && g == 0 && round < 4096) \
-            p.trace[round * 8 + (k)] = clock64();                       \
+            p.trace[round * 16 + (k)] = clock64();                      \
     } while (0)
 
 // X2 payload header: (score, row) + (|b|^2 of the candidate row, pad)
@@ -434,10 +443,16 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                     slot[k] = sl;
                     qown[sl] = tid;
                     float* st = stage + sl * SPITCH;
+                    if (!SMEM_ROWS && !(REG && k == 0)) {
+                        // sketch / L2 rows: the fp32 row comes from L2 asynchronously, so the
+                        // owner moves on and all queued rows' fetches overlap in one round trip
+                        const float* src = gX + (int64_t)(tid + k * NT) * p.rstride;
 #pragma unroll
-                    for (int c4 = 0; c4 < D / 4; ++c4) {
-                        const float4 v = (REG && k == 0) ? reg4(c4) : far4(tid + k * NT - RR)(c4);
-                        st[4 * c4] = v.x; st[4 * c4 + 1] = v.y; st[4 * c4 + 2] = v.z; st[4 * c4 + 3] = v.w;
+                        for (int c4 = 0; c4 < D / 4; ++c4) cp_async16(st + 4 * c4, src + 4 * c4);
+                    } else {
+#pragma unroll
+                        for (int c4 = 0; c4 < D / 4; ++c4)
+                            reinterpret_cast<float4*>(st)[c4] = (REG && k == 0) ? reg4(c4) : far4(tid + k * NT - RR)(c4);
                     }
                 } else {  // queue full: evaluate in place
                     const double d2 = (REG && k == 0) ? exact_sq(reg4, bw) : exact_sq<2>(far4(tid + k * NT - RR), bw);
@@ -448,17 +463,20 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                     }
                 }
             }
+            asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();
+            STAMP(6);
+            if (p.trace && p.trace != (long long*)1 && tid == 0 && rank == 0 && g == 0 && round < 4096)
+                p.trace[round * 16 + 8] = qn[0];  // rows queued for exact evaluation (before the cap)
             const int nq = min(qn[0], qcap);
             if (tid < nq) {
-                const float* st = stage + tid * SPITCH;
-                const double d2 = exact_sq<2>([&](int c4) {
-                    return make_float4(st[4 * c4], st[4 * c4 + 1], st[4 * c4 + 2], st[4 * c4 + 3]);
-                }, bw);
+                const float4* st = reinterpret_cast<const float4*>(stage + tid * SPITCH);
+                const double d2 = exact_sq<2>([&](int c4) { return st[c4]; }, bw);
                 qres[2 * tid] = d2;
                 qres[2 * tid + 1] = __dsqrt_rn(d2);
             }
             __syncthreads();
+            STAMP(7);
             if (tid == 0) qn[0] = 0;  // next use is after >= 2 more barriers
 #pragma unroll
             for (int k = 0; k < MAXRPT; ++k) {
@@ -832,7 +850,7 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     prm.out_scores = scores;
     prm.trace = nullptr;
     const char* tr = getenv("CX_SEL_TRACE");
-    if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 8 * 4096));
+    if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
     if (tr && tr[0] == 'p') prm.trace = (long long*)1;
     const size_t smem = sel64_layout(Rs, mode).total;
     const int rpt = (S + NT - 1) / NT;
@@ -869,17 +887,22 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     }
     if (prm.trace && prm.trace != (long long*)1) {  // debugging aid: average cycles per phase over rounds 2..take-2
         CX_CUDA(cudaStreamSynchronize(s));
-        double acc[6] = {0};
+        double acc[10] = {0};
         int n = 0;
         for (int r = 2; r < std::min(take, 4096) - 1; ++r, ++n) {
-            const long long* t = prm.trace + r * 8;
+            const long long* t = prm.trace + r * 16;
             for (int k = 0; k < 5; ++k) acc[k] += (double)(t[k + 1] - t[k]);
-            acc[5] += (double)(prm.trace[(r + 1) * 8] - t[0]);
+            acc[5] += (double)(prm.trace[(r + 1) * 16] - t[0]);
+            acc[6] += (double)(t[6] - t[0]);  // filter + staging
+            acc[7] += (double)(t[7] - t[6]);  // exact evaluation
+            acc[8] += (double)(t[1] - t[7]);  // apply
+            acc[9] += (double)t[8];           // queued rows
         }
         if (n > 0)
-            fprintf(stderr, "select64 C=%d S=%d Rs=%d rows=%d cycles/round: U=%.0f X1send=%.0f X1wait=%.0f "
-                            "H=%.0f X2=%.0f total=%.0f\n",
-                    C, S, Rs, mode, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
+            fprintf(stderr, "select%d C=%d S=%d Rs=%d rows=%d cycles/round: U=%.0f (filter+stage %.0f, exact %.0f, "
+                            "apply %.0f; %.1f rows queued) X1send=%.0f X1wait=%.0f H=%.0f X2=%.0f total=%.0f\n",
+                    D, C, S, Rs, mode, acc[0] / n, acc[6] / n, acc[7] / n, acc[8] / n, acc[9] / n, acc[1] / n,
+                    acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
         cudaFree(prm.trace);
     }
     return true;
