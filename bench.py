@@ -306,7 +306,7 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
                                f"L=8192 -> k=164 (98%), lambda=0.5; decode N={args.n_agents} agents, T={T_PRIV}",
                    "groups": G, "parallelism": f"groups sharded over {world} GPU(s)",
                    "l2": "flushed (256 MB write) between timed steps"},
-        "roofline": {"kernel": "select_kernel (greedy max-min selection)", "bound": "hbm",
+        "roofline": {"kernel": "select64_kernel (greedy max-min selection, thread-block clusters)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_source": peak_kind, "traffic": ncu_traffic("select64_kernel"),
                      "traffic_unit": "bytes per step: all select64 launches of one compression (ncu --set full, profiles/r1_ncu_full_summary.json)",
