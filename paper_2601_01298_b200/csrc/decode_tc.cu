@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             mbar_wait_sleep(&mbar[2 + tpar], (uint32_t)(ti >> 1) & 1u);
             if (tid == 0) TC_TRACE(ti * 16 + 5);
             {
-                const float* Opt = Op + (size_t)(OP_BUFS == 2 ? tpar : 0) * TM * OPS;
+                float* Opt = Op + (size_t)(OP_BUFS == 2 ? tpar : 0) * TM * OPS;
                 float v[TD];
                 const uint32_t trow_o = tO + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
@@ -620,26 +620,32 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[c0 + j] += w[j];
                 }
-                if (live) {
-                    const int a = a0 + r_own / QPG, hh = r_own % QPG;
+                if (live) {  // merged row -> the O_priv row it came from (in place, own row)
                     const float m_p = Mp[tpar * TM + r_own], l_p = Lp[tpar * TM + r_own];
                     const float m = fmaxf(m_s, m_p);
                     const float as = __expf(m_s - m), ap = __expf(m_p - m);
                     const float inv = 1.0f / (l_s * as + l_p * ap);
                     const float cs = as * inv, cp = ap * inv;
-                    float* out = b.out + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD;
-                    const float4* op = reinterpret_cast<const float4*>(Opt + r_own * OPS);
+                    float4* op = reinterpret_cast<float4*>(Opt + r_own * OPS);
 #pragma unroll
                     for (int c4 = 0; c4 < TD / 4; ++c4) {
                         const float4 pp = op[c4];
-                        reinterpret_cast<float4*>(out)[c4] =
-                            make_float4(v[4 * c4] * cs + pp.x * cp, v[4 * c4 + 1] * cs + pp.y * cp,
-                                        v[4 * c4 + 2] * cs + pp.z * cp, v[4 * c4 + 3] * cs + pp.w * cp);
+                        op[c4] = make_float4(v[4 * c4] * cs + pp.x * cp, v[4 * c4 + 1] * cs + pp.y * cp,
+                                             v[4 * c4 + 2] * cs + pp.z * cp, v[4 * c4 + 3] * cs + pp.w * cp);
                     }
                 }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                bar_sync(1, SWARPS * 32);  // merged rows in shared memory, TMEM O read
+                // coalesced store: a warp instruction writes two whole 256-B rows (a thread per
+                // row would put 32 rows' 16-B pieces in one instruction: 32 partial lines)
+                for (int e = tid; e < rows * (TD / 4); e += SWARPS * 32) {
+                    const int r = e / (TD / 4), c4 = e % (TD / 4);
+                    const int a = a0 + r / QPG, hh = r % QPG;
+                    float* out = b.out + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD;
+                    reinterpret_cast<float4*>(out)[c4] = reinterpret_cast<const float4*>(Opt + r * OPS)[c4];
+                }
             }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            bar_sync(1, SWARPS * 32);  // O / this tile's O_priv buffer fully read
+            bar_sync(1, SWARPS * 32);  // this tile's O_priv buffer fully read
             if (tid == 0) {
                 __threadfence_block();
                 *epi_done = ti + 1;    // private warps may now overwrite this parity's buffers
