@@ -140,6 +140,22 @@ __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// packed fp32x2 add (sm_100)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&d);
+}
+
+// one 32-byte sector per lane (256-bit load, sm_100), no L1 allocation
+__device__ __forceinline__ void ld_v8_na(const float* p, float (&x)[8]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
+                 : "l"(p));
+}
+
 // long waits (a role waiting for the other): back off instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* m, uint32_t parity) {
     uint32_t ok = 0;
@@ -460,24 +476,24 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
         auto stage_q = [&](int tile_q) {
             const int a0q = tile_q * AT;
             const int rows_q = min(AT, b.n_agents - a0q) * QPG;
-            float4 xa[8], xb[8];
+            // one 256-bit load per (row, 8-dim chunk): a lane reads a whole 32-B sector, and
+            // no L1 allocation over the private rows' prefetches
+            float x[8][8];
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
                 const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
-                xa[it] = xb[it] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (r < rows_q) {
                     const int a = a0q + r / QPG, hh = r % QPG;
-                    const float4* src = reinterpret_cast<const float4*>(
-                        b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD + 8 * c);
-                    xa[it] = __ldcg(src);  // L2 only: no L1 allocation over the private rows' prefetches
-                    xb[it] = __ldcg(src + 1);
+                    ld_v8_na(b.q + (((size_t)a * b.n_layers + l) * b.n_q + (size_t)g * QPG + hh) * TD + 8 * c, x[it]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) x[it][u] = 0.f;
                 }
             }
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
                 const int r = warp * 32 + (it >> 1) * 8 + (lane & 7), c = (it & 1) * 4 + (lane >> 3);
-                const float x[8] = {xa[it].x, xa[it].y, xa[it].z, xa[it].w, xb[it].x, xb[it].y, xb[it].z, xb[it].w};
-                split8_store(x, Qh, Ql, cm_off(r, 8 * c, TM));
+                split8_store(x[it], Qh, Ql, cm_off(r, 8 * c, TM));
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -533,6 +549,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             // softmax over the synapse keys, thread per row
             const bool live = r_own < rows;
             float mx = -INFINITY, l_s = 0.f;
+            float2 lsum2 = make_float2(0.f, 0.f);
             for (int c0 = 0; c0 < NS; c0 += 16) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)c0, v);
@@ -555,26 +572,34 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 float v[16];
                 tmem_ld16(trow + (uint32_t)c0, v);
                 float p[16];
-                if (c0 + 16 <= ks) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) p[j] = ex2(fmaf(v[j], c2, -m2));
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) p[j] = c0 + j < ks ? ex2(fmaf(v[j], c2, -m2)) : 0.f;
+                for (int u = 0; u < 8; ++u) {  // packed exponent arguments: v c2 - m2
+                    const float2 e = ffma2(make_float2(v[2 * u], v[2 * u + 1]), make_float2(c2, c2), make_float2(-m2, -m2));
+                    p[2 * u] = ex2(e.x);
+                    p[2 * u + 1] = ex2(e.y);
                 }
+                if (c0 + 16 > ks) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (c0 + j >= ks) p[j] = 0.f;
+                }
+                // P = hi + lo: hi = p truncated to bf16 (exact bits), lo = p - hi (exact in fp32)
+                // rounded to bf16; |P - p| <= 2^-17 |p|
                 uint32_t hv[8], lv[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    l_s += p[2 * u] + p[2 * u + 1];
-                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(p[2 * u], p[2 * u + 1]);
-                    const float2 hf = __bfloat1622float2(h2);
-                    const __nv_bfloat162 l2 = __floats2bfloat162_rn(p[2 * u] - hf.x, p[2 * u + 1] - hf.y);
-                    hv[u] = *reinterpret_cast<const uint32_t*>(&h2);
+                    const uint32_t b0 = __float_as_uint(p[2 * u]), b1 = __float_as_uint(p[2 * u + 1]);
+                    hv[u] = __byte_perm(b0, b1, 0x7632);  // the two high halves, packed bf16x2
+                    const float2 lo = add2(make_float2(p[2 * u], p[2 * u + 1]),
+                                           make_float2(-__uint_as_float(b0 & 0xFFFF0000u), -__uint_as_float(b1 & 0xFFFF0000u)));
+                    const __nv_bfloat162 l2 = __floats2bfloat162_rn(lo.x, lo.y);
                     lv[u] = *reinterpret_cast<const uint32_t*>(&l2);
+                    lsum2 = add2(lsum2, make_float2(p[2 * u], p[2 * u + 1]));
                 }
                 tmem_st8(trow_ph + (uint32_t)(c0 / 2), hv);
                 tmem_st8(trow_pl + (uint32_t)(c0 / 2), lv);
             }
+            l_s = lsum2.x + lsum2.y;
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             bar_sync(1, SWARPS * 32);  // S of this tile fully read; P in TMEM
