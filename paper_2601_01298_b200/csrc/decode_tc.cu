@@ -265,12 +265,17 @@ __device__ __forceinline__ void prefetch_rows16_l1(const float* base, int r0, in
     if (L1PF && r0 + (lane >> 1) < nrows)
         asm volatile("prefetch.global.L1 [%0];" ::"l"(base + (size_t)r0 * TD + lane * 32));
 }
-// Private rows are read with ld.global.cg (L2-coherent, no L1 allocation: they have
-// no reuse).  q lives in registers: lane rl of a row's 8 lanes holds dims
-// [4 rl, 4 rl + 4) and [32 + 4 rl, 32 + 4 rl + 4) of every head.
+// q lives in registers: lane rl of a row's 8 lanes holds dims [8 rl, 8 rl + 8) of every
+// head (one 256-bit load per row and lane), as qa = [8 rl, 8 rl + 4), qb = [8 rl + 4, 8 rl + 8).
+// 256-bit load of a row's 8-dim chunk through L1 (the private rows are prefetched there)
+__device__ __forceinline__ void ld_row8(const float* p, float4& a, float4& b) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p));
+}
 
 // score of one row per 8-lane group (row t of lane group lane / 8, whose lanes hold
-// its dims [4 rl, 4 rl + 4) in ka and [32 + 4 rl, ...) in kb): packed FMAs, then a
+// its dims [8 rl, 8 rl + 4) in ka and [8 rl + 4, 8 rl + 8) in kb): packed FMAs, then a
 // reduce-scatter so that the 8 lanes end up with one head each; stored when `valid`
 template <int QPG>
 __device__ __forceinline__ void score_group(const float4& ka, const float4& kb, int t, bool valid,
@@ -321,8 +326,7 @@ __device__ __forceinline__ void score_rows(const float* tk, int r0, int nt, cons
         const int t = r0 + 4 * j + rg;
         const float4* kp = reinterpret_cast<const float4*>(tk + (size_t)t * TD);
         if (!PRED || t < nt) {
-            ka[j] = ldrow(kp + rl);
-            kb[j] = ldrow(kp + 8 + rl);
+            ld_row8(reinterpret_cast<const float*>(kp + 2 * rl), ka[j], kb[j]);
         } else {
             ka[j] = kb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -707,14 +711,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 float4 qa[QPG], qb[QPG];
 #pragma unroll
                 for (int h = 0; h < QPG; ++h) {
-                    qa[h] = __ldg(reinterpret_cast<const float4*>(qrow + (size_t)h * TD) + (lane & 7));
-                    qb[h] = __ldg(reinterpret_cast<const float4*>(qrow + (size_t)h * TD) + 8 + (lane & 7));
+                    ld_row8(qrow + (size_t)h * TD + 8 * (lane & 7), qa[h], qb[h]);
                 }
                 float4 nka = make_float4(0.f, 0.f, 0.f, 0.f), nkb = nka;
                 float2 nvv = make_float2(0.f, 0.f);
                 if (app) {
-                    nka = __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + (lane & 7));
-                    nkb = __ldg(reinterpret_cast<const float4*>(b.new_keys + noff) + 8 + (lane & 7));
+                    ld_row8(b.new_keys + noff + 8 * (lane & 7), nka, nkb);
                     nvv = __ldg(reinterpret_cast<const float2*>(b.new_values + noff) + lane);
                 }  // (appended at the end of the agent: a store here would hold back every load below)
                 // ---- scores of the stored rows [0, len): 16-row batches, then 4-row groups ----
@@ -815,8 +817,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 }
                 if (app) {  // the fused append of the new token's K/V (row len; never read above)
                     if (lane < 8) {
-                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[lane] = nka;
-                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[8 + lane] = nkb;
+                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[2 * lane] = nka;
+                        reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[2 * lane + 1] = nkb;
                     }
                     reinterpret_cast<float2*>(b.tail_values + toff + (size_t)len * TD)[lane] = nvv;
                 }
