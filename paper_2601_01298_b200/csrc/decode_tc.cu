@@ -424,10 +424,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             for (int k = 0; k < IT; ++k) {
                 const int it = base + tid + k * ST, j = it >> 3, c = it & 7;
                 ka[k] = kb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (j < ks) {
-                    ka[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c));
-                    kb[k] = __ldg(reinterpret_cast<const float4*>(sk + (size_t)j * TD + 8 * c) + 1);
-                }
+                if (j < ks) ld_row8(sk + (size_t)j * TD + 8 * c, ka[k], kb[k]);
             }
 #pragma unroll
             for (int k = 0; k < IT; ++k) {
