@@ -413,7 +413,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                             (uint32_t)(QPG * TD * sizeof(float)));
         }
         const float* sk = b.syn_keys + (size_t)lh * ks * TD;
-        const float* sv = b.syn_values + (size_t)lh * ks * TD;
         // items per pass per thread: all NS * 8 = 1408 items (k <= 176) in ONE pass, so the
         // staging costs two loaded-latency round trips (K, then V) instead of nine
         constexpr int ST = SWARPS * 32, IT = (TNS_MAX * 8 + ST - 1) / ST;
@@ -433,25 +432,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     const float x[8] = {ka[k].x, ka[k].y, ka[k].z, ka[k].w, kb[k].x, kb[k].y, kb[k].z, kb[k].w};
                     split8_store(x, Kh, Kl, cm_off(j, 8 * c, NS));  // B of S = Q K^T: N = keys, K = dims
                 }
-            }
-        }
-        // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
-        for (int base = 0; base < TD * (NS / 8); base += IT * ST) {
-            float xv[IT][8];
-#pragma unroll
-            for (int k = 0; k < IT; ++k) {
-                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int j = 8 * jc + u;
-                    xv[k][u] = (jc < NS / 8 && j < ks) ? __ldg(sv + (size_t)j * TD + c) : 0.f;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < IT; ++k) {
-                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
-                // B of O = P V (N = dims, K = keys): hi at N-row c, lo at N-row 64 + c (+1024 B)
-                if (jc < NS / 8) split8_store(xv[k], Vhl, Vhl + cm_off(TD, 0, 2 * TD), cm_off(c, 8 * jc, 2 * TD));
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -529,6 +509,31 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
         if (!(skip & 1) && (int)blockIdx.y < n_tiles) {
             stage_q(blockIdx.y);
             issue_s();
+        }
+        {  // V_syn^T is first needed by the first P.V: staged while the first scores run
+            const float* sv = b.syn_values + (size_t)lh * ks * TD;
+            constexpr int ST = SWARPS * 32, IT = (TNS_MAX * 8 + ST - 1) / ST;
+        // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
+        for (int base = 0; base < TD * (NS / 8); base += IT * ST) {
+            float xv[IT][8];
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = 8 * jc + u;
+                    xv[k][u] = (jc < NS / 8 && j < ks) ? __ldg(sv + (size_t)j * TD + c) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
+                // B of O = P V (N = dims, K = keys): hi at N-row c, lo at N-row 64 + c (+1024 B)
+                if (jc < NS / 8) split8_store(xv[k], Vhl, Vhl + cm_off(TD, 0, 2 * TD), cm_off(c, 8 * jc, 2 * TD));
+            }
+        }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_sync(1, SWARPS * 32);
         }
         int ti = 0;
         for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
