@@ -495,7 +495,10 @@ void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const bool allow_v2 = !pin || !strcmp(pin, "v2");
     if (allow_tc && decode_tc_launch(ctx, b, s)) return;
     if (pin && !strcmp(pin, "tc")) fail(CX_PRECONDITION_ERROR, "decode_step: CX_DECODE=tc does not apply to this shape");
-    if (allow_v2 && b.d_k == DV2_DK && b.k_syn <= 32 * DV2_KPL && b.t_cap <= 64) {
+    auto al = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
+    const bool v2_aligned = al(b.syn_keys, 16) && al(b.syn_values, 16) && al(b.q, 16) && al(b.tail_keys, 16) &&
+                            al(b.tail_values, 16) && al(b.new_keys, 16) && al(b.new_values, 16) && al(b.out, 8);
+    if (allow_v2 && v2_aligned && b.d_k == DV2_DK && b.k_syn <= 32 * DV2_KPL && b.t_cap <= 64) {
         bool done = false;
         switch (qpg) {
             case 1: done = launch_decode_v2<1>(ctx, b, s); break;

@@ -846,6 +846,11 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
 bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int qpg = b.n_q / b.n_kv;
     if (b.d_k != TD || b.k_syn < 1 || b.k_syn > TNS_MAX || b.t_cap > TTAIL) return false;
+    // 256-bit loads of q, K rows, the new key and K_syn; 16-byte accesses elsewhere
+    auto al = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
+    if (!al(b.q, 32) || !al(b.tail_keys, 32) || !al(b.new_keys, 32) || !al(b.syn_keys, 32) || !al(b.out, 16) ||
+        !al(b.tail_values, 16) || !al(b.new_values, 16) || !al(b.syn_values, 16))
+        return false;
     const TcLayout lay = tc_layout(b.k_syn, qpg);
     static int max_optin = -1;
     if (max_optin < 0) {

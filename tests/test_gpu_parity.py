@@ -481,23 +481,32 @@ def test_bench_landmarks_on_b200(cx, orc):
     assert wins / 100 == exp["hybrid_win_rate"] and wins >= 90
 
 
-@pytest.mark.parametrize("k,Tc", [(0, 33), (20, 80), (164, 33)])
-def test_decode_default_dispatch_edges(dev, orc, k, Tc):
+@pytest.mark.parametrize("k,Tc,off", [(0, 33, 0), (20, 80, 0), (164, 33, 0), (164, 33, 4), (164, 33, 2)])
+def test_decode_default_dispatch_edges(dev, orc, k, Tc, off):
     """No pin: the default dispatch (tcgen05 -> v2 -> v1) on shapes the tcgen05
     kernel declines -- an empty synapse (k_syn = 0: a snapshot before the river has
-    context) and more private rows than it stages (t_cap > 64) -- plus the common case."""
+    context), more private rows than it stages (t_cap > 64), and buffers `off` floats
+    past a 32-byte boundary (off=4: 16-B aligned, no 256-bit loads -> v2; off=2: 8-B
+    aligned -> v1) -- plus the common case."""
     import torch
     gen = torch.Generator(device="cuda").manual_seed(5 + k + Tc)
     N, Lr, H, Q, dk = 6, 2, 2, 14, 64
-    syn_k = torch.randn(Lr, H, max(k, 1), dk, device="cuda", generator=gen)[:, :, :k].contiguous()
-    syn_v = torch.randn(Lr, H, max(k, 1), dk, device="cuda", generator=gen)[:, :, :k].contiguous()
-    tk = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
-    tv = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
+
+    def mk(*shape, empty=False):  # contiguous tensor starting `off` floats into a fresh buffer
+        n = int(np.prod(shape))
+        buf = torch.empty(n + off, device="cuda") if empty else torch.randn(n + off, device="cuda", generator=gen)
+        return buf[off:off + n].view(*shape)
+
+    syn_k = mk(Lr, H, k, dk)
+    syn_v = mk(Lr, H, k, dk)
+    tk = mk(N, Lr, H, Tc, dk)
+    tv = mk(N, Lr, H, Tc, dk)
     tl = torch.randint(0, Tc, (N,), device="cuda", generator=gen).to(torch.int32)
-    nk = torch.randn(N, Lr, H, dk, device="cuda", generator=gen)
-    nv = torch.randn(N, Lr, H, dk, device="cuda", generator=gen)
-    q = torch.randn(N, Lr, Q, dk, device="cuda", generator=gen)
-    out = torch.empty_like(q)
+    nk = mk(N, Lr, H, dk)
+    nv = mk(N, Lr, H, dk)
+    q = mk(N, Lr, Q, dk)
+    out = mk(N, Lr, Q, dk, empty=True)
+    assert q.data_ptr() % 32 == (4 * off) % 32
     dev.decode_step(syn_k, syn_v, tk, tv, tl, q, out, nk, nv)
     torch.cuda.synchronize()
     o, tkn, tvn, tln = out.cpu().numpy(), tk.cpu().numpy(), tv.cpu().numpy(), tl.cpu().numpy()
