@@ -438,7 +438,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
         bar_sync(1, SWARPS * 32);
         if (tid == 0) TC_TRACE(1000);
     }
-    // TMEM columns: S [0, NS), O [NS, NS + 64), P hi [256, 256 + NS/2), P lo [256 + NS/2, 256 + NS)
     // TMEM columns: S [0, NS), O [NS, NS + 128) (P_hi V_hi + P_lo V_hi | P_hi V_lo), P hi / lo after
     const uint32_t tS = *tbase_s, tO = tS + (uint32_t)NS, tPh = tS + (uint32_t)max(256, NS + 2 * TD),
                    tPl = tPh + (uint32_t)(NS / 2);
