@@ -133,3 +133,23 @@ def test_compress_grouped_host_matches_device(cx, G, pinned):
     assert torch.equal(sk, dsk.cpu()) and torch.equal(sv, dsv.cpu())
     with pytest.raises(cx.errors.config_error):
         device.compress_grouped_host(hk, hv, hq, 0, 0.5)
+
+
+def test_compress_grouped_host_mha_d128(cx):
+    """The reference-mode cloud through the host path: a 2-head MHA cache's rows
+    (d_model = 128, heads concatenated, col_step = d_k; synapse.cpp:423-457) -- the
+    d = 128 selection kernel and the fallback chunking -- == the device path, bitwise."""
+    import torch
+    from paper_2601_01298_b200 import device
+    G, L, dm, H, k = 3, 2100, 128, 2, 45
+    gen = torch.Generator().manual_seed(77)
+    hk = torch.randn(G, L, dm, generator=gen).pin_memory()
+    hv = torch.randn(G, L, dm, generator=gen).pin_memory()
+    hq = torch.randn(G, H, dm // H, generator=gen).pin_memory()
+    rows, scores, sk, sv = device.compress_grouped_host(hk, hv, hq, k, 0.5, mode="mha")
+    dr, ds, dsk, dsv = device.compress_grouped(hk.cuda(), hv.cuda(), hq.cuda(), k, 0.5, mode="mha")
+    torch.cuda.synchronize()
+    assert torch.equal(rows, dr.cpu()) and torch.equal(scores, ds.cpu())
+    assert torch.equal(sk, dsk.cpu()) and torch.equal(sv, dsv.cpu())
+    gi = torch.arange(G)[:, None]
+    assert torch.equal(sk, hk[gi, rows]) and torch.equal(sv, hv[gi, rows])
