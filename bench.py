@@ -295,7 +295,7 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
     bytes_per_launch = COMPRESS_BYTES * keys.shape[0] / G
     achieved = bytes_per_launch / (sel_ms * 1e-3) / 1e9
     dec = run_decode(args, dev, rank, world)
-    e2e = run_e2e(args, dev) if rank == 0 else None
+    e2e = run_e2e(args, dev, rank, world)
     cfg5 = run_cfg5(args, dev) if rank == 0 else None
     cfg4 = run_cfg4(args, dev, rank, world)
     line = {
@@ -540,6 +540,9 @@ def run_cfg4(args, dev, rank=0, world=1, steps=3):
            torch.empty(ge - gb, k4, D, device=dev), torch.empty(ge - gb, k4, D, device=dev))
     cxd.compress_grouped(keys, values, queries, k4, LAM, out=out)
     torch.cuda.synchronize()
+    if world > 1:  # rank 0 comes from the e2e / cfg5 legs: align the ranks before timing
+        dist.barrier()
+        torch.cuda.synchronize()
     times = []
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -560,18 +563,23 @@ def run_cfg4(args, dev, rank=0, world=1, steps=3):
             "compressions_per_s": 1000.0 / ms, "ms_per_step": ms, "groups_per_gpu": ge - gb}
 
 
-def run_e2e(args, dev):
+def run_e2e(args, dev, rank=0, world=1):
     """compressions/s through the C-ABI with HOST buffers: pinned H2D of the
-    step's keys, values and queries, the compression, D2H of the synapse."""
+    step's keys, values and queries, the compression, D2H of the synapse.  N > 1:
+    each rank runs the call on its shard of the groups (its own host buffers); the
+    step time is the max over ranks."""
     import torch
+    import torch.distributed as dist
 
     from paper_2601_01298_b200 import device as cxd
-    hk = torch.randn(G, L, D).pin_memory()
-    hv = torch.randn(G, L, D).pin_memory()
-    hq = torch.randn(G, N_Q // N_KV, D).pin_memory()
-    h_out = (torch.empty(G, K, dtype=torch.int64).pin_memory(), torch.empty(G, K, dtype=torch.float64).pin_memory(),
-             torch.empty(G, K, D).pin_memory(), torch.empty(G, K, D).pin_memory())
-    h_rows, h_sk, h_sv = h_out[0], h_out[2], h_out[3]
+    from paper_2601_01298_b200.parallel import shard_range
+    gb, ge = shard_range(G, rank, world)
+    g = ge - gb
+    hk = torch.randn(g, L, D).pin_memory()
+    hv = torch.randn(g, L, D).pin_memory()
+    hq = torch.randn(g, N_Q // N_KV, D).pin_memory()
+    h_out = (torch.empty(g, K, dtype=torch.int64).pin_memory(), torch.empty(g, K, dtype=torch.float64).pin_memory(),
+             torch.empty(g, K, D).pin_memory(), torch.empty(g, K, D).pin_memory())
 
     def step():  # ONE C-ABI call (cx_compress_grouped_host): chunked uploads overlap the compressions
         cxd.compress_grouped_host(hk, hv, hq, K, LAM, out=h_out)
@@ -579,6 +587,9 @@ def run_e2e(args, dev):
     for _ in range(2):
         step()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
     reps = max(3, min(args.steps, 10))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -587,10 +598,14 @@ def run_e2e(args, dev):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    # keys and queries are uploaded; values cross PCIe only at the selected rows (the
-    # pinned buffer is read zero-copy by the gather: G x K rows x D floats)
-    h2d = (hk.numel() + hq.numel()) * 4 + G * K * D * 4
-    d2h = h_rows.numel() * 8 + h_out[1].numel() * 8 + (h_sk.numel() + h_sv.numel()) * 4
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    # whole job, all ranks: keys and queries are uploaded; values cross PCIe only at the
+    # selected rows (the pinned buffer is read zero-copy by the gather: G x K rows x D floats)
+    h2d = (G * L * D + G * (N_Q // N_KV) * D) * 4 + G * K * D * 4
+    d2h = G * K * 8 * 2 + 2 * G * K * D * 4
     return {"value": 1000.0 / ms, "unit": "compressions/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms}
 
