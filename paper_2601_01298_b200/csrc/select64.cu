@@ -139,6 +139,7 @@ struct Sel64Params {
     int64_t* out_rows;
     double* out_scores;
     long long* trace;    // optional per-round phase timestamps (CX_SEL_TRACE=1)
+    int dbg;             // timing experiments only (CX_SEL_DBG): results are wrong when nonzero
 };
 
 #define STAMP(k)                                                        \
@@ -258,18 +259,19 @@ __device__ __forceinline__ float gram_lower_bound(float nx, float nb, float dot)
     const float sum = __fadd_rn(nx, nb);
     const float s = __fsub_rn(sum, __fmul_rn(2.0f, dot));
     const float e = __fmaf_ru(GRAM_SLACK, sum, 0x1p-100f);
-    return __fsub_rd(s, e);
+    // a non-finite dot (overflow; -inf would make the bound +inf) bounds nothing: -inf
+    return isfinite(dot) ? __fsub_rd(s, e) : -INFINITY;
 }
 
 // The same bound when x is only known through its fp16 rounding x~ (the sketch):
 // |x_c - x~_c| <= 2^-11 |x_c| + 2^-25 (subnormals), so |2 (x - x~).b| <= 2^-11 (|x|^2 +
-// |b|^2) + 2^-24 sqrt(D) |b| (<= 2^-21 |b| at d = 64, 2^-20 |b| at d = 128), added to the slack.  An fp16 overflow makes the dot inf/NaN,
+// |b|^2) + 2^-24 sqrt(D) |b| (<= 2^-21 |b| at d = 64, 2^-20 |b| at d = 128), added to the slack.  An fp16 overflow makes the dot +-inf/NaN,
 // the comparison false, and the row is evaluated exactly.
 __device__ __forceinline__ float gram_lower_bound_sketch(float nx, float nb, float dot) {
     const float sum = __fadd_rn(nx, nb);
     const float s = __fsub_rn(sum, __fmul_rn(2.0f, dot));
     const float e = __fadd_ru(__fmaf_ru(GRAM_SLACK + 0x1p-11f, sum, 0x1p-100f), __fmul_ru(SKETCH_SUB, __fsqrt_ru(nb)));
-    return __fsub_rd(s, e);
+    return isfinite(dot) ? __fsub_rd(s, e) : -INFINITY;  // fp16 overflow (+-inf / NaN): evaluate exactly
 }
 
 template <int RPT, int ROWMODE>
@@ -431,7 +433,9 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                     need = true;
                 } else {
                     if (ROWMODE == ROWS_SKETCH && !(REG && k == 0)) {
+                        if (p.dbg == 1) continue;
                         need = !(gram_lower_bound_sketch(nx[k], nbw, sketch_dot(tid + k * NT - RR, bw)) > th[k]);
+                        if (p.dbg == 2 && need) continue;
                     } else {
                         const float dt = (REG && k == 0) ? dot_f32x2(reg4, bw) : dot_f32x2<4>(far4(tid + k * NT - RR), bw);
                         need = !(gram_lower_bound(nx[k], nbw, dt) > th[k]);
@@ -462,6 +466,10 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                         th[k] = __double2float_ru(d2);
                     }
                 }
+            }
+            if (p.trace && p.trace != (long long*)1) {  // tracing only: split filter / staging wait
+                __syncthreads();
+                STAMP(9);
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();
@@ -849,6 +857,7 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     prm.out_rows = rows;
     prm.out_scores = scores;
     prm.trace = nullptr;
+    prm.dbg = getenv("CX_SEL_DBG") ? atoi(getenv("CX_SEL_DBG")) : 0;
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
     if (tr && tr[0] == 'p') prm.trace = (long long*)1;
@@ -887,21 +896,22 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     }
     if (prm.trace && prm.trace != (long long*)1) {  // debugging aid: average cycles per phase over rounds 2..take-2
         CX_CUDA(cudaStreamSynchronize(s));
-        double acc[10] = {0};
+        double acc[11] = {0};
         int n = 0;
         for (int r = 2; r < std::min(take, 4096) - 1; ++r, ++n) {
             const long long* t = prm.trace + r * 16;
             for (int k = 0; k < 5; ++k) acc[k] += (double)(t[k + 1] - t[k]);
             acc[5] += (double)(prm.trace[(r + 1) * 16] - t[0]);
             acc[6] += (double)(t[6] - t[0]);  // filter + staging
+            acc[10] += (double)(t[9] - t[0]);  // filter + staging issue (before the cp.async wait)
             acc[7] += (double)(t[7] - t[6]);  // exact evaluation
             acc[8] += (double)(t[1] - t[7]);  // apply
             acc[9] += (double)t[8];           // queued rows
         }
         if (n > 0)
             fprintf(stderr, "select%d C=%d S=%d Rs=%d rows=%d cycles/round: U=%.0f (filter+stage %.0f, exact %.0f, "
-                            "apply %.0f; %.1f rows queued) X1send=%.0f X1wait=%.0f H=%.0f X2=%.0f total=%.0f\n",
-                    D, C, S, Rs, mode, acc[0] / n, acc[6] / n, acc[7] / n, acc[8] / n, acc[9] / n, acc[1] / n,
+                            "apply %.0f; %.1f rows queued; filter+issue %.0f) X1send=%.0f X1wait=%.0f H=%.0f X2=%.0f total=%.0f\n",
+                    D, C, S, Rs, mode, acc[0] / n, acc[6] / n, acc[7] / n, acc[8] / n, acc[9] / n, acc[10] / n, acc[1] / n,
                     acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
         cudaFree(prm.trace);
     }

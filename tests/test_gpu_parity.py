@@ -201,6 +201,28 @@ def test_select128_matches_reference(dev, orc, monkeypatch, G, L, k, force):
         assert scores[gi].cpu().numpy().tobytes() == sc.tobytes(), gi
 
 
+@pytest.mark.parametrize("force", ["3", "5"])
+def test_sketch_rows_fp16_overflow(dev, orc, monkeypatch, force):
+    """Sketch-row mode with coordinates beyond the fp16 range (+-65504): the sketch dot
+    becomes +-inf / NaN, and the filter must then evaluate exactly (a -inf dot would
+    otherwise make the lower bound +inf and skip the row)."""
+    import torch
+    monkeypatch.setenv("CX_SEL_C", force)
+    L, d, k = 4000, 64, 40
+    r = orc.rng(515)
+    keys = r.gaussian_f32(L * d).reshape(L, d)
+    keys[::97, 0] = 1.0e5     # rows whose fp16 sketch overflows to +inf
+    keys[50::131, 3] = -2.0e5  # and to -inf
+    a = np.abs(r.gaussian_f32(L)).astype(np.float64)
+    kt = torch.from_numpy(keys).cuda()[None]
+    at = torch.from_numpy(a).cuda()[None]
+    rows, scores = dev.select_grouped(kt, at, k, 0.5)
+    torch.cuda.synchronize()
+    idx, sc = orc.select_landmarks_points(keys, a, k, 0.5)
+    assert rows.cpu().numpy()[0].tobytes() == idx.tobytes()
+    assert scores.cpu().numpy()[0].tobytes() == sc.tobytes()
+
+
 def test_full_cfg2_properties(dev):
     """All 48 (layer, KV-head) groups at L=8192, k=164: size-independent
     properties (sorted unique rows in range, gather == source rows)."""
