@@ -139,7 +139,6 @@ struct Sel64Params {
     int64_t* out_rows;
     double* out_scores;
     long long* trace;    // optional per-round phase timestamps (CX_SEL_TRACE=1)
-    int dbg;             // timing experiments only (CX_SEL_DBG): results are wrong when nonzero
 };
 
 #define STAMP(k)                                                        \
@@ -433,9 +432,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
                     need = true;
                 } else {
                     if (ROWMODE == ROWS_SKETCH && !(REG && k == 0)) {
-                        if (p.dbg == 1) continue;
                         need = !(gram_lower_bound_sketch(nx[k], nbw, sketch_dot(tid + k * NT - RR, bw)) > th[k]);
-                        if (p.dbg == 2 && need) continue;
                     } else {
                         const float dt = (REG && k == 0) ? dot_f32x2(reg4, bw) : dot_f32x2<4>(far4(tid + k * NT - RR), bw);
                         need = !(gram_lower_bound(nx[k], nbw, dt) > th[k]);
@@ -857,7 +854,6 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     prm.out_rows = rows;
     prm.out_scores = scores;
     prm.trace = nullptr;
-    prm.dbg = getenv("CX_SEL_DBG") ? atoi(getenv("CX_SEL_DBG")) : 0;
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
     if (tr && tr[0] == 'p') prm.trace = (long long*)1;
