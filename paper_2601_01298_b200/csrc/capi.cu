@@ -603,8 +603,21 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         const int w = dim == 64 ? select64_wave(count, n_groups) : 0;
         const int WAVE = w > 0 ? w : 15;
         std::vector<int> start;
-        for (int g0 = 0, first = n_groups % WAVE ? n_groups % WAVE : WAVE; g0 < n_groups; g0 += (g0 ? WAVE : first))
-            start.push_back(g0);
+        if (const char* ch = getenv("CX_E2E_CHUNKS")) {  // tuning only: explicit chunk sizes "a,b,c"
+            int g0 = 0;
+            for (const char* q = ch; *q && g0 < n_groups;) {
+                const int n = std::max(1, atoi(q));
+                start.push_back(g0);
+                g0 += n;
+                while (*q && *q != ',') ++q;
+                if (*q == ',') ++q;
+            }
+            if (start.empty()) start.push_back(0);
+            if (g0 < n_groups) start.push_back(g0);  // the rest as one chunk
+        } else {
+            for (int g0 = 0, first = n_groups % WAVE ? n_groups % WAVE : WAVE; g0 < n_groups; g0 += (g0 ? WAVE : first))
+                start.push_back(g0);
+        }
         const int nch = (int)start.size();
         start.push_back(n_groups);
         while ((int)c->hev.size() < nch) {
