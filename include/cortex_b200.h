@@ -87,6 +87,10 @@ cx_status cx_mean_pairwise_reduction(const float* cloud, int64_t count, int dim,
 cx_status cx_mean_pairwise_reduction_subset(const float* cloud, int64_t count, int dim,
                                             const int64_t* rows, int64_t n_rows, double* out);
 
+/* gate.hpp:22 / gate.cpp:27-43 gate_score(h_main, t_side): fp64 cosine clamped to [-1, 1];
+ * CX_DEGENERATE_INPUT_ERROR for a zero-norm input.  Host pointers; computed on the device. */
+cx_status cx_gate_score(const float* h_main, const float* t_side, int64_t n, double* out);
+
 /* kernels.hpp:40-42 attend(q, keys, values, n_entries, n_heads, d_k, out)
  * fp64 accumulation like the reference (tolerance 1e-6, test_kernels.cpp:159). */
 cx_status cx_attend(const float* q, const float* keys, const float* values,
@@ -188,6 +192,15 @@ typedef struct cx_decode_batch {
 } cx_decode_batch;
 
 cx_status cx_decode_step_dev(cx_ctx* ctx, const cx_decode_batch* b, void* stream);
+
+/* gate.hpp:26 / gate.cpp:45-61 decide(h_main, t_side, theta) for n_pairs (row h[i], row t[i])
+ * device pairs (row strides in floats): scores[i] (NaN when degenerate), accepted[i] =
+ * scores[i] >= theta, degenerate[i] = zero norm (accepted and degenerate may be NULL).
+ * theta outside [-1, 1] -> CX_PRECONDITION_ERROR before any work (gate.cpp:47-48).
+ * The gate fused after an agent step: h = main-model hidden states, t = thoughts. */
+cx_status cx_gate_decide_dev(cx_ctx* ctx, int64_t n_pairs, int dim, const float* h, int64_t h_stride,
+                             const float* t, int64_t t_stride, double theta, double* scores,
+                             uint8_t* accepted, uint8_t* degenerate, void* stream);
 
 /* ======================================================================
  * Device-resident KvCache (model.hpp:67-113) and Referential Injection.

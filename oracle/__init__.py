@@ -193,6 +193,13 @@ class Backend:
         self._check(st, "select_landmarks_points")
         return idx[: n.value].copy(), sc[: n.value].copy()
 
+    # ---- gate.cpp ------------------------------------------------------
+    def gate_score(self, h_main, t_side) -> float:
+        h, t = _f32(h_main).reshape(-1), _f32(t_side).reshape(-1)
+        out = C.c_double(0.0)
+        self._check(self._fn("gate_score")(_p(h, _f32p), _p(t, _f32p), C.c_int64(h.size), C.byref(out)), "gate_score")
+        return out.value
+
     def hausdorff_distance(self, cloud, landmarks) -> float:
         c, l = _f32(cloud), _f32(landmarks)
         out = C.c_double(0)

@@ -233,6 +233,23 @@ int orc_select_landmarks_points(const float* cloud, int64_t count, int dim,
     return ORC_OK;
 }
 
+/* ---- gate.cpp:27-43 ------------------------------------------------------ */
+
+int orc_gate_score(const float* h_main, const float* t_side, int64_t n, double* out) {
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (int64_t i = 0; i < n; ++i) {  /* one pass, three sequential sums */
+        const double a = h_main[i], b = t_side[i];
+        dot += a * b;
+        na += a * a;
+        nb += b * b;
+    }
+    if (na == 0.0 || nb == 0.0) return ORC_DEGENERATE_INPUT_ERROR;
+    double s = dot / (sqrt(na) * sqrt(nb));
+    s = s < -1.0 ? -1.0 : (1.0 < s ? 1.0 : s); /* std::clamp(s, -1, 1) */
+    *out = s;
+    return ORC_OK;
+}
+
 /* ---- synapse.cpp:276-302 ------------------------------------------------ */
 
 int orc_hausdorff_distance(const float* cloud, int64_t count, int dim,

@@ -76,6 +76,10 @@ int orc_select_landmarks_points(const float* cloud, int64_t count, int dim,
                                 int64_t* out_indices, double* out_scores, int64_t* out_n);
 
 /* synapse.cpp:276-302. */
+/* gate.cpp:27-43 gate_score: fp64 cosine with sequential sums, clamped to [-1, 1];
+ * ORC_DEGENERATE_INPUT_ERROR on a zero norm. */
+int orc_gate_score(const float* h_main, const float* t_side, int64_t n, double* out);
+
 int orc_hausdorff_distance(const float* cloud, int64_t count, int dim,
                            const float* landmarks, int64_t m, int ldim, double* out);
 int orc_hausdorff_to_subset(const float* cloud, int64_t count, int dim,

@@ -15,6 +15,7 @@
 #include "cortex/kernels.hpp"
 #include "cortex/model.hpp"
 #include "cortex/rng.hpp"
+#include "cortex/gate.hpp"
 #include "cortex/synapse.hpp"
 
 #include <algorithm>
@@ -119,6 +120,13 @@ int ref_select_landmarks_points(const float* cloud, int64_t count, int dim, cons
         std::copy(r.indices.begin(), r.indices.end(), idx);
         std::copy(r.scores.begin(), r.scores.end(), scores);
         *out_n = static_cast<int64_t>(r.indices.size());
+    });
+}
+
+int ref_gate_score(const float* h, const float* t, int64_t n, double* out) {
+    return guarded([&] {
+        *out = gate_score(std::span<const float>(h, static_cast<size_t>(n)),
+                          std::span<const float>(t, static_cast<size_t>(n)));
     });
 }
 

@@ -7,6 +7,7 @@ Layout:
   _lib.py        ctypes binding of libcortex_b200.so
   synapse.py     cortex::synapse API (synapse.hpp)
   kernels.py     cortex::kernels::attend (kernels.hpp)
+  gate.py        cortex::gate_score / decide (gate.hpp)
   model.py       Origin, ModelConfig, KvCache (model.hpp, config.hpp)
   injector.py    KvBlock, inject, VirtualPositionPlanner (injector.hpp)
   device.py      the batched device path (grouped compression, N-agent decode)
@@ -14,6 +15,7 @@ Layout:
 """
 from . import errors  # noqa: F401
 from ._lib import EXPORTED_SYMBOLS, LIB_PATH, lib  # noqa: F401
+from .gate import GateDecision, decide, gate_score  # noqa: F401
 from .injector import InjectionRecord, KvBlock, VirtualPositionPlanner, inject  # noqa: F401
 from .kernels import attend  # noqa: F401
 from .model import KvCache, ModelConfig, Origin  # noqa: F401

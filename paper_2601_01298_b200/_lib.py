@@ -74,6 +74,9 @@ _SIGS = [
     ("cx_mean_pairwise_reduction", C.c_int, [c_f32p, C.c_int64, C.c_int, c_f32p, C.c_int64, C.c_int, c_f64p]),
     ("cx_mean_pairwise_reduction_subset", C.c_int, [c_f32p, C.c_int64, C.c_int, c_i64p, C.c_int64, c_f64p]),
     ("cx_attend", C.c_int, [c_f32p, c_f32p, c_f32p, C.c_int64, C.c_int, C.c_int, c_f32p]),
+    ("cx_gate_score", C.c_int, [c_f32p, c_f32p, C.c_int64, c_f64p]),
+    ("cx_gate_decide_dev", C.c_int,
+     [c_vp, C.c_int64, C.c_int, c_vp, C.c_int64, c_vp, C.c_int64, C.c_double, c_vp, c_vp, c_vp, c_vp]),
     ("cx_ctx_create", C.c_int, [C.c_int, C.POINTER(c_vp)]),
     ("cx_ctx_destroy", C.c_int, [c_vp]),
     ("cx_ctx_lane_stream", C.c_int, [c_vp, C.c_int, C.POINTER(c_vp), C.POINTER(C.c_int)]),

@@ -431,6 +431,34 @@ __global__ void __launch_bounds__(DV2_WARPS * 32, 1) decode_v2_kernel(cx_decode_
 }
 
 // ---- KV append: [n_layers][T][d_model] block into [n_layers][cap][d_model] --
+// ---- gate (gate.cpp:27-61): cosine of the main model's hidden state and a side
+// agent's thought, one thread per pair; the three fp64 sums run sequentially in the
+// reference's order with explicit roundings (no FMA contraction), so scores are bitwise.
+__global__ void gate_kernel(const float* __restrict__ h, int64_t hs, const float* __restrict__ t, int64_t ts,
+                            int64_t n, int dim, double theta, double* __restrict__ score,
+                            uint8_t* __restrict__ accepted, uint8_t* __restrict__ degenerate) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* a = h + i * hs;
+    const float* c = t + i * ts;
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (int k = 0; k < dim; ++k) {
+        const double x = (double)__ldg(a + k), y = (double)__ldg(c + k);
+        dot = __dadd_rn(dot, __dmul_rn(x, y));
+        na = __dadd_rn(na, __dmul_rn(x, x));
+        nb = __dadd_rn(nb, __dmul_rn(y, y));
+    }
+    const bool deg = na == 0.0 || nb == 0.0;  // degenerate_input_error: decide() rejects
+    double s = __longlong_as_double(0x7ff8000000000000LL);  // quiet NaN
+    if (!deg) {
+        s = __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb)));
+        s = s < -1.0 ? -1.0 : (1.0 < s ? 1.0 : s);  // std::clamp(s, -1, 1)
+    }
+    score[i] = s;
+    if (accepted) accepted[i] = (!deg && s >= theta) ? 1 : 0;
+    if (degenerate) degenerate[i] = deg ? 1 : 0;
+}
+
 __global__ void kv_append_kernel(float* __restrict__ ck, float* __restrict__ cv, int64_t cap, int dm,
                                  const float* __restrict__ bk, const float* __restrict__ bv, int64_t T,
                                  int64_t dst_row) {
@@ -541,6 +569,13 @@ void kv_append_rows(float* ck, float* cv, int64_t cap, int n_layers, int dm, con
     if (T <= 0) return;
     kv_append_kernel<<<dim3((unsigned)T, (unsigned)n_layers), 128, 0, s>>>(ck, cv, cap, dm, bk, bv, T, dst_row);
     check_launch("kv_append_kernel");
+}
+
+void gate_decide(const float* h, int64_t hs, const float* t, int64_t ts, int64_t n, int dim, double theta,
+                 double* score, uint8_t* accepted, uint8_t* degenerate, cudaStream_t s) {
+    if (n <= 0) return;
+    gate_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(h, hs, t, ts, n, dim, theta, score, accepted, degenerate);
+    check_launch("gate_kernel");
 }
 
 }  // namespace cx

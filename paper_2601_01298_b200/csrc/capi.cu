@@ -439,6 +439,50 @@ extern "C" cx_status cx_attend(const float* q, const float* keys, const float* v
     });
 }
 
+// gate.cpp:27-43 gate_score for one (h_main, t_side) pair, on the device
+extern "C" cx_status cx_gate_score(const float* h_main, const float* t_side, int64_t n, double* out) {
+    return guard([&] {
+        if (n < 1) fail(CX_DEGENERATE_INPUT_ERROR, "gate_score: zero-norm input");  // empty: both norms 0
+        if (!h_main || !t_side || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
+        cx_ctx* c = default_ctx();
+        std::lock_guard<std::mutex> lk(c->mu);
+        ArenaPlan pl;
+        pl.take<float>((size_t)n);
+        pl.take<float>((size_t)n);
+        pl.take<double>(1);
+        pl.take<uint8_t>(1);
+        c->arena.reserve(pl.used);
+        c->arena.reset();
+        float* dh = c->arena.take<float>((size_t)n);
+        float* dt = c->arena.take<float>((size_t)n);
+        double* ds = c->arena.take<double>(1);
+        uint8_t* dd = c->arena.take<uint8_t>(1);
+        h2d(dh, h_main, sizeof(float) * n, c->stream);
+        h2d(dt, t_side, sizeof(float) * n, c->stream);
+        gate_decide(dh, 0, dt, 0, 1, (int)n, 0.0, ds, nullptr, dd, c->stream);
+        uint8_t deg = 0;
+        d2h(out, ds, sizeof(double), c->stream);
+        d2h(&deg, dd, 1, c->stream);
+        CX_CUDA(cudaStreamSynchronize(c->stream));
+        if (deg) fail(CX_DEGENERATE_INPUT_ERROR, "gate_score: zero-norm input");
+    });
+}
+
+// gate.cpp:45-61 decide for n_pairs rows of h / t on the device (the gate fused after an
+// agent step: h = the main model's last hidden states, t = the side agents' thoughts)
+extern "C" cx_status cx_gate_decide_dev(cx_ctx* c, int64_t n_pairs, int dim, const float* h, int64_t h_stride,
+                                        const float* t, int64_t t_stride, double theta, double* scores,
+                                        uint8_t* accepted, uint8_t* degenerate, void* stream) {
+    return guard([&] {
+        if (theta < -1.0 || theta > 1.0) fail(CX_PRECONDITION_ERROR, "decide: theta must be in [-1,1]");
+        if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
+        if (n_pairs < 0 || dim < 0) fail(CX_PRECONDITION_ERROR, "gate: bad shape");
+        if (n_pairs == 0) return;
+        if (!h || !t || !scores) fail(CX_INVALID_ARGUMENT, "null pointer");
+        gate_decide(h, h_stride, t, t_stride, n_pairs, dim, theta, scores, accepted, degenerate, (cudaStream_t)stream);
+    });
+}
+
 // ============================================================================
 // grouped device path
 // ============================================================================

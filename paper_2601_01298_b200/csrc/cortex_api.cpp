@@ -1,10 +1,11 @@
 // cortex_api.cpp -- the C++ cortex:: drop-in shim (include/cortex/*.hpp) over
 // the C-ABI (include/cortex_b200.h).  Code written against the reference's
-// synapse / KvCache / inject / attend API links against libcortex_b200.so
+// synapse / KvCache / inject / attend / gate API links against libcortex_b200.so
 // unchanged; every compute call runs the sm_100a kernels.  cx_status codes are
 // rethrown as the reference's exception types (errors.hpp).
 #include "cortex/config.hpp"
 #include "cortex/errors.hpp"
+#include "cortex/gate.hpp"
 #include "cortex/injector.hpp"
 #include "cortex/kernels.hpp"
 #include "cortex/model.hpp"
@@ -13,6 +14,7 @@
 
 #include <charconv>
 #include <cmath>
+#include <limits>
 #include <sstream>
 #include <unordered_map>
 
@@ -407,6 +409,44 @@ int64_t VirtualPositionPlanner::reserve(int64_t token_count) {
     if (base + token_count > limit_) throw capacity_error("planner: reserved virtual range exhausted");
     taken_ += token_count;
     return base;
+}
+
+// ---- gate.cpp:12-61 -------------------------------------------------------
+std::string GateDecision::csv_header() { return "thought_id,score,theta,accepted"; }
+
+std::string GateDecision::csv_row() const {  // gate.cpp:14-25 (precision 17, "nan" when degenerate)
+    std::ostringstream os;
+    os.precision(17);
+    os << thought_id << ',';
+    if (degenerate)
+        os << "nan";
+    else
+        os << score;
+    os << ',' << threshold << ',' << (accepted ? 1 : 0);
+    return os.str();
+}
+
+double gate_score(std::span<const float> h_main, std::span<const float> t_side) {
+    if (h_main.size() != t_side.size()) throw precondition_error("gate_score: width mismatch");
+    double s = 0.0;
+    ck(cx_gate_score(h_main.data(), t_side.data(), (int64_t)h_main.size(), &s));
+    return s;
+}
+
+GateDecision decide(std::span<const float> h_main, std::span<const float> t_side, double theta, int64_t thought_id) {
+    if (theta < -1.0 || theta > 1.0) throw precondition_error("decide: theta must be in [-1,1]");
+    GateDecision d;
+    d.threshold = theta;
+    d.thought_id = thought_id;
+    try {
+        d.score = gate_score(h_main, t_side);
+        d.accepted = d.score >= theta;
+    } catch (const degenerate_input_error&) {
+        d.score = std::numeric_limits<double>::quiet_NaN();
+        d.degenerate = true;
+        d.accepted = false;
+    }
+    return d;
 }
 
 }  // namespace cortex

@@ -147,6 +147,10 @@ bool select128_launch(const GroupView& g, const double* attn, const double* cen,
                       unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                       cudaStream_t s);
 int select128_wave(int64_t L, int G);
+// gate.cpp:27-61 for n (h, t) pairs (row strides in floats): score (NaN when degenerate),
+// accepted = score >= theta, degenerate = zero norm
+void gate_decide(const float* h, int64_t hs, const float* t, int64_t ts, int64_t n, int dim, double theta,
+                 double* score, uint8_t* accepted, uint8_t* degenerate, cudaStream_t s);
 // groups per selection wave for G groups of L rows (dim 64), 0 if not on chip
 int select64_wave(int64_t L, int G);
 // centroid_of for every group (synapse.cpp:173-181), bit-exact sequential sums

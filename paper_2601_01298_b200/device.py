@@ -214,5 +214,22 @@ def decode_step(syn_keys: torch.Tensor, syn_values: torch.Tensor, tail_keys: tor
     return out
 
 
+def gate_decide(h: torch.Tensor, t: torch.Tensor, theta: float):
+    """gate.cpp:45-61 for every row pair of h / t ([n, dim] float32 CUDA, row-contiguous):
+    -> (scores fp64 [n] (NaN when degenerate), accepted bool [n], degenerate bool [n])."""
+    if h.shape != t.shape or h.dim() != 2 or h.dtype != torch.float32 or t.dtype != torch.float32:
+        raise TypeError("gate_decide: h and t must be float32 [n, dim] of the same shape")
+    if h.stride(1) != 1 or t.stride(1) != 1:
+        raise ValueError("gate_decide: rows must be contiguous")
+    n, dim = h.shape
+    scores = torch.empty(n, dtype=torch.float64, device=h.device)
+    acc = torch.empty(n, dtype=torch.uint8, device=h.device)
+    deg = torch.empty(n, dtype=torch.uint8, device=h.device)
+    check(lib.cx_gate_decide_dev(ctx(h.device.index), n, dim, h.data_ptr(), h.stride(0), t.data_ptr(), t.stride(0),
+                                 float(theta), scores.data_ptr(), acc.data_ptr(), deg.data_ptr(), _stream()),
+          "gate_decide")
+    return scores, acc.bool(), deg.bool()
+
+
 def kernel_launch_count() -> int:
     return int(lib.cx_kernel_launch_count())

@@ -166,3 +166,26 @@ def test_golden_clustered_and_bench_landmarks(orc):
     assert wins / 100 == exp["hybrid_win_rate"]
     assert mh / 100 == exp["mean_pairwise_reduction_hybrid"]
     assert mr / 100 == exp["mean_pairwise_reduction_random"]
+
+
+def test_gate_oracle_bitwise_vs_reference(orc, ref):
+    """gate.cpp:27-43: the C restatement == the unmodified reference, bit for bit, plus
+    the reference's own known answers (test_gate.cpp:33-70)."""
+    r = orc.rng(21)
+    for dim in (1, 3, 64, 128, 1000):
+        for _ in range(20):
+            a, b = r.gaussian_f32(dim), r.gaussian_f32(dim)
+            assert orc.gate_score(a, b) == ref.gate_score(a, b)
+            assert orc.gate_score(a, -a) == ref.gate_score(a, -a)  # clamp side
+    f = np.float32
+    assert abs(orc.gate_score(np.array([0.4, -1.0, 2.0], f), np.array([0.4, -1.0, 2.0], f)) - 1.0) <= 1e-12
+    assert orc.gate_score(np.array([1, 0, 0], f), np.array([0, 2, 0], f)) == 0.0
+    assert abs(orc.gate_score(np.array([1, 2, 2], f), np.array([2, 1, 2], f)) - 8.0 / 9.0) <= 1e-12
+    h, t = np.zeros(8, f), np.zeros(8, f)
+    h[0] = 1.0
+    t[:4] = 1.0
+    assert orc.gate_score(h, t) == 0.5
+    for be in (orc, ref):
+        with pytest.raises(oracle.OracleError) as e:
+            be.gate_score(np.zeros(4, f), np.array([1, 0, 0, 0], f))
+        assert e.value.code == 7  # degenerate_input_error
