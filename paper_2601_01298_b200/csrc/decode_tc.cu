@@ -190,6 +190,31 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* out) {
     for (int j = 0; j < 16; ++j) out[j] = __uint_as_float(v[j]);
 }
 
+// two 16-column loads under ONE wait (the O halves of the epilogue): out = a + b
+__device__ __forceinline__ void tmem_ld16x2_sum(uint32_t ta, uint32_t tb, float* out) {
+    uint32_t a[16], b[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7]), "=r"(a[8]),
+          "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]), "=r"(a[14]), "=r"(a[15])
+        : "r"(ta));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]), "=r"(b[4]), "=r"(b[5]), "=r"(b[6]), "=r"(b[7]), "=r"(b[8]),
+          "=r"(b[9]), "=r"(b[10]), "=r"(b[11]), "=r"(b[12]), "=r"(b[13]), "=r"(b[14]), "=r"(b[15])
+        : "r"(tb));
+    // the wait takes every destination register as an operand: no use can move above it
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                   "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]), "+r"(a[15]),
+                   "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]),
+                   "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]), "+r"(b[14]), "+r"(b[15])
+                 :
+                 : "memory");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) out[j] = __uint_as_float(a[j]) + __uint_as_float(b[j]);
+}
+
 // 8 floats -> one 16-byte core-matrix row chunk of hi and of lo (packed bf16x2 conversions)
 __device__ __forceinline__ void split8_store(const float* x, unsigned char* hi_base, unsigned char* lo_base, uint32_t off) {
     uint32_t hv[4], lv[4];
@@ -643,13 +668,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 float v[TD];
                 const uint32_t trow_o = tO + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
-                for (int c0 = 0; c0 < TD; c0 += 16) {
-                    float w[16];
-                    tmem_ld16(trow_o + (uint32_t)c0, v + c0);
-                    tmem_ld16(trow_o + (uint32_t)(TD + c0), w);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[c0 + j] += w[j];
-                }
+                for (int c0 = 0; c0 < TD; c0 += 16)
+                    tmem_ld16x2_sum(trow_o + (uint32_t)c0, trow_o + (uint32_t)(TD + c0), v + c0);
                 if (live) {  // merged row -> the O_priv row it came from (in place, own row)
                     const float m_p = Mp[tpar * TM + r_own], l_p = Lp[tpar * TM + r_own];
                     const float m = fmaxf(m_s, m_p);
