@@ -324,7 +324,7 @@ void hausdorff_impl(const float* cloud, int64_t count, int dim, const float* lm,
 // mean pairwise distance over a point set (synapse.cpp:306-328)
 double mean_pairwise_impl(cx_ctx* c, const float* d_pts, int64_t count, int dim, const int64_t* d_rows, int64_t n) {
     if (n < 2) return 0.0;
-    double* dsum = c->arena.take<double>((size_t)n + 1);
+    double* dsum = c->arena.take<double>(mean_pairwise_scratch(n, dim));
     mean_pairwise(d_pts, n, dim, d_rows, dsum, c->stream);
     double sum = 0.0;
     d2h(&sum, dsum, sizeof(double), c->stream);
@@ -366,7 +366,7 @@ extern "C" cx_status cx_mean_pairwise_reduction(const float* cloud, int64_t coun
         ArenaPlan pl;
         pl.take<float>((size_t)count * dim);
         pl.take<float>((size_t)m * ldim);
-        pl.take<double>((size_t)std::max(count, m) + 1);
+        pl.take<double>(std::max(mean_pairwise_scratch(count, dim), mean_pairwise_scratch(m, ldim)));
         c->arena.reserve(pl.used);
         c->arena.reset();
         float* dc = c->arena.take<float>((size_t)count * dim);
@@ -393,7 +393,7 @@ extern "C" cx_status cx_mean_pairwise_reduction_subset(const float* cloud, int64
         ArenaPlan pl;
         pl.take<float>((size_t)count * dim);
         pl.take<int64_t>((size_t)n_rows);
-        pl.take<double>((size_t)std::max(count, n_rows) + 1);
+        pl.take<double>(std::max(mean_pairwise_scratch(count, dim), mean_pairwise_scratch(n_rows, dim)));
         c->arena.reserve(pl.used);
         c->arena.reset();
         float* dc = c->arena.take<float>((size_t)count * dim);

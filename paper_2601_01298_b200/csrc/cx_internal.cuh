@@ -174,6 +174,8 @@ void coverage_centroid(cx_ctx* ctx, const GroupView& g, double* out, cudaStream_
 // metrics (one cloud): sq-dist min/max reduction and pairwise means.
 void hausdorff(const float* cloud, int64_t count, int dim, const float* lm, int64_t m,
                const int64_t* rows, double* out_worst_sq, cudaStream_t s);
+// doubles of scratch mean_pairwise needs at out_sum (the sum, then its working space)
+size_t mean_pairwise_scratch(int64_t count, int dim);
 void mean_pairwise(const float* pts, int64_t count, int dim, const int64_t* rows, double* out_sum,
                    cudaStream_t s);
 

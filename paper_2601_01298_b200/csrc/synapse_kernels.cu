@@ -641,6 +641,59 @@ __global__ void mean_pairwise_kernel(const float* __restrict__ pts, int64_t coun
     if (threadIdx.x == 0) partial[i] = acc;
 }
 
+// Tiled form: the points are converted to fp64 once (rows gathered), then each CTA takes a
+// 32 x 32 tile of the upper triangle (bi <= bj) with both tiles' rows staged in shared
+// memory; every pair's squared distance is still the sequential fp64 sum of the reference
+// (coordinates in order), only the sum over pairs is reordered (1e-12 relative).
+constexpr int MP_T = 32;
+constexpr int MP_MAXDIM = 256;
+__global__ void to_f64_kernel(const float* __restrict__ pts, int64_t n, int dim, const int64_t* __restrict__ rows,
+                              double* __restrict__ out) {
+    const int64_t tot = n * dim;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / dim, c = e % dim;
+        out[e] = (double)pts[(rows ? rows[i] : i) * dim + c];
+    }
+}
+__global__ void __launch_bounds__(256) mean_pairwise_tile_kernel(const double* __restrict__ p64, int64_t n, int dim,
+                                                                 double* __restrict__ partial) {
+    extern __shared__ double mp_sm[];  // [2][MP_T][dim + 1]
+    __shared__ double red[32];
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    const int64_t slot = (int64_t)bi * gridDim.x + bj;
+    if (bj < bi) {  // lower triangle: nothing (uniform per CTA)
+        if (threadIdx.x == 0) partial[slot] = 0.0;
+        return;
+    }
+    const int pitch = dim + 1;
+    double* si = mp_sm;
+    double* sj = mp_sm + MP_T * pitch;
+    const int64_t i0 = (int64_t)bi * MP_T, j0 = (int64_t)bj * MP_T;
+    for (int e = threadIdx.x; e < MP_T * dim; e += blockDim.x) {
+        const int r = e / dim, c = e % dim;
+        si[r * pitch + c] = i0 + r < n ? p64[(i0 + r) * dim + c] : 0.0;
+        sj[r * pitch + c] = j0 + r < n ? p64[(j0 + r) * dim + c] : 0.0;
+    }
+    __syncthreads();
+    const int ti = threadIdx.x & 31, tw = threadIdx.x >> 5;  // lane -> i row, warp -> j rows tw + 8u
+    double acc = 0.0;
+    for (int u = 0; u < MP_T / 8; ++u) {
+        const int tj = tw + 8 * u;
+        if (i0 + ti < n && j0 + tj < n && (bi < bj || tj > ti)) {
+            const double* a = si + ti * pitch;
+            const double* b = sj + tj * pitch;  // warp-uniform row: broadcast reads
+            double d2 = 0.0;
+            for (int c = 0; c < dim; ++c) {
+                const double d = __dsub_rn(a[c], b[c]);
+                d2 = __dadd_rn(d2, __dmul_rn(d, d));
+            }
+            acc = __dadd_rn(acc, __dsqrt_rn(d2));
+        }
+    }
+    acc = block_reduce(acc, [](double x, double y) { return __dadd_rn(x, y); }, 0.0, red);
+    if (threadIdx.x == 0) partial[slot] = acc;
+}
+
 __global__ void sum_partials_kernel(const double* __restrict__ partial, int64_t n, double* __restrict__ out) {
     __shared__ double red[32];
     double acc = 0.0;
@@ -818,13 +871,34 @@ void hausdorff(const float* cloud, int64_t count, int dim, const float* lm, int6
     check_launch("hausdorff_kernel");
 }
 
+size_t mean_pairwise_scratch(int64_t count, int dim) {
+    if (dim > MP_MAXDIM) return (size_t)count + 1;
+    const int64_t nt = (count + MP_T - 1) / MP_T;
+    return 1 + (size_t)count * dim + (size_t)(nt * nt);
+}
+
 void mean_pairwise(const float* pts, int64_t count, int dim, const int64_t* rows, double* out_sum,
                    cudaStream_t s) {
-    // partial sums live right after out_sum (caller allocates count + 1 doubles)
-    double* partial = out_sum + 1;
-    mean_pairwise_kernel<<<(unsigned)count, 256, 0, s>>>(pts, count, dim, rows, partial);
-    check_launch("mean_pairwise_kernel");
-    sum_partials_kernel<<<1, 1024, 0, s>>>(partial, count, out_sum);
+    // scratch right after out_sum: mean_pairwise_scratch(count, dim) - 1 doubles
+    if (dim > MP_MAXDIM) {  // wide rows: a CTA per row i (partial sums per row)
+        double* partial = out_sum + 1;
+        mean_pairwise_kernel<<<(unsigned)count, 256, 0, s>>>(pts, count, dim, rows, partial);
+        check_launch("mean_pairwise_kernel");
+        sum_partials_kernel<<<1, 1024, 0, s>>>(partial, count, out_sum);
+        check_launch("sum_partials_kernel");
+        return;
+    }
+    double* p64 = out_sum + 1;
+    double* partial = p64 + (size_t)count * dim;
+    const int64_t nt = (count + MP_T - 1) / MP_T;
+    to_f64_kernel<<<(unsigned)std::min<int64_t>((count * dim + 255) / 256, 4096), 256, 0, s>>>(pts, count, dim, rows, p64);
+    check_launch("to_f64_kernel");
+    const size_t smem = sizeof(double) * 2 * MP_T * (size_t)(dim + 1);
+    if (smem > 48 * 1024)
+        CX_CUDA(cudaFuncSetAttribute(mean_pairwise_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    mean_pairwise_tile_kernel<<<dim3((unsigned)nt, (unsigned)nt), 256, smem, s>>>(p64, count, dim, partial);
+    check_launch("mean_pairwise_tile_kernel");
+    sum_partials_kernel<<<1, 1024, 0, s>>>(partial, nt * nt, out_sum);
     check_launch("sum_partials_kernel");
 }
 
