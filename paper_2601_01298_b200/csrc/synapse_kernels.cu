@@ -629,6 +629,49 @@ __global__ void hausdorff_kernel(const float* __restrict__ cloud, int64_t count,
     if ((threadIdx.x & 31) == 0) atomicMax(worst_bits, (unsigned long long)__double_as_longlong(best));
 }
 
+// Tiled form (dim <= 128): a CTA stages its 128 cloud rows and then 32-landmark tiles as
+// fp64 in shared memory (converted once), so a pair costs shared-memory reads and the
+// sequential fp64 sum only; min / max are order-free, so the result stays bitwise.
+constexpr int HD_ROWS = 128, HD_T = 32, HD_MAXDIM = 128;
+__global__ void __launch_bounds__(HD_ROWS) hausdorff_tile_kernel(const float* __restrict__ cloud, int64_t count, int dim,
+                                                                 const float* __restrict__ lm, int64_t m,
+                                                                 const int64_t* __restrict__ rows,
+                                                                 unsigned long long* __restrict__ worst_bits) {
+    extern __shared__ double hd_sm[];
+    const int pitch = dim + 1;
+    double* sx = hd_sm;                      // [HD_ROWS][pitch]
+    double* sl = hd_sm + HD_ROWS * pitch;    // [HD_T][pitch]
+    const int64_t r0 = (int64_t)blockIdx.x * HD_ROWS;
+    for (int e = threadIdx.x; e < HD_ROWS * dim; e += HD_ROWS) {
+        const int r = e / dim, c = e % dim;
+        sx[r * pitch + c] = r0 + r < count ? (double)cloud[(r0 + r) * dim + c] : 0.0;
+    }
+    const double* x = sx + threadIdx.x * pitch;
+    double best = INFINITY;
+    for (int64_t j0 = 0; j0 < m; j0 += HD_T) {
+        __syncthreads();  // previous tile consumed (and the cloud rows staged)
+        for (int e = threadIdx.x; e < HD_T * dim; e += HD_ROWS) {
+            const int r = e / dim, c = e % dim;
+            const int64_t j = j0 + r;
+            sl[r * pitch + c] = j < m ? (double)(rows ? cloud[rows[j] * dim + c] : lm[j * dim + c]) : 0.0;
+        }
+        __syncthreads();
+        const int nt = (int)min((int64_t)HD_T, m - j0);
+        for (int jj = 0; jj < nt; ++jj) {
+            const double* y = sl + jj * pitch;  // broadcast
+            double acc = 0.0;
+            for (int c = 0; c < dim; ++c) {
+                const double d = __dsub_rn(x[c], y[c]);
+                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            }
+            best = dmin_std(best, acc);
+        }
+    }
+    if (r0 + threadIdx.x >= count) best = 0.0;
+    best = warp_reduce(best, [](double a, double b) { return dmax_std(a, b); });
+    if ((threadIdx.x & 31) == 0) atomicMax(worst_bits, (unsigned long long)__double_as_longlong(best));
+}
+
 __global__ void mean_pairwise_kernel(const float* __restrict__ pts, int64_t count, int dim,
                                      const int64_t* __restrict__ rows, double* __restrict__ partial) {
     __shared__ double red[32];
@@ -866,6 +909,15 @@ void coverage_centroid(cx_ctx* ctx, const GroupView& g, double* out, cudaStream_
 void hausdorff(const float* cloud, int64_t count, int dim, const float* lm, int64_t m, const int64_t* rows,
                double* out_worst_sq, cudaStream_t s) {
     CX_CUDA(cudaMemsetAsync(out_worst_sq, 0, sizeof(double), s));
+    if (dim <= HD_MAXDIM) {
+        const size_t smem = sizeof(double) * (size_t)(HD_ROWS + HD_T) * (size_t)(dim + 1);
+        if (smem > 48 * 1024)
+            CX_CUDA(cudaFuncSetAttribute(hausdorff_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        hausdorff_tile_kernel<<<(unsigned)((count + HD_ROWS - 1) / HD_ROWS), HD_ROWS, smem, s>>>(
+            cloud, count, dim, lm, m, rows, reinterpret_cast<unsigned long long*>(out_worst_sq));
+        check_launch("hausdorff_tile_kernel");
+        return;
+    }
     hausdorff_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(
         cloud, count, dim, lm, m, rows, reinterpret_cast<unsigned long long*>(out_worst_sq));
     check_launch("hausdorff_kernel");

@@ -223,6 +223,21 @@ def test_sketch_rows_fp16_overflow(dev, orc, monkeypatch, force):
     assert scores.cpu().numpy()[0].tobytes() == sc.tobytes()
 
 
+@pytest.mark.parametrize("L,d,m", [(3000, 64, 50), (1200, 128, 70), (700, 200, 33)])
+def test_metrics_at_scale(cx, orc, L, d, m):
+    """A7 metrics on cfg-sized clouds through the tiled kernels (d <= 128) and the
+    fallbacks (d = 200): Hausdorff bitwise, mean-pairwise reduction within 1e-12."""
+    r = orc.rng(40 + d)
+    cloud = r.gaussian_f32(L * d).reshape(L, d)
+    rows = np.sort(orc.random_subset(r, L, m))
+    lms = np.ascontiguousarray(cloud[rows])
+    assert cx.hausdorff_to_subset(cloud, rows) == orc.hausdorff_to_subset(cloud, rows)
+    assert cx.hausdorff_distance(cloud, lms) == orc.hausdorff_distance(cloud, lms)
+    for got, exp in [(cx.mean_pairwise_reduction_subset(cloud, rows), orc.mean_pairwise_reduction_subset(cloud, rows)),
+                     (cx.mean_pairwise_reduction(cloud, lms), orc.mean_pairwise_reduction(cloud, lms))]:
+        assert abs(got - exp) <= 1e-12 * max(1.0, abs(exp)), (got, exp)
+
+
 def test_full_cfg2_properties(dev):
     """All 48 (layer, KV-head) groups at L=8192, k=164: size-independent
     properties (sorted unique rows in range, gather == source rows)."""
