@@ -904,9 +904,17 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
         CX_CUDA(cudaMalloc(&trc, 2048 * sizeof(unsigned long long)));
         CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
     }
+    const int skip = getenv("CX_TC_SKIP") ? atoi(getenv("CX_TC_SKIP")) : 0;
+    if (skip) {  // timing experiments only: say so once, loudly
+        static bool warned = false;
+        if (!warned) {
+            fprintf(stderr, "cortex_b200: CX_TC_SKIP=%d is set -- decode outputs are NOT valid (timing experiments only)\n",
+                    skip);
+            warned = true;
+        }
+    }
     kern<<<dim3((unsigned)n_lh, (unsigned)per_lh), TTHREADS, smem, s>>>(b, (float)(1.0 / std::sqrt((double)b.d_k)),
-                                                                             tracing ? trc : nullptr,
-                                                                             getenv("CX_TC_SKIP") ? atoi(getenv("CX_TC_SKIP")) : 0);
+                                                                             tracing ? trc : nullptr, skip);
     check_launch("decode_tc_kernel");
     if (tracing) {  // debugging only: per-tile phase times of CTA (0, 0), us since the staging ended
         std::vector<unsigned long long> h(2048);
