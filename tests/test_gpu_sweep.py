@@ -1,8 +1,10 @@
-"""Randomised parity sweep of the grouped compression (attention mass -> greedy
-selection -> landmark K/V gather) against the oracle, per group: seeded random
-group counts, lengths, k, lambda and widths (64: select64, 128: select128, 48 / 96:
-the generic kernel), with clustered and duplicated rows mixed in.  Rows, scores and
-gathered K/V bit-exact."""
+"""Randomised parity sweeps against the oracle:
+* the grouped compression (attention mass -> greedy selection -> landmark K/V
+  gather) per group, with seeded random group counts, lengths, k, lambda and widths
+  (64: select64, 128: select128, 48 / 96: the generic kernel), clustered and
+  duplicated rows, and forced small-cluster row modes -- rows, scores and K/V bit-exact;
+* the batched decode on random shapes (ragged tails, q-heads per KV head, append on /
+  off) -- within 1e-3, the appended rows bitwise."""
 import numpy as np
 import pytest
 
@@ -98,3 +100,55 @@ def test_grouped_compress_forced_row_modes(dev, orc, monkeypatch, seed):
         assert rows[gi].tobytes() == idx.tobytes(), (seed, gi, d, C, L, k)
         assert scores[gi].tobytes() == sc.tobytes(), (seed, gi)
         assert np.array_equal(sk[gi], ks[gi][idx])
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_decode_random_sweep(dev, orc, seed):
+    """Batched decode (default dispatch: tcgen05 -> v2 -> v1) on seeded random shapes:
+    agents, synapse size, tail capacity, ragged per-agent tail lengths, q-heads per KV
+    head, layers, KV heads, with and without the fused append; every (agent, layer,
+    q-head) output within 1e-3 (unit floor) of the oracle's attend over
+    [synapse rows || private rows || new row], and the appended row bitwise."""
+    import torch
+    rs = np.random.default_rng(900 + seed)
+    N = int(rs.integers(1, 40))
+    Lr = int(rs.integers(1, 3))
+    H = int(rs.integers(1, 3))
+    qpg = int(rs.choice([1, 2, 4, 7, 8]))
+    Q = H * qpg
+    dk = 64
+    k = int(rs.integers(1, 177))
+    Tc = int(rs.integers(1, 65))
+    app = bool(rs.random() < 0.8)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    syn_k = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
+    syn_v = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)
+    tk = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
+    tv = torch.randn(N, Lr, H, Tc, dk, device="cuda", generator=gen)
+    hi = Tc - 1 if app else Tc
+    tl = torch.randint(0, hi + 1, (N,), device="cuda", generator=gen).to(torch.int32)
+    nk = torch.randn(N, Lr, H, dk, device="cuda", generator=gen) if app else None
+    nv = torch.randn(N, Lr, H, dk, device="cuda", generator=gen) if app else None
+    q = torch.randn(N, Lr, Q, dk, device="cuda", generator=gen)
+    out = torch.empty_like(q)
+    dev.decode_step(syn_k, syn_v, tk, tv, tl, q, out, nk, nv)
+    torch.cuda.synchronize()
+    o, tkn, tvn, tln = out.cpu().numpy(), tk.cpu().numpy(), tv.cpu().numpy(), tl.cpu().numpy()
+    sk, sv, qn = syn_k.cpu().numpy(), syn_v.cpu().numpy(), q.cpu().numpy()
+    nkn = nk.cpu().numpy() if app else None
+    nvn = nv.cpu().numpy() if app else None
+    worst = 0.0
+    for a in range(N):
+        n_t = int(tln[a]) + (1 if app else 0)
+        for l in range(Lr):
+            for g in range(H):
+                if app:  # the fused append wrote row tail_len
+                    assert np.array_equal(tkn[a, l, g, tln[a]], nkn[a, l, g])
+                    assert np.array_equal(tvn[a, l, g, tln[a]], nvn[a, l, g])
+                kk = np.concatenate([sk[l, g], tkn[a, l, g, :n_t]])
+                vv = np.concatenate([sv[l, g], tvn[a, l, g, :n_t]])
+                for hh in range(qpg):
+                    h = g * qpg + hh
+                    exp = orc.attend(qn[a, l, h], kk, vv, k + n_t, 1, dk)
+                    worst = max(worst, float(np.max(np.abs(o[a, l, h] - exp) / np.maximum(1.0, np.abs(exp)))))
+    assert worst <= 1e-3, (seed, worst, N, k, Tc, qpg)
