@@ -892,7 +892,8 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int n_tiles = (b.n_agents + at - 1) / at;
     const int sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
     // one resident CTA per SM: fill the SMs in a single wave
-    const int per_lh = std::max(1, std::min(n_tiles, sms / n_lh));
+    int per_lh = std::max(1, std::min(n_tiles, sms / n_lh));
+    if (const char* f = getenv("CX_TC_PER_LH")) per_lh = std::max(1, std::min(n_tiles, atoi(f)));  // tuning only
     // debugging only (CX_TC_SMEM_PAD=bytes): reserve extra shared memory, i.e. shrink the L1
     // carveout, to measure how the private-row stream depends on L1 capacity
     const size_t smem = lay.total + (getenv("CX_TC_SMEM_PAD") ? (size_t)atol(getenv("CX_TC_SMEM_PAD")) : 0);
