@@ -1,0 +1,24 @@
+"""Decode step time vs agent count (tools only): N up to 10,000 agents, T=32, cfg2 shape."""
+import os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_01298_b200 import device as cxd
+torch.cuda.set_device(0)
+g = torch.Generator(device="cuda").manual_seed(0)
+for N in [int(x) for x in (sys.argv[1:] or ["2000", "4000", "10000"])]:
+    sk = torch.randn(24, 2, 164, 64, device="cuda", generator=g); sv = torch.randn_like(sk)
+    tk = torch.randn(N, 24, 2, 33, 64, device="cuda", generator=g); tv = torch.randn_like(tk)
+    tl = torch.full((N,), 32, dtype=torch.int32, device="cuda")
+    nk = torch.randn(N, 24, 2, 64, device="cuda", generator=g); nv = torch.randn_like(nk)
+    q = torch.randn(N, 24, 14, 64, device="cuda", generator=g); o = torch.empty_like(q)
+    for _ in range(3): cxd.decode_step(sk, sv, tk, tv, tl, q, o, nk, nv)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(10): cxd.decode_step(sk, sv, tk, tv, tl, q, o, nk, nv)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    B = 24 * 2 * 164 * 64 * 4 * 2 + N * (24576 * 33 + 172032)
+    print(f"N={N}: {ms*1000:.1f} us/step  {N/ms*1000/1e6:.2f} M agent-steps/s  {B/ms/1e6:.0f} GB/s ({B/ms/1e6/6552.3*100:.1f}% of HBM)", flush=True)
+    del tk, tv, q, o, nk, nv
+    torch.cuda.empty_cache()
