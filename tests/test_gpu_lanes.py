@@ -112,14 +112,15 @@ def test_compress_through_kvcache_view_and_lanes(cx):
         assert torch.equal(sk, res[h][2]) and torch.equal(sv, res[h][3])
 
 
-@pytest.mark.parametrize("G,pinned", [(13, True), (3, False)])
-def test_compress_grouped_host_matches_device(cx, G, pinned):
+@pytest.mark.parametrize("G,pinned,L,k", [(13, True, 1500, 60), (3, False, 1500, 60), (1, True, 700, 30),
+                                         (5, True, 40, 64)])
+def test_compress_grouped_host_matches_device(cx, G, pinned, L, k):
     """cx_compress_grouped_host (chunked uploads overlapping the per-chunk
     compressions) == cx_compress_grouped_dev on the same data, bit for bit,
     including a ragged last chunk and pageable host memory."""
     import torch
     from paper_2601_01298_b200 import device
-    L, d, P, k = 1500, 64, 7, 60
+    d, P = 64, 7  # (5, 40, 64): k > L, every row taken (take = min(k, L))
     gen = torch.Generator().manual_seed(21 + G)
     hk = torch.randn(G, L, d, generator=gen)
     hv = torch.randn(G, L, d, generator=gen)
