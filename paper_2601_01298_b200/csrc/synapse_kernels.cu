@@ -169,7 +169,7 @@ __global__ void centroid_kernel(GroupView gv, double* __restrict__ cen) {
 // Same sum with the loads off the critical path: one warp per 32 coordinates
 // of one group; rows stream through an 8-stage cp.async ring (32 rows x 128 B
 // per stage) so the only serial cost is the fp64 add chain (L x 8.4 cycles).
-constexpr int kCpStages = 8;
+constexpr int kCpStages = 12;  // 12 x 32 rows x 128 B = 48 KB static: ~2 us of loads in flight per warp
 constexpr int kCpRows = 32;
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
