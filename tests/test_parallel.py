@@ -65,3 +65,56 @@ def test_all_gather_synapse_world2(n_groups):
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(0, True), (1, True)]
+
+
+def _select_worker(rank, world, port, n_groups, q):
+    """Each rank runs the whole greedy selection for its own groups (no
+    collective inside selection), then the one all-gather exchange builds the
+    full synapse: rows, scores and landmark K/V of every group."""
+    import numpy as np
+
+    import oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = oracle.load()
+        b, e = shard_range(n_groups, rank, world)
+        L, d, k, lam = 192, 16, 12, 0.5
+        rows, scores, sk, sv = [], [], [], []
+        for gi in range(b, e):
+            keys, values, queries = oracle.synthetic_group(orc, 100 + gi, L, d, 3)
+            idx, sc = orc.select_landmarks_points(keys, oracle.group_attention(orc, keys, queries), k, lam)
+            rows.append(idx), scores.append(sc), sk.append(keys[idx]), sv.append(values[idx])
+        loc = [torch.from_numpy(np.stack(x)) if x else torch.empty((0,) + s)
+               for x, s in ((rows, (k,)), (scores, (k,)), (sk, (k, d)), (sv, (k, d)))]
+        loc[0] = loc[0].to(torch.int64)
+        loc[1] = loc[1].to(torch.float64)
+        full = all_gather_groups(loc, n_groups)
+        ok = True
+        for gi in range(n_groups):  # every rank checks every group against a local recompute
+            keys, values, queries = oracle.synthetic_group(orc, 100 + gi, L, d, 3)
+            idx, sc = orc.select_landmarks_points(keys, oracle.group_attention(orc, keys, queries), k, lam)
+            ok &= (np.array_equal(full[0][gi].numpy(), idx) and full[1][gi].numpy().tobytes() == sc.tobytes()
+                   and np.array_equal(full[2][gi].numpy(), keys[idx])
+                   and np.array_equal(full[3][gi].numpy(), values[idx]))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_groups", [(2, 5), (3, 7)])
+def test_sharded_selection_gathers_the_single_rank_synapse(world, n_groups):
+    """groups sharded over ranks, one all-gather -> every rank
+    holds the synapse a single rank computes, bit for bit (uneven shards)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_select_worker, args=(r, world, port, n_groups, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(r, True) for r in range(world)]
