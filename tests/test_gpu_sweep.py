@@ -152,3 +152,31 @@ def test_decode_random_sweep(dev, orc, seed):
                     exp = orc.attend(qn[a, l, h], kk, vv, k + n_t, 1, dk)
                     worst = max(worst, float(np.max(np.abs(o[a, l, h] - exp) / np.maximum(1.0, np.abs(exp)))))
     assert worst <= 1e-3, (seed, worst, N, k, Tc, qpg)
+
+
+@pytest.mark.parametrize("N,lo,hi", [(100, 13, 37), (100, 0, 50), (64, 63, 64)])
+def test_decode_agent_shard_is_bitwise(dev, N, lo, hi):
+    """SURVEY.md §8(e) agent sharding: a rank decodes a contiguous block of
+    agents on its own; every agent's output and appended rows must equal, bit
+    for bit, the same agent's result inside the full batch (tile membership,
+    grid shape and CTA count differ between the two launches)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(N + lo)
+    Lr, H, Q, dk, T, k = 3, 2, 14, 64, 33, 164
+    syn_k = torch.randn(Lr, H, k, dk, device="cuda", generator=g)
+    syn_v = torch.randn(Lr, H, k, dk, device="cuda", generator=g)
+    tk = torch.randn(N, Lr, H, T, dk, device="cuda", generator=g)
+    tv = torch.randn(N, Lr, H, T, dk, device="cuda", generator=g)
+    tl = torch.randint(0, T, (N,), dtype=torch.int32, device="cuda", generator=g)
+    nk = torch.randn(N, Lr, H, dk, device="cuda", generator=g)
+    nv = torch.randn(N, Lr, H, dk, device="cuda", generator=g)
+    q = torch.randn(N, Lr, Q, dk, device="cuda", generator=g)
+    tk_s, tv_s = tk[lo:hi].clone(), tv[lo:hi].clone()
+    out = torch.empty_like(q)
+    dev.decode_step(syn_k, syn_v, tk, tv, tl, q, out, nk, nv)
+    out_s = torch.empty_like(q[lo:hi])
+    dev.decode_step(syn_k, syn_v, tk_s, tv_s, tl[lo:hi].contiguous(), q[lo:hi].contiguous(), out_s,
+                    nk[lo:hi].contiguous(), nv[lo:hi].contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(out[lo:hi], out_s)
+    assert torch.equal(tk[lo:hi], tk_s) and torch.equal(tv[lo:hi], tv_s)
