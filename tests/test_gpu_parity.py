@@ -589,3 +589,27 @@ def test_grouped_compress_edge_shapes(dev, orc, G, L, k, lam, flags):
         idx, _ = orc.select_landmarks_points(ks[gi], a, k, lam)
         assert np.array_equal(rows[gi], idx), (gi, rows[gi][:8], idx[:8])
         assert np.array_equal(sk[gi], ks[gi][idx]) and np.array_equal(sv[gi], vs[gi][idx])
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_group_shards_match_the_full_cfg2_compression(dev, world):
+    """SURVEY.md §8(e) group sharding at cfg2 size: each rank's block of the 48
+    groups compressed alone (6 groups at 8 ranks: C=16 register rows; 24 at 2:
+    the sketch-row waves) reproduces the full 48-group launch bit for bit --
+    rows, scores and landmark K/V -- although the cluster size, wave split and
+    row mode all differ."""
+    import torch
+
+    from paper_2601_01298_b200.parallel import shard_range
+    G, L, d, nq, k = 48, 8192, 64, 7, 164
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    kt = torch.randn(G, L, d, device="cuda", generator=gen)
+    vt = torch.randn(G, L, d, device="cuda", generator=gen)
+    qt = torch.randn(G, nq, d, device="cuda", generator=gen)
+    full = dev.compress_grouped(kt, vt, qt, k, 0.5)
+    for r in range(world):
+        b, e = shard_range(G, r, world)
+        part = dev.compress_grouped(kt[b:e].contiguous(), vt[b:e].contiguous(), qt[b:e].contiguous(), k, 0.5)
+        torch.cuda.synchronize()
+        for x, y in zip(full, part):
+            assert torch.equal(x[b:e], y), f"rank {r} of {world}: groups {b}..{e} differ"
