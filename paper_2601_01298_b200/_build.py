@@ -55,19 +55,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for src in _sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
         if src.endswith(".cu"):
-            cmd += ["-Xptxas", "-v"] if verbose else []
+            cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else [])
         else:
-            cmd = [NVCC, "-x", "cu"] + NVCC_FLAGS + ["-c", src, "-o", obj] if False else \
-                  ["g++", "-std=c++20", "-O3", "-fPIC", "-I" + INCLUDE, "-I/usr/local/cuda/include", "-c", src, "-o", obj]
+            cmd = ["g++", "-std=c++20", "-O3", "-fPIC", "-I" + INCLUDE, "-I/usr/local/cuda/include", "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
         objs.append(obj)
+    # translation units compile independently: one nvcc per source, in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs + ["-lcudart_static", "-lpthread", "-ldl", "-lrt"]
     subprocess.run(cmd, check=True)
