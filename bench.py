@@ -447,7 +447,7 @@ def run_cfg5(args, dev, tokens=600, n_agents=100, inj_every=10, push_every=10, t
 
     River lane (highest priority): every `inj_every` agent tokens, inject a
     16-token thought block into the river's device KvCache (cx_inject_dev,
-    injector.cpp:136-160); every `push_every` tokens, if the previous push has
+    injector.cpp:70-94); every `push_every` tokens, if the previous push has
     landed, re-compress the river's L=8192 context rows (48 (layer, KV-head)
     groups, k=164) into the back synapse buffer -- the push (scheduler.cpp:
     158-165).  Stream lane (medium priority): N agents x 24 layers decode one

@@ -117,7 +117,7 @@ cx_status cx_ctx_lane_stream(cx_ctx* ctx, int lane, void** stream, int* priority
  * queries[(g * n_pass + p) * d_k + c].  Pass p scores columns
  * [p * col_step, p * col_step + d_k) -- col_step = d_k reproduces the
  * reference's head-concatenated MHA cloud (attention_scores_points with
- * n_heads = n_pass, synapse.cpp:200-230); col_step = 0 is the GQA group mode
+ * n_heads = n_pass, synapse.cpp:63-93); col_step = 0 is the GQA group mode
  * (sum over the group's q-heads of attention_scores_points(cloud, q_h, 1)). */
 typedef struct cx_groups {
     int n_groups;
@@ -135,7 +135,7 @@ typedef struct cx_groups {
 /* attention mass per row for every group: out[G][count] (device, fp64). */
 cx_status cx_attention_grouped_dev(cx_ctx* ctx, const cx_groups* g, double* out, void* stream);
 
-/* Greedy hybrid selection (synapse.cpp:353-421) for every group given its
+/* Greedy hybrid selection (synapse.cpp:216-284) for every group given its
  * attention [G][count] (device).  Outputs (device): rows [G][take] ascending,
  * scores [G][take], take = min(k, count).  flags: CX_SELECT_* below. */
 #define CX_SELECT_EXACT_ONLY 1u /* disable the conservative fp32 distance filter */
@@ -144,7 +144,7 @@ cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* a
                                 int k, double lambda, unsigned flags,
                                 int64_t* out_rows, double* out_scores, void* stream);
 
-/* Landmark gather (synapse.cpp:440-455 copy, per group): dst[g][s][:] =
+/* Landmark gather (synapse.cpp:303-318 copy, per group): dst[g][s][:] =
  * src row rows[g][s] of group g (same addressing as g->clouds, base `src`). */
 cx_status cx_gather_grouped_dev(cx_ctx* ctx, const cx_groups* g, const float* src,
                                 const int64_t* rows, int take, float* dst, void* stream);

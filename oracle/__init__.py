@@ -294,7 +294,7 @@ def load_ref():
 
 def group_attention(backend: Backend, cloud, queries) -> np.ndarray:
     """SURVEY.md §8(d) per-(layer, KV-head) attention: sum, in q-head order, of
-    attention_scores_points(cloud, q_h, 1) (composition of synapse.cpp:200-230)."""
+    attention_scores_points(cloud, q_h, 1) (composition of synapse.cpp:63-93)."""
     total = np.zeros(np.asarray(cloud).shape[0], dtype=np.float64)
     for q in np.asarray(queries, dtype=np.float32).reshape(-1, np.asarray(cloud).shape[1]):
         total = total + backend.attention_scores_points(cloud, q, 1)

@@ -61,7 +61,7 @@ void orc_rng_fill_gaussian_f32(orc_rng* r, float* dst, int64_t n, double mean, d
 static inline double std_min(double a, double b) { return (b < a) ? b : a; }
 static inline double std_max(double a, double b) { return (a < b) ? b : a; }
 
-/* synapse.cpp:155-162: sq_dist(span<float>, span<float>) */
+/* synapse.cpp:18-25: sq_dist(span<float>, span<float>) */
 static double sq_dist_ff(const float* a, const float* b, int n) {
     double acc = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -71,7 +71,7 @@ static double sq_dist_ff(const float* a, const float* b, int n) {
     return acc;
 }
 
-/* synapse.cpp:164-171: sq_dist(span<float>, vector<double>) */
+/* synapse.cpp:27-34: sq_dist(span<float>, vector<double>) */
 static double sq_dist_fd(const float* a, const double* b, int n) {
     double acc = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -81,7 +81,7 @@ static double sq_dist_fd(const float* a, const double* b, int n) {
     return acc;
 }
 
-/* ---- kernels.cpp:110-125 ------------------------------------------------ */
+/* ---- kernels.cpp:66-81 ------------------------------------------------ */
 
 int orc_softmax(const double* scores, int64_t n, double* out) {
     if (n <= 0) return ORC_PRECONDITION_ERROR; /* "softmax: empty input" */
@@ -99,14 +99,14 @@ int orc_softmax(const double* scores, int64_t n, double* out) {
     return ORC_OK;
 }
 
-/* ---- synapse.cpp:200-230 ------------------------------------------------ */
+/* ---- synapse.cpp:63-93 ------------------------------------------------ */
 
 int orc_attention_scores_points(const float* keys, int64_t count, int dim,
                                 const float* query, int64_t query_len, int n_heads,
                                 double* out) {
-    if (count == 0) return ORC_PRECONDITION_ERROR;            /* :203 */
-    if (query_len != (int64_t)dim) return ORC_PRECONDITION_ERROR; /* :204-205 */
-    if (n_heads < 1 || dim % n_heads != 0) return ORC_PRECONDITION_ERROR; /* :206-207 */
+    if (count == 0) return ORC_PRECONDITION_ERROR;            /* :66 */
+    if (query_len != (int64_t)dim) return ORC_PRECONDITION_ERROR; /* :67-68 */
+    if (n_heads < 1 || dim % n_heads != 0) return ORC_PRECONDITION_ERROR; /* :69-70 */
     const int d_k = dim / n_heads;
     const double inv_sqrt_dk = 1.0 / sqrt((double)d_k);
     double* scores = (double*)malloc(sizeof(double) * (size_t)count);
@@ -130,7 +130,7 @@ int orc_attention_scores_points(const float* keys, int64_t count, int dim,
     return st;
 }
 
-/* ---- synapse.cpp:173-181, 240-257 --------------------------------------- */
+/* ---- synapse.cpp:36-44, 103-120 --------------------------------------- */
 
 void orc_centroid(const float* cloud, int64_t count, int dim, double* c) {
     for (int j = 0; j < dim; ++j) c[j] = 0.0;
@@ -163,7 +163,7 @@ int orc_coverage_scores_points(const float* cloud, int64_t count, int dim,
     return ORC_OK;
 }
 
-/* ---- synapse.cpp:353-421 ------------------------------------------------ */
+/* ---- synapse.cpp:216-284 ------------------------------------------------ */
 
 typedef struct { int64_t row; double score; } orc_pick;
 
@@ -176,21 +176,21 @@ int orc_select_landmarks_points(const float* cloud, int64_t count, int dim,
                                 const double* attention, int64_t attention_len,
                                 int k, double lambda,
                                 int64_t* out_indices, double* out_scores, int64_t* out_n) {
-    if (k < 1) return ORC_CONFIG_ERROR;                        /* :356 */
-    if (lambda < 0.0 || lambda > 1.0) return ORC_CONFIG_ERROR; /* :357-358 */
-    if (attention_len != count) return ORC_PRECONDITION_ERROR; /* :359-360 */
+    if (k < 1) return ORC_CONFIG_ERROR;                        /* :219 */
+    if (lambda < 0.0 || lambda > 1.0) return ORC_CONFIG_ERROR; /* :220-221 */
+    if (attention_len != count) return ORC_PRECONDITION_ERROR; /* :222-223 */
     const int64_t n = count;
-    const int64_t take = (int64_t)k < n ? (int64_t)k : n;      /* :363 */
+    const int64_t take = (int64_t)k < n ? (int64_t)k : n;      /* :226 */
     if (out_n) *out_n = take;
     if (n == 0) return ORC_OK;
     unsigned char* remaining = (unsigned char*)malloc((size_t)n);
     memset(remaining, 1, (size_t)n);
     double* mindist = (double*)malloc(sizeof(double) * (size_t)n);
-    orc_coverage_scores_points(cloud, count, dim, NULL, 0, mindist); /* :365 */
+    orc_coverage_scores_points(cloud, count, dim, NULL, 0, mindist); /* :228 */
     orc_pick* picked = (orc_pick*)malloc(sizeof(orc_pick) * (size_t)(take > 0 ? take : 1));
 
     for (int64_t round = 0; round < take; ++round) {
-        /* minmax_remaining (:369-378) for attention then coverage (:382-383) */
+        /* minmax_remaining (:232-241) for attention then coverage (:245-246) */
         double amin = INFINITY, amax = -INFINITY, cmin = INFINITY, cmax = -INFINITY;
         for (int64_t i = 0; i < n; ++i) {
             if (!remaining[i]) continue;
@@ -204,7 +204,7 @@ int orc_select_landmarks_points(const float* cloud, int64_t count, int dim,
         }
         int64_t best = -1;
         double best_score = -1.0;
-        for (int64_t i = 0; i < n; ++i) { /* :386-397 */
+        for (int64_t i = 0; i < n; ++i) { /* :249-260 */
             if (!remaining[i]) continue;
             const double na = amax > amin ? (attention[i] - amin) / (amax - amin) : 0.0;
             const double nc = cmax > cmin ? (mindist[i] - cmin) / (cmax - cmin) : 0.0;
@@ -218,13 +218,13 @@ int orc_select_landmarks_points(const float* cloud, int64_t count, int dim,
         remaining[best] = 0;
         picked[round].row = best;
         picked[round].score = best_score;
-        const float* bp = cloud + (size_t)best * (size_t)dim; /* :402-410 */
+        const float* bp = cloud + (size_t)best * (size_t)dim; /* :265-273 */
         for (int64_t i = 0; i < n; ++i) {
             const double d = sqrt(sq_dist_ff(cloud + (size_t)i * (size_t)dim, bp, dim));
             mindist[i] = (round == 0) ? d : std_min(mindist[i], d);
         }
     }
-    qsort(picked, (size_t)take, sizeof(orc_pick), pick_cmp); /* :413-414 (rows unique) */
+    qsort(picked, (size_t)take, sizeof(orc_pick), pick_cmp); /* :276-277 (rows unique) */
     for (int64_t s = 0; s < take; ++s) {
         out_indices[s] = picked[s].row;
         out_scores[s] = picked[s].score;
@@ -250,7 +250,7 @@ int orc_gate_score(const float* h_main, const float* t_side, int64_t n, double* 
     return ORC_OK;
 }
 
-/* ---- synapse.cpp:276-302 ------------------------------------------------ */
+/* ---- synapse.cpp:139-165 ------------------------------------------------ */
 
 int orc_hausdorff_distance(const float* cloud, int64_t count, int dim,
                            const float* landmarks, int64_t m, int ldim, double* out) {
@@ -283,7 +283,7 @@ int orc_hausdorff_to_subset(const float* cloud, int64_t count, int dim,
     return ORC_OK;
 }
 
-/* ---- synapse.cpp:306-351 ------------------------------------------------ */
+/* ---- synapse.cpp:169-214 ------------------------------------------------ */
 
 static double mean_pairwise(const float* cloud, int64_t count, int dim) {
     double sum = 0.0;
@@ -328,7 +328,7 @@ int orc_mean_pairwise_reduction_subset(const float* cloud, int64_t count, int di
     return ORC_OK;
 }
 
-/* ---- kernels.cpp:147-186 ------------------------------------------------ */
+/* ---- kernels.cpp:103-142 ------------------------------------------------ */
 
 void orc_attend(const float* q, const float* keys, const float* values,
                 int64_t n_entries, int n_heads, int d_k, float* out) {

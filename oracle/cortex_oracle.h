@@ -53,45 +53,45 @@ double orc_rng_next_gaussian(orc_rng* r, double mean, double stddev);
 /* Fills n floats with (float)next_gaussian(mean, stddev), in order. */
 void orc_rng_fill_gaussian_f32(orc_rng* r, float* dst, int64_t n, double mean, double stddev);
 
-/* kernels.cpp:110-125 (softmax_impl). */
+/* kernels.cpp:66-81 (softmax_impl). */
 int orc_softmax(const double* scores, int64_t n, double* out);
 
-/* synapse.cpp:200-230. */
+/* synapse.cpp:63-93. */
 int orc_attention_scores_points(const float* keys, int64_t count, int dim,
                                 const float* query, int64_t query_len, int n_heads,
                                 double* out);
 
-/* synapse.cpp:173-181 (centroid_of). */
+/* synapse.cpp:36-44 (centroid_of). */
 void orc_centroid(const float* cloud, int64_t count, int dim, double* out);
 
-/* synapse.cpp:240-257. */
+/* synapse.cpp:103-120. */
 int orc_coverage_scores_points(const float* cloud, int64_t count, int dim,
                                const int64_t* selected, int64_t n_selected, double* out);
 
-/* synapse.cpp:353-421.  Writes min(k,count) ascending rows and their scores;
+/* synapse.cpp:216-284.  Writes min(k,count) ascending rows and their scores;
  * *out_n receives the count. */
 int orc_select_landmarks_points(const float* cloud, int64_t count, int dim,
                                 const double* attention, int64_t attention_len,
                                 int k, double lambda,
                                 int64_t* out_indices, double* out_scores, int64_t* out_n);
 
-/* synapse.cpp:276-302. */
-/* gate.cpp:27-43 gate_score: fp64 cosine with sequential sums, clamped to [-1, 1];
+/* gate.cpp:27-42 gate_score: fp64 cosine with sequential sums, clamped to [-1, 1];
  * ORC_DEGENERATE_INPUT_ERROR on a zero norm. */
 int orc_gate_score(const float* h_main, const float* t_side, int64_t n, double* out);
 
+/* synapse.cpp:139-165. */
 int orc_hausdorff_distance(const float* cloud, int64_t count, int dim,
                            const float* landmarks, int64_t m, int ldim, double* out);
 int orc_hausdorff_to_subset(const float* cloud, int64_t count, int dim,
                             const int64_t* rows, int64_t n_rows, double* out);
 
-/* synapse.cpp:306-351. */
+/* synapse.cpp:169-214. */
 int orc_mean_pairwise_reduction(const float* cloud, int64_t count, int dim,
                                 const float* landmarks, int64_t m, int ldim, double* out);
 int orc_mean_pairwise_reduction_subset(const float* cloud, int64_t count, int dim,
                                        const int64_t* rows, int64_t n_rows, double* out);
 
-/* kernels.cpp:147-186 (attend). */
+/* kernels.cpp:103-142 (attend). */
 void orc_attend(const float* q, const float* keys, const float* values,
                 int64_t n_entries, int n_heads, int d_k, float* out);
 

@@ -210,7 +210,7 @@ int ref_bench_landmarks(uint64_t seed, int n_seeds, int64_t cloud_size, int k, d
     });
 }
 
-// ---- KvCache-level path: select_landmarks (synapse.cpp:423-457) ------------
+// ---- KvCache-level path: select_landmarks (synapse.cpp:286-320) ------------
 // keys/values: [n_entries][n_layers][d_model] (append_entry layout).
 int ref_select_landmarks(int n_layers, int n_heads, int d_model, int64_t max_positions,
                          int64_t n_entries, const int64_t* positions, const uint8_t* origins,

@@ -1,7 +1,7 @@
 // attend_kernels.cu -- decode attention against the shared synapse (SURVEY.md
 // §8(a) A9) and the KV append used by Referential Injection (A10/A11).
 //
-// attend_fp64: the reference-shaped kernels::attend (kernels.cpp:147-186) for
+// attend_fp64: the reference-shaped kernels::attend (kernels.cpp:103-142) for
 //   the drop-in call, fp64 scores/softmax/accumulation (reference tolerance
 //   1e-6, test_kernels.cpp:159-160).
 // decode_step: one decode step of N agents.  For every (agent, layer, q-head)

@@ -118,7 +118,7 @@ static void validate_groups(const cx_groups* gr, bool need_queries) {
     if (gr->n_groups < 0 || gr->count < 0 || gr->dim < 1) fail(CX_INVALID_ARGUMENT, "bad group shape");
     if (gr->count > 0 && gr->n_groups > 0 && !gr->clouds) fail(CX_INVALID_ARGUMENT, "null clouds");
     if (need_queries) {
-        // attention_scores_points checks (synapse.cpp:203-207), per group
+        // attention_scores_points checks (synapse.cpp:66-70), per group
         if (gr->count == 0) fail(CX_PRECONDITION_ERROR, "attention_scores: empty candidate set");
         if (gr->n_pass < 1 || gr->d_k < 1) fail(CX_PRECONDITION_ERROR, "attention_scores: bad head count");
         if ((int64_t)(gr->n_pass - 1) * gr->col_step + gr->d_k > gr->dim)
@@ -192,7 +192,7 @@ extern "C" cx_status cx_ctx_lane_stream(cx_ctx* c, int lane, void** stream, int*
 extern "C" cx_status cx_attention_scores_points(const float* keys, int64_t count, int dim, const float* query,
                                                 int64_t query_len, int n_heads, double* out) {
     return guard([&] {
-        // synapse.cpp:203-207, in order
+        // synapse.cpp:66-70, in order
         if (count == 0) fail(CX_PRECONDITION_ERROR, "attention_scores: empty candidate set");
         if (query_len != (int64_t)dim) fail(CX_PRECONDITION_ERROR, "attention_scores: query width mismatch");
         if (n_heads < 1 || dim % n_heads != 0) fail(CX_PRECONDITION_ERROR, "attention_scores: bad head count");
@@ -227,7 +227,7 @@ extern "C" cx_status cx_attention_scores_points(const float* keys, int64_t count
 extern "C" cx_status cx_coverage_scores_points(const float* cloud, int64_t count, int dim, const int64_t* selected,
                                                int64_t n_selected, double* out) {
     return guard([&] {
-        if (count == 0) return;  // synapse.cpp:242-243 (empty output)
+        if (count == 0) return;  // synapse.cpp:105-106 (empty output)
         if (count < 0 || dim < 1 || !cloud || !out || (n_selected > 0 && !selected))
             fail(CX_INVALID_ARGUMENT, "null pointer / bad shape");
         cx_ctx* c = default_ctx();
@@ -259,7 +259,7 @@ extern "C" cx_status cx_select_landmarks_points(const float* cloud, int64_t coun
                                                 int64_t attention_len, int k, double lambda, int64_t* out_indices,
                                                 double* out_scores, int64_t* out_n) {
     return guard([&] {
-        // synapse.cpp:356-360, in order
+        // synapse.cpp:219-223, in order
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
         if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
         if (attention_len != count) fail(CX_PRECONDITION_ERROR, "select_landmarks: attention length mismatch");
@@ -295,7 +295,7 @@ extern "C" cx_status cx_select_landmarks_points(const float* cloud, int64_t coun
 
 namespace {
 
-// shared implementation of hausdorff_* (synapse.cpp:276-302)
+// shared implementation of hausdorff_* (synapse.cpp:139-165)
 void hausdorff_impl(const float* cloud, int64_t count, int dim, const float* lm, int64_t m, const int64_t* rows,
                     double* out) {
     cx_ctx* c = default_ctx();
@@ -321,7 +321,7 @@ void hausdorff_impl(const float* cloud, int64_t count, int dim, const float* lm,
     *out = std::sqrt(worst);
 }
 
-// mean pairwise distance over a point set (synapse.cpp:306-328)
+// mean pairwise distance over a point set (synapse.cpp:169-191)
 double mean_pairwise_impl(cx_ctx* c, const float* d_pts, int64_t count, int dim, const int64_t* d_rows, int64_t n) {
     if (n < 2) return 0.0;
     double* dsum = c->arena.take<double>(mean_pairwise_scratch(n, dim));
@@ -1005,7 +1005,7 @@ extern "C" cx_status cx_kvcache_read(const cx_kvcache* c, int layer, int64_t fir
     });
 }
 
-// ---- inject (injector.cpp:136-160) ------------------------------------------
+// ---- inject (injector.cpp:70-94) ------------------------------------------
 namespace {
 
 // Validates like inject() and begin_entry() per token; returns how many tokens
@@ -1115,7 +1115,7 @@ extern "C" cx_status cx_inject_dev(cx_kvcache* c, const float* keys, const float
 }
 
 // ============================================================================
-// cache-level select_landmarks (synapse.cpp:423-457) + snapshots + buffer
+// cache-level select_landmarks (synapse.cpp:286-320) + snapshots + buffer
 // ============================================================================
 struct cx_snapshot {
     std::atomic<int> refs{1};
@@ -1138,11 +1138,11 @@ struct cx_snapshot {
 extern "C" cx_status cx_select_landmarks(const cx_kvcache* kc, const float* query, int64_t query_len, int k,
                                          double lambda, cx_snapshot** out) {
     return guard([&] {
-        if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");  // synapse.cpp:425
+        if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");  // synapse.cpp:288
         if (!kc || !out) fail(CX_INVALID_ARGUMENT, "null cache/out");
         auto snap = std::make_unique<cx_snapshot>();
-        const int layer = kc->n_layers - 1;  // :427
-        // A1 context_key_cloud (synapse.cpp:185-198): rows with origin == context
+        const int layer = kc->n_layers - 1;  // :290
+        // A1 context_key_cloud (synapse.cpp:48-61): rows with origin == context
         std::vector<int64_t> entry_index;
         entry_index.reserve(kc->positions.size());
         for (size_t i = 0; i < kc->positions.size(); ++i)
@@ -1152,11 +1152,11 @@ extern "C" cx_status cx_select_landmarks(const cx_kvcache* kc, const float* quer
         snap->k_configured = k;
         snap->n_layers = kc->n_layers;
         snap->d_model = kc->d_model;
-        if (count == 0) {  // :435
+        if (count == 0) {  // :298
             *out = snap.release();
             return;
         }
-        // attention_scores_points checks (synapse.cpp:204-207)
+        // attention_scores_points checks (synapse.cpp:67-70)
         if (query_len != kc->d_model) fail(CX_PRECONDITION_ERROR, "attention_scores: query width mismatch");
         if (!query) fail(CX_INVALID_ARGUMENT, "null query");
         cx_ctx* c = default_ctx();
@@ -1218,7 +1218,7 @@ extern "C" cx_status cx_select_landmarks(const cx_kvcache* kc, const float* quer
         d2h(h_rows.data(), rows, sizeof(int64_t) * take, s);
         d2h(snap->scores.data(), scores, sizeof(double) * take, s);
         check_flag_and_sync(c);
-        // gather the winners' K/V for EVERY layer (synapse.cpp:440-455)
+        // gather the winners' K/V for EVERY layer (synapse.cpp:303-318)
         std::vector<int64_t> h_entries((size_t)take);
         snap->positions.resize((size_t)take);
         for (int s2 = 0; s2 < take; ++s2) {
@@ -1327,7 +1327,7 @@ extern "C" cx_status cx_snapshot_read(const cx_snapshot* s, int64_t* positions, 
     });
 }
 
-// ---- SynapseBuffer (synapse.cpp:474-499) --------------------------------------
+// ---- SynapseBuffer (synapse.cpp:337-362) --------------------------------------
 struct cx_synapse_buffer {
     std::mutex mu;
     std::condition_variable cv;

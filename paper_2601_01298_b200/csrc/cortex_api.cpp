@@ -313,7 +313,7 @@ SynapseSnapshot select_landmarks(const KvCache& cache, std::span<const float> qu
 }
 
 std::string SynapseSnapshot::to_json() const {
-    // synapse.cpp:459-472: nlohmann object (sorted keys), compact dump
+    // synapse.cpp:322-335: nlohmann object (sorted keys), compact dump
     std::ostringstream os;
     os << "{\"hybrid_scores\":[";
     for (size_t i = 0; i < landmarks.size(); ++i) os << (i ? "," : "") << json_double(landmarks[i].hybrid_score);
@@ -323,7 +323,7 @@ std::string SynapseSnapshot::to_json() const {
     return os.str();
 }
 
-// SynapseBuffer (synapse.cpp:474-499): version-stamped latest-value slot.
+// SynapseBuffer (synapse.cpp:337-362): version-stamped latest-value slot.
 // Snapshots are immutable after push; the device K/V travel inside them.
 uint64_t SynapseBuffer::push(SynapseSnapshot snap) {
     auto owned = std::make_shared<SynapseSnapshot>(std::move(snap));

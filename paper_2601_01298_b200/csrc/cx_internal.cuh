@@ -153,7 +153,7 @@ void gate_decide(const float* h, int64_t hs, const float* t, int64_t ts, int64_t
                  double* score, uint8_t* accepted, uint8_t* degenerate, cudaStream_t s);
 // groups per selection wave for G groups of L rows (dim 64), 0 if not on chip
 int select64_wave(int64_t L, int G);
-// centroid_of for every group (synapse.cpp:173-181), bit-exact sequential sums
+// centroid_of for every group (synapse.cpp:36-44), bit-exact sequential sums
 void centroid_launch(const GroupView& g, double* cen, cudaStream_t s);
 void plan_select(ArenaPlan& p, const GroupView& g, int k);
 // dim-64 fast path (select64.cu); false when it does not apply

@@ -28,7 +28,7 @@
 //   (gated by an epilogue counter; two parity-split mbarriers hand tiles over).
 // The merge (m = max(m_s, m_p); O = (O_s e^{m_s-m} + O_p e^{m_p-m}) /
 // (l_s e^{m_s-m} + l_p e^{m_p-m})) is the one-pass softmax of the reference's
-// kernels::attend (kernels.cpp:127-158) over [synapse rows || private rows].
+// kernels::attend (kernels.cpp:103-142) over [synapse rows || private rows].
 // Accuracy: every synapse product is formed to ~2^-16 relative and all sums
 // accumulate in fp32: the north_star's "fp32 accumulate, 1e-3 relative".
 #include <cuda_bf16.h>

@@ -1,5 +1,5 @@
 // select64.cu -- the greedy hybrid selection (SURVEY.md §8(a) A4/A6,
-// synapse.cpp:353-421) specialised for d = 64, the per-(layer, KV-head) key
+// synapse.cpp:216-284) specialised for d = 64, the per-(layer, KV-head) key
 // width of the 0.5B-class shape.  select128.cu compiles the same kernel for
 // d = 128 (the head-concatenated reference-mode cloud) with no register rows.
 //
@@ -181,7 +181,7 @@ __host__ __device__ inline Sel64Layout sel64_layout(int Rs, int mode) {
     return l;
 }
 
-// exact sq_dist(point, pick) in the reference's order (synapse.cpp:155-162);
+// exact sq_dist(point, pick) in the reference's order (synapse.cpp:18-25);
 // the row is read through get4(c4) -> float4, the pick as floats (exact in fp64).
 template <int UNR = 16, class Get4>
 __device__ __forceinline__ double exact_sq(Get4 get4, const float* b) {
@@ -202,7 +202,7 @@ __device__ __forceinline__ double exact_sq(Get4 get4, const float* b) {
     return acc;
 }
 
-// same against the fp64 centroid (sq_dist(span<float>, vector<double>), synapse.cpp:164-171)
+// same against the fp64 centroid (sq_dist(span<float>, vector<double>), synapse.cpp:27-34)
 template <int UNR = 16, class Get4>
 __device__ __forceinline__ double exact_sq_d(Get4 get4, const double* b) {
     double acc = 0.0;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
             if (k < nr) {
                 const int li = tid + k * NT;
                 a[k] = p.attn[(int64_t)g * p.L + r0 + li];
-                // coverage init: distance to the centroid (synapse.cpp:244-249)
+                // coverage init: distance to the centroid (synapse.cpp:107-112)
                 if (REG && k == 0) {
                     m[k] = __dsqrt_rn(exact_sq_d(reg4, cen));
                     nx[k] = (float)norm2(reg4);
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         }
         STAMP(3);
 
-        // ======== H: hybrid argmax (synapse.cpp:384-397) ========
+        // ======== H: hybrid argmax (synapse.cpp:247-260) ========
         const bool a_span = amax > amin, c_span = cmax > cmin;
         const double ar = __dsub_rn(amax, amin), cr = __dsub_rn(cmax, cmin);
         const double iar = a_span ? __drcp_rn(ar) : 0.0, icr = c_span ? __drcp_rn(cr) : 0.0;
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         STAMP(5);
     }
 
-    // ---- sort the picks ascending by row (synapse.cpp:413-414) ----
+    // ---- sort the picks ascending by row (synapse.cpp:276-277) ----
     __syncthreads();
     if (rank == 0) {
         int64_t* out_rows = p.out_rows + (int64_t)g * p.take;

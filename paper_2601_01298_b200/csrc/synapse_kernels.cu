@@ -27,7 +27,7 @@ __device__ __forceinline__ double dmax_std(double a, double b) { return (a < b) 
 
 // ----------------------------------------------------------------------------
 // A3: attention mass.  K1: scores[g][p][i] = (sum_c q_c * k_ic) * (1/sqrt(d_k))
-// with the reference's sequential fp64 dot (synapse.cpp:213-223).
+// with the reference's sequential fp64 dot (synapse.cpp:76-86).
 // ----------------------------------------------------------------------------
 __global__ void attn_scores_kernel(GroupView gv, double inv_sqrt_dk, double* __restrict__ scores,
                                    int* flag) {
@@ -113,7 +113,7 @@ __device__ T block_reduce(T v, Op op, T identity, T* smem /* >= 32 */) {
     return r;
 }
 
-// K2: per (group, pass): max, e_i = exp(s_i - max) in place, sum (kernels.cpp:110-125).
+// K2: per (group, pass): max, e_i = exp(s_i - max) in place, sum (kernels.cpp:66-81).
 __global__ void attn_softmax_kernel(int64_t L, int P, double* __restrict__ scores,
                                     double* __restrict__ sums) {
     __shared__ double red[32];
@@ -132,7 +132,7 @@ __global__ void attn_softmax_kernel(int64_t L, int P, double* __restrict__ score
     if (threadIdx.x == 0) sums[gp] = acc;
 }
 
-// K3: total_i = ((0 + e_0i/sum_0) + e_1i/sum_1) + ...  (pass order, synapse.cpp:224-227)
+// K3: total_i = ((0 + e_0i/sum_0) + e_1i/sum_1) + ...  (pass order, synapse.cpp:87-90)
 __global__ void attn_total_kernel(int64_t L, int P, const double* __restrict__ e,
                                   const double* __restrict__ sums, double* __restrict__ out) {
     const int g = blockIdx.y;
@@ -145,7 +145,7 @@ __global__ void attn_total_kernel(int64_t L, int P, const double* __restrict__ e
 }
 
 // ----------------------------------------------------------------------------
-// A2: centroid_of (synapse.cpp:173-181) -- summed sequentially over rows, as
+// A2: centroid_of (synapse.cpp:36-44) -- summed sequentially over rows, as
 // the reference does; one thread per coordinate.
 // ----------------------------------------------------------------------------
 __global__ void centroid_kernel(GroupView gv, double* __restrict__ cen) {
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) centroid_staged_kernel(GroupView gv, doub
 }
 
 // sq_dist(span<float>, vector<double>) / sq_dist(span<float>, span<float>)
-// (synapse.cpp:155-171): sequential over coordinates, no FMA.
+// (synapse.cpp:18-34): sequential over coordinates, no FMA.
 __device__ __forceinline__ double sq_dist_exact(const float* x, int64_t xs, const double* b, int dim) {
     double acc = 0.0;
     for (int c = 0; c < dim; ++c) {
@@ -262,7 +262,7 @@ __device__ __forceinline__ double sq_dist_exact_ff(const float* a, const float* 
     return acc;
 }
 
-// coverage with empty selection: sqrt(sq_dist(x_i, centroid))  (synapse.cpp:244-249)
+// coverage with empty selection: sqrt(sq_dist(x_i, centroid))  (synapse.cpp:107-112)
 __global__ void coverage_centroid_kernel(GroupView gv, const double* __restrict__ cen,
                                          double* __restrict__ out) {
     extern __shared__ double cs[];
@@ -275,7 +275,7 @@ __global__ void coverage_centroid_kernel(GroupView gv, const double* __restrict_
         __dsqrt_rn(sq_dist_exact(gv.X + g * gv.gstride + i * gv.rstride, 1, cs, gv.dim));
 }
 
-// coverage with a selection: sqrt(min_s sq_dist(x_i, x_s))  (synapse.cpp:251-256)
+// coverage with a selection: sqrt(min_s sq_dist(x_i, x_s))  (synapse.cpp:114-119)
 __global__ void coverage_selected_kernel(GroupView gv, const int64_t* __restrict__ sel, int64_t n_sel,
                                          double* __restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -287,7 +287,7 @@ __global__ void coverage_selected_kernel(GroupView gv, const int64_t* __restrict
 }
 
 // ----------------------------------------------------------------------------
-// A4/A6: greedy hybrid selection (synapse.cpp:353-421).
+// A4/A6: greedy hybrid selection (synapse.cpp:216-284).
 //
 // One thread-block cluster per group; CTA r owns rows [r*S, r*S+S).  Rows are
 // staged once into shared memory, column-major (conflict-free), when they fit;
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(512, 1) select_kernel(SelectParams p) {
             cmax = dmax_std(cmax, mm[r * 4 + 3]);
         }
 
-        // ---- 2. hybrid argmax (synapse.cpp:384-397) ----
+        // ---- 2. hybrid argmax (synapse.cpp:247-260) ----
         const bool a_span = amax > amin, c_span = cmax > cmin;
         const double ar = __dsub_rn(amax, amin), cr = __dsub_rn(cmax, cmin);
         double bs = -1.0;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(512, 1) select_kernel(SelectParams p) {
         if (br >= r0 && br < r0 + nrows && tid == 0) rem[br - r0] = 0;
         __syncthreads();
 
-        // ---- 3. distance update against the pick (synapse.cpp:402-410) ----
+        // ---- 3. distance update against the pick (synapse.cpp:265-273) ----
         amin = INFINITY; amax = -INFINITY; cmin = INFINITY; cmax = -INFINITY;
         if (round + 1 < p.take) {
             for (int li = tid; li < nrows; li += nt) {
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(512, 1) select_kernel(SelectParams p) {
         }
     }
 
-    // ---- sort picks ascending by row (synapse.cpp:413-414) ----
+    // ---- sort picks ascending by row (synapse.cpp:276-277) ----
     cluster.sync();
     if (rank == 0) {
         __syncthreads();

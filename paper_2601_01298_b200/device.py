@@ -106,7 +106,7 @@ def _groups(keys: torch.Tensor, queries: torch.Tensor | None, mode: str) -> CxGr
 
 
 def attention_grouped(keys: torch.Tensor, queries: torch.Tensor, mode: str = "gqa") -> torch.Tensor:
-    """Attention mass per row of every group -> [G, L] fp64 (synapse.cpp:200-230)."""
+    """Attention mass per row of every group -> [G, L] fp64 (synapse.cpp:63-93)."""
     g = _groups(keys, queries, mode)
     out = torch.empty((g.n_groups, g.count), dtype=torch.float64, device=keys.device)
     check(lib.cx_attention_grouped_dev(ctx(keys.device.index), C.byref(g), out.data_ptr(), _stream()),
@@ -127,7 +127,7 @@ def select_grouped(keys: torch.Tensor, attention: torch.Tensor, k: int, lam: flo
 
 
 def gather_rows(src: torch.Tensor, rows: torch.Tensor, dst: torch.Tensor) -> torch.Tensor:
-    """Landmark gather: dst[g, s] = src[g, rows[g, s]] (synapse.cpp:440-455 copy)."""
+    """Landmark gather: dst[g, s] = src[g, rows[g, s]] (synapse.cpp:303-318 copy)."""
     g = _groups(src, None, "gqa")
     if not rows.is_contiguous() or rows.dtype != torch.int64 or not dst.is_contiguous():
         raise TypeError("rows must be contiguous int64 [G, take]; dst contiguous [G, take, d]")

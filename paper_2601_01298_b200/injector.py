@@ -55,7 +55,7 @@ class InjectionRecord:
 
 
 def inject(river_cache: KvCache, block: KvBlock, thought_id: int, stream_position: int) -> InjectionRecord:
-    """injector.hpp:46-47 / injector.cpp:136-160."""
+    """injector.hpp:46-47 / injector.cpp:70-94."""
     n = block.n_layers * block.token_count * block.d_model
     k = np.ascontiguousarray(block.keys, np.float32).reshape(-1)
     v = np.ascontiguousarray(block.values, np.float32).reshape(-1)
@@ -81,7 +81,7 @@ def inject_dev(river_cache: KvCache, keys_dev: int, values_dev: int, base_positi
 
 
 class VirtualPositionPlanner:
-    """injector.hpp:51-64 / injector.cpp:162-176 (host bookkeeping)."""
+    """injector.hpp:51-64 / injector.cpp:96-110 (host bookkeeping)."""
 
     def __init__(self, reserved_start: int, max_positions: int):
         if reserved_start < 0 or reserved_start >= max_positions:

@@ -100,7 +100,7 @@ class SynapseSnapshot:
         return len(self.landmarks) * self.n_layers * 2 * self.d_model * 4
 
     def to_json(self) -> str:
-        """synapse.cpp:459-472 (nlohmann dump: no spaces)."""
+        """synapse.cpp:322-335 (nlohmann dump: no spaces)."""
         import json
         return json.dumps({"hybrid_scores": [lm.hybrid_score for lm in self.landmarks],
                            "positions": [lm.source_position for lm in self.landmarks],
@@ -148,7 +148,7 @@ class ContextCloud:
 
 
 def context_key_cloud(cache: KvCache, layer: int) -> ContextCloud:
-    """synapse.cpp:185-198: rows with origin == context, in cache order."""
+    """synapse.cpp:48-61: rows with origin == context, in cache order."""
     keys = cache.layer_keys(layer).reshape(cache.size(), cache.config().d_model)
     org = cache.origins()
     idx = np.nonzero(org == int(Origin.context))[0].astype(np.int64)
@@ -168,7 +168,7 @@ def attention_scores_points(keys, query, n_heads: int) -> np.ndarray:
 
 
 def attention_scores(cache: KvCache, query, layer: int) -> np.ndarray:
-    """synapse.hpp:68-69 / synapse.cpp:232-238."""
+    """synapse.hpp:68-69 / synapse.cpp:95-101."""
     ctx = context_key_cloud(cache, layer)
     if ctx.cloud.count == 0:
         raise errors.precondition_error("attention_scores: cache has no context entries")
@@ -186,7 +186,7 @@ def coverage_scores_points(cloud, selected: Sequence[int] = ()) -> np.ndarray:
 
 
 def coverage_scores(cache: KvCache, selected_positions: Sequence[int], layer: int) -> np.ndarray:
-    """synapse.hpp:77-79 / synapse.cpp:259-274."""
+    """synapse.hpp:77-79 / synapse.cpp:122-137."""
     ctx = context_key_cloud(cache, layer)
     pos_to_row = {int(p): r for r, p in enumerate(ctx.positions)}
     rows = []
@@ -269,7 +269,7 @@ class SynapseBuffer:
 
     def push(self, snap: SynapseSnapshot) -> int:
         """Stamps and returns the version (1, 2, ...); the buffer takes the
-        snapshot over (the reference moves it in, synapse.cpp:474-481)."""
+        snapshot over (the reference moves it in, synapse.cpp:337-344)."""
         if snap.handle is None:
             snap._h = _device_snapshot_from_host(snap)
         v = C.c_uint64(0)

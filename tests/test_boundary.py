@@ -81,7 +81,7 @@ def _select(lib, cloud, attn, k, lam):
 
 def test_validation_precedes_device_work(lib):
     cloud = np.zeros((3, 2), np.float32)
-    # synapse.cpp:356-360 order: k, then lambda, then attention length
+    # synapse.cpp:219-223 order: k, then lambda, then attention length
     assert _select(lib, cloud, np.zeros(3), 0, 0.5) == 1           # config_error
     assert _select(lib, cloud, np.zeros(3), 1, 1.5) == 1           # config_error
     assert _select(lib, cloud, np.zeros(3), 0, 7.0) == 1           # k checked first

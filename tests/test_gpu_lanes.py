@@ -138,7 +138,7 @@ def test_compress_grouped_host_matches_device(cx, G, pinned, L, k):
 
 def test_compress_grouped_host_mha_d128(cx):
     """The reference-mode cloud through the host path: a 2-head MHA cache's rows
-    (d_model = 128, heads concatenated, col_step = d_k; synapse.cpp:423-457) -- the
+    (d_model = 128, heads concatenated, col_step = d_k; synapse.cpp:286-320) -- the
     d = 128 selection kernel and the fallback chunking -- == the device path, bitwise."""
     import torch
     from paper_2601_01298_b200 import device

@@ -321,7 +321,7 @@ def test_cache_level_reference_cases(cx):
     empty = cx.KvCache(cx.ModelConfig(n_layers=1, n_heads=1, d_model=2, d_k=2, max_positions=64))
     with pytest.raises(cx.errors.precondition_error):
         cx.attention_scores(empty, np.array([1, 0], np.float32), 0)
-    # injected-only cache: snapshot with no landmarks (synapse.cpp:435)
+    # injected-only cache: snapshot with no landmarks (synapse.cpp:298)
     snap = cx.select_landmarks(empty, np.array([1, 0], np.float32), 4, 0.5)
     assert snap.source_length == 0 and snap.landmarks == []
 
@@ -355,7 +355,7 @@ def test_kvcache_protocol(cx):
 
 
 def test_inject(cx):
-    """injector.cpp:136-160 + test_injector.cpp:81-125 semantics."""
+    """injector.cpp:70-94 + test_injector.cpp:81-125 semantics."""
     cfg = cx.ModelConfig(n_layers=3, n_heads=2, d_model=8, d_k=4, max_positions=8192)
     c = cx.KvCache(cfg)
     rs = np.random.default_rng(5)
@@ -386,7 +386,7 @@ def test_inject(cx):
     c.begin_entry(6, cx.Origin.context)
     with pytest.raises(cx.errors.sequencing_error):
         cx.inject(c, blk, 1, 6)
-    # planner (injector.cpp:162-176)
+    # planner (injector.cpp:96-110)
     p = cx.VirtualPositionPlanner(7168, 8192)
     assert p.reserve(16) == 7168 and p.reserve(8) == 7184
     with pytest.raises(cx.errors.capacity_error):
