@@ -144,6 +144,20 @@ cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* a
                                 int k, double lambda, unsigned flags,
                                 int64_t* out_rows, double* out_scores, void* stream);
 
+/* Decision-gap monitor (SURVEY.md §7 "per-round gap monitor").  Writes, for
+ * each of the n_groups groups of this ctx's most recent selection launch (the
+ * last cx_select_grouped_dev / cx_compress_grouped_dev call, or the last chunk
+ * of cx_compress_grouped_host), the smallest top-1 / top-2 gap of the exact
+ * hybrid score over its greedy rounds, capped at 1e-10 (gaps above the cap are
+ * not resolved).  The attention mass is within 1e-12 relative of the
+ * reference's (CUDA vs glibc exp, tree-ordered softmax sum), which moves a
+ * normalised hybrid score by a few 1e-12 when amax >> amin; a gap above 1e-11
+ * therefore certifies that the reference makes the same pick in every round.
+ * NaN = not monitored (the generic-dim kernel).  `out` may be host or device
+ * memory; the copy is ordered on `stream`, after the selection.
+ * CX_PRECONDITION_ERROR if n_groups exceeds the last launch's group count. */
+cx_status cx_selection_gaps(cx_ctx* ctx, int n_groups, double* out, void* stream);
+
 /* Landmark gather (synapse.cpp:303-318 copy, per group): dst[g][s][:] =
  * src row rows[g][s] of group g (same addressing as g->clouds, base `src`). */
 cx_status cx_gather_grouped_dev(cx_ctx* ctx, const cx_groups* g, const float* src,

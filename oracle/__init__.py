@@ -246,6 +246,34 @@ class Backend:
               _p(out, _f32p))
         return out
 
+    def decode_attend(self, syn_k, syn_v, tail_k, tail_v, tail_len, q, n_threads: int | None = None) -> np.ndarray:
+        """Expected batched-decode outputs: attend (n_heads = 1) per (agent, layer,
+        q-head) over [synapse rows || private rows [0, tail_len[a])]
+        (orc_decode_attend_agents).  Agents are split over host threads: the C
+        call releases the GIL."""
+        import threading
+        if self.is_ref:
+            raise NotImplementedError("decode_attend is a restatement-side composition")
+        sk, sv, tk, tv, qq = _f32(syn_k), _f32(syn_v), _f32(tail_k), _f32(tail_v), _f32(q)
+        tl = np.ascontiguousarray(tail_len, dtype=np.int32)
+        n, n_layers, n_q, d_k = qq.shape
+        n_kv, k_syn, t_cap = sk.shape[1], sk.shape[2], tk.shape[3]
+        out = np.empty_like(qq)
+        f = self._fn("decode_attend_agents")
+        n_threads = max(1, min(n, n_threads or (os.cpu_count() or 1)))
+
+        def run(a0, a1):
+            f(C.c_int64(a0), C.c_int64(a1), n_layers, n_kv, n_q, d_k, C.c_int64(k_syn), C.c_int64(t_cap),
+              _p(sk, _f32p), _p(sv, _f32p), _p(tk, _f32p), _p(tv, _f32p), _p(tl, _i32p), _p(qq, _f32p), _p(out, _f32p))
+
+        bounds = [n * i // n_threads for i in range(n_threads + 1)]
+        ts = [threading.Thread(target=run, args=(bounds[i], bounds[i + 1])) for i in range(n_threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return out
+
     # ---- harness/bench.cpp ---------------------------------------------
     def make_clustered_cloud(self, rng: Rng, count: int, dim: int, n_clusters: int, separation: float,
                              sigma: float, rare: int = 4):

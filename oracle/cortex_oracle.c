@@ -360,6 +360,42 @@ void orc_attend(const float* q, const float* keys, const float* values,
     free(w);
 }
 
+/* Batched decode oracle (GQA composition): for agents
+ * [a0, a1), every layer l and q-head h of KV head g = h / (n_q / n_kv), the
+ * reference's kernels::attend (kernels.cpp:103-142) with n_heads = 1 over the
+ * agent's cache as run_agent builds it (scheduler.cpp:245-262): the k_syn
+ * synapse rows of (l, g) first, then the agent's private rows [0, tail_len[a]).
+ * Layouts: syn [n_layers][n_kv][k_syn][d_k]; tail [N][n_layers][n_kv][t_cap][d_k];
+ * q / out [N][n_layers][n_q][d_k]. */
+void orc_decode_attend_agents(int64_t a0, int64_t a1, int n_layers, int n_kv, int n_q, int d_k, int64_t k_syn,
+                              int64_t t_cap, const float* syn_k, const float* syn_v, const float* tail_k,
+                              const float* tail_v, const int32_t* tail_len, const float* q, float* out) {
+    const int64_t cap = k_syn + t_cap;
+    float* kk = (float*)malloc(sizeof(float) * (size_t)(cap > 0 ? cap : 1) * (size_t)d_k);
+    float* vv = (float*)malloc(sizeof(float) * (size_t)(cap > 0 ? cap : 1) * (size_t)d_k);
+    const int qpg = n_q / n_kv;
+    for (int64_t a = a0; a < a1; ++a) {
+        const int64_t nt = tail_len[a];
+        for (int l = 0; l < n_layers; ++l)
+            for (int g = 0; g < n_kv; ++g) {
+                const size_t so = ((size_t)l * (size_t)n_kv + (size_t)g) * (size_t)k_syn * (size_t)d_k;
+                const size_t to = (((size_t)a * (size_t)n_layers + (size_t)l) * (size_t)n_kv + (size_t)g) *
+                                  (size_t)t_cap * (size_t)d_k;
+                memcpy(kk, syn_k + so, sizeof(float) * (size_t)k_syn * (size_t)d_k);
+                memcpy(vv, syn_v + so, sizeof(float) * (size_t)k_syn * (size_t)d_k);
+                memcpy(kk + (size_t)k_syn * (size_t)d_k, tail_k + to, sizeof(float) * (size_t)nt * (size_t)d_k);
+                memcpy(vv + (size_t)k_syn * (size_t)d_k, tail_v + to, sizeof(float) * (size_t)nt * (size_t)d_k);
+                for (int hh = 0; hh < qpg; ++hh) {
+                    const size_t qo = (((size_t)a * (size_t)n_layers + (size_t)l) * (size_t)n_q +
+                                       (size_t)g * (size_t)qpg + (size_t)hh) * (size_t)d_k;
+                    orc_attend(q + qo, kk, vv, k_syn + nt, 1, d_k, out + qo);
+                }
+            }
+    }
+    free(kk);
+    free(vv);
+}
+
 /* ---- harness/bench.cpp:65-125 ------------------------------------------- */
 
 void orc_make_clustered_cloud(orc_rng* r, int64_t count, int dim, int n_clusters,

@@ -95,6 +95,13 @@ int orc_mean_pairwise_reduction_subset(const float* cloud, int64_t count, int di
 void orc_attend(const float* q, const float* keys, const float* values,
                 int64_t n_entries, int n_heads, int d_k, float* out);
 
+/* Batched decode oracle: kernels.cpp:103-142 attend (n_heads = 1) per
+ * (agent, layer, q-head) over [synapse rows of its KV head || private rows
+ * [0, tail_len[a])] (scheduler.cpp:245-262); agents [a0, a1). */
+void orc_decode_attend_agents(int64_t a0, int64_t a1, int n_layers, int n_kv, int n_q, int d_k, int64_t k_syn,
+                              int64_t t_cap, const float* syn_k, const float* syn_v, const float* tail_k,
+                              const float* tail_v, const int32_t* tail_len, const float* q, float* out);
+
 /* harness/bench.cpp:65-112 (make_clustered_cloud); writes count*dim floats,
  * dim query floats and count cluster ids. */
 void orc_make_clustered_cloud(orc_rng* r, int64_t count, int dim, int n_clusters,

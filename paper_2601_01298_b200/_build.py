@@ -50,14 +50,30 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps() + [__file__])
 
 
+NEGCTL_LIB = os.path.join(ROOT, "tests", "negctl", "libcortex_negctl.so")
+# test-only variant (tests/test_gpu_decode_scale.py negative control): the decode
+# score GEMM without its bf16 lo terms.  Never loaded by the product.
+NEGCTL_DEFS = {"decode_tc.cu": ["-DCX_NEGCTL_BF16_S"]}
+
+
+def _link(objs, out):
+    tmp = out + ".tmp"
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs + \
+          ["-lcudart_static", "-lpthread", "-ldl", "-lrt"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, out)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+    if not force and up_to_date() and os.path.exists(NEGCTL_LIB):
         return LIB
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs, cmds = [], []
+    os.makedirs(os.path.dirname(NEGCTL_LIB), exist_ok=True)
+    objs, negobjs, cmds = [], [], []
     for src in _sources():
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        base = os.path.basename(src)
+        obj = os.path.join(objdir, base + ".o")
         if src.endswith(".cu"):
             cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else [])
         else:
@@ -66,16 +82,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), file=sys.stderr)
         cmds.append(cmd)
         objs.append(obj)
+        if base in NEGCTL_DEFS:
+            nobj = os.path.join(objdir, base + ".negctl.o")
+            cmds.append([NVCC] + NVCC_FLAGS + NEGCTL_DEFS[base] + ["-c", src, "-o", nobj])
+            negobjs.append(nobj)
+        else:
+            negobjs.append(obj)
     # translation units compile independently: one nvcc per source, in parallel
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
         for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
             if r.returncode != 0:
                 raise subprocess.CalledProcessError(r.returncode, r.args)
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs + ["-lcudart_static", "-lpthread", "-ldl", "-lrt"]
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    _link(objs, LIB)
+    _link(negobjs, NEGCTL_LIB)
     return LIB
 
 

@@ -87,6 +87,7 @@ _SIGS = [
     ("cx_select_grouped_dev", C.c_int,
      [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp]),
     ("cx_gather_grouped_dev", C.c_int, [c_vp, C.POINTER(CxGroups), c_vp, c_vp, C.c_int, c_vp, c_vp]),
+    ("cx_selection_gaps", C.c_int, [c_vp, C.c_int, c_vp, c_vp]),
     ("cx_compress_grouped_dev", C.c_int,
      [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp, c_vp, c_vp]),
     ("cx_decode_step_dev", C.c_int, [c_vp, C.POINTER(CxDecodeBatch), c_vp]),

@@ -159,6 +159,7 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
         cudaStreamSynchronize(c->side);
         if (c->arena.base) cudaFree(c->arena.base);
         if (c->d_flag) cudaFree(c->d_flag);
+        if (c->gaps) cudaFree(c->gaps);
         cudaEventDestroy(c->ev_fork);
         cudaEventDestroy(c->ev_join);
         cudaStreamSynchronize(c->copy);
@@ -515,6 +516,17 @@ extern "C" cx_status cx_select_grouped_dev(cx_ctx* c, const cx_groups* gr, const
         c->arena.reserve(pl.used);
         c->arena.reset();
         select_grouped(c, g, attention, k, lambda, flags, out_rows, out_scores, (cudaStream_t)stream);
+    });
+}
+
+extern "C" cx_status cx_selection_gaps(cx_ctx* c, int n_groups, double* out, void* stream) {
+    return guard([&] {
+        if (!c || !out) fail(CX_INVALID_ARGUMENT, "null ctx/out");
+        if (n_groups < 0 || n_groups > c->gaps_n)
+            fail(CX_PRECONDITION_ERROR, "selection_gaps: more groups than the last selection launch");
+        if (n_groups == 0) return;
+        CX_CUDA(cudaMemcpyAsync(out, c->gaps, sizeof(double) * (size_t)n_groups, cudaMemcpyDefault,
+                                (cudaStream_t)stream));
     });
 }
 

@@ -110,6 +110,8 @@ struct cx_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cx::Arena arena;                // device scratch
     int* d_flag = nullptr;          // device-side error flag (softmax non-finite, ...)
+    double* gaps = nullptr;         // decision-gap monitor: [gaps_n] of the last selection (device)
+    int gaps_cap = 0, gaps_n = 0;
     int num_sms = 0;
     std::mutex mu;
 };
@@ -138,6 +140,8 @@ void attention_grouped(cx_ctx* ctx, const GroupView& g, double* out, cudaStream_
 // bytes of arena scratch attention_grouped needs
 void plan_attention(ArenaPlan& p, const GroupView& g);
 
+// selection-monitor scratch per (group, round): one candidate per cluster CTA (<= 16)
+constexpr int kGapRecStride = 16;
 // greedy selection for all groups.  rows/scores out [G][take] ascending.
 void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
                     unsigned flags, int64_t* rows, double* scores, cudaStream_t s,
@@ -145,7 +149,7 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
 // d = 128 instantiation (select128.cu): the reference-mode cloud of a 2-head MHA cache
 bool select128_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
                       unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
-                      cudaStream_t s);
+                      double* gaps, double* gap_rec, cudaStream_t s);
 int select128_wave(int64_t L, int G);
 // gate.cpp:27-61 for n (h, t) pairs (row strides in floats): score (NaN when degenerate),
 // accepted = score >= theta, degenerate = zero norm
@@ -159,7 +163,7 @@ void plan_select(ArenaPlan& p, const GroupView& g, int k);
 // dim-64 fast path (select64.cu); false when it does not apply
 bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
-                     cudaStream_t s);
+                     double* gaps, double* gap_rec, cudaStream_t s);
 
 // gather selected rows from a (values or keys) tensor with the group addressing.
 void gather_rows(const GroupView& g, const float* src, const int64_t* rows, int take, float* dst,

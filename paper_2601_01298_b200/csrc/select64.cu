@@ -66,8 +66,15 @@ enum : int { ROWS_L2 = 0, ROWS_SMEM = 1, ROWS_SKETCH = 2 };
 // float4 reads (thread t, row t) hit 8 distinct 16-byte slots per quarter warp
 constexpr int SPITCH = D + 4;
 constexpr int MAXC = 16;
+static_assert(MAXC == kGapRecStride, "gap-monitor record stride");
 constexpr int MAXRPT_ALL = 4;    // rows per thread (S <= 2048)
-constexpr double HYB_MARGIN = 1e-12;
+// decision-gap monitor window: rows whose approximate hybrid is within GAP_WINDOW of the
+// CTA maximum are scored exactly, so the top-1 / top-2 gap of every round is known
+// exactly when it is below GAP_WINDOW (and reported as GAP_WINDOW otherwise)
+#ifndef CX_GAP_WINDOW
+#define CX_GAP_WINDOW 1e-10
+#endif
+constexpr double GAP_WINDOW = CX_GAP_WINDOW;
 
 __device__ __forceinline__ double dmin_std(double a, double b) { return (b < a) ? b : a; }  // std::min
 __device__ __forceinline__ double dmax_std(double a, double b) { return (a < b) ? b : a; }  // std::max
@@ -139,6 +146,8 @@ struct Sel64Params {
     int64_t* out_rows;
     double* out_scores;
     long long* trace;    // optional per-round phase timestamps (CX_SEL_TRACE=1)
+    double* gaps;        // [G]: smallest top-1 / top-2 hybrid gap over the rounds (capped at GAP_WINDOW)
+    double* gap_rec;     // [G][take][MAXC] scratch: per round, each CTA's runner-up candidate
 };
 
 #define STAMP(k)                                                        \
@@ -147,12 +156,13 @@ struct Sel64Params {
             p.trace[round * 16 + (k)] = clock64();                      \
     } while (0)
 
-// X2 payload header: (score, row) + (|b|^2 of the candidate row, pad)
+// X2 payload header: (score, row) + (|b|^2 of the candidate row, the CTA's second-best
+// exact score in its gap window, -1 if none)
 struct alignas(16) Hdr {
     double score;
     long long row;
     double nb;
-    double pad;
+    double second;
 };
 
 struct Sel64Layout {
@@ -307,6 +317,9 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
     int* qn = reinterpret_cast<int*>(&misc[0]);              // queue length
     unsigned long long* hkey = &misc[1];                      // max exact score bits
     unsigned long long* hrow = &misc[2];                      // min row among ties
+    unsigned long long* hkey2 = &misc[3];                     // [2] by round parity: second-best score bits
+    unsigned long long* min_gap = &misc[5];                   // gap monitor: bits of the smallest gap (rank 0)
+    unsigned long long* ties = &misc[6];                      // [2] by round parity: rows scoring the CTA max
 
     const float* gX = p.X + g * p.gstride + r0 * p.rstride;
 
@@ -400,6 +413,9 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         qn[0] = 0;
         *hkey = 0ull;
         *hrow = ~0ull;
+        hkey2[0] = hkey2[1] = 0ull;
+        ties[0] = ties[1] = 0ull;
+        *min_gap = (unsigned long long)__double_as_longlong(GAP_WINDOW);
     }
     __syncthreads();
     cluster.sync();  // mbarriers visible cluster-wide before any remote push
@@ -583,7 +599,7 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         // the reciprocal form is within ~1e-15 of the exact hybrid unless a range
         // is so small that 1/range leaves the normal range: then rank exactly
         const bool approx_ok = (!a_span || ar >= 1e-290) && (!c_span || cr >= 1e-290);
-        const double cut = approx_ok ? hmax - HYB_MARGIN : -INFINITY;
+        const double cut = approx_ok ? hmax - GAP_WINDOW : -INFINITY;
         double hex[MAXRPT];
 #pragma unroll
         for (int k = 0; k < MAXRPT; ++k) {
@@ -598,9 +614,16 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         __syncthreads();
         const unsigned long long kbest = *hkey;
 #pragma unroll
-        for (int k = 0; k < MAXRPT; ++k)
-            if ((remm >> k & 1u) && hex[k] >= 0.0 && (unsigned long long)__double_as_longlong(hex[k]) == kbest)
+        for (int k = 0; k < MAXRPT; ++k) {
+            if (!(remm >> k & 1u) || hex[k] < 0.0) continue;
+            const unsigned long long kb = (unsigned long long)__double_as_longlong(hex[k]);
+            if (kb == kbest) {
                 atomicMin(hrow, (unsigned long long)(r0 + tid + k * NT));  // strict >: lowest row wins ties
+                atomicAdd(&ties[round & 1], 1ull);  // gap monitor: > 1 means a runner-up equal to the winner
+            } else {
+                atomicMax(&hkey2[round & 1], kb);  // gap monitor: the CTA's best below the winner
+            }
+        }
         __syncthreads();
         const unsigned long long rbest = *hrow;
         if (p.trace == (long long*)1 && round < 3 && tid < 64 && (remm & 1u))
@@ -637,7 +660,9 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
             const double sc = rbest != ~0ull ? __longlong_as_double((long long)kbest) : -1.0;
             const long long rw = rbest != ~0ull ? (long long)rbest : LLONG_MAX;
             st_async_v2(dst, __double_as_longlong(sc), (uint64_t)rw, mb);
-            st_async_v2(dst + 16, __double_as_longlong(cand_hdr->nb), 0ull, mb);
+            const unsigned long long k2 = ties[round & 1] > 1ull ? kbest : hkey2[round & 1];  // after the barrier above
+            st_async_v2(dst + 16, __double_as_longlong(cand_hdr->nb),
+                        (uint64_t)__double_as_longlong(k2 ? __longlong_as_double((long long)k2) : -1.0), mb);
         }
         for (int e = tid - 32; tid >= 32 && e < (int)C * (D / 4); e += NT - 32) {
             const int dst_rank = e / (D / 4), c4 = e % (D / 4);
@@ -647,6 +672,8 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         if (tid == 0) {  // reset the argmax atomics (next use is after >= 2 more barriers)
             *hkey = 0ull;
             *hrow = ~0ull;
+            hkey2[(round + 1) & 1] = 0ull;  // next round's; this round's may still be read above
+            ties[(round + 1) & 1] = 0ull;
         }
         mbar_wait(&mbar[1], ph2);
         ph2 ^= 1u;
@@ -662,6 +689,8 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
             const int ow = __shfl_xor_sync(0xffffffffu, w, o);
             if (os > bs || (os == bs && orow < br)) { bs = os; br = orow; w = ow; }
         }
+        if (rank == 0 && lane < (int)C && wid == 0 && p.gap_rec)  // gap monitor record (see below)
+            p.gap_rec[((int64_t)g * p.take + round) * MAXC + lane] = lane == w ? hdr[lane].second : hdr[lane].score;
         bw = bc + w * D;
         nbw = (float)hdr[w].nb;
         if (br >= r0 && br < r0 + nrows) {
@@ -677,6 +706,22 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
 
     // ---- sort the picks ascending by row (synapse.cpp:276-277) ----
     __syncthreads();
+    // ---- decision-gap monitor: per round, the runner-up is the winning CTA's second or
+    // another CTA's best (recorded above, a tie with the winner included); a row outside
+    // every CTA's window scores < winner - GAP_WINDOW (+ ~1e-15) ----
+    if (rank == 0 && p.gaps) {
+        for (int r = tid; r < p.take; r += NT) {
+            const double* rec = p.gap_rec + ((int64_t)g * p.take + r) * MAXC;
+            double b2 = -1.0;
+            for (int c = 0; c < (int)C; ++c) b2 = dmax_std(b2, rec[c]);
+            if (b2 >= 0.0) {
+                const double gap = dmin_std(__dsub_rn(pick_scores[r], b2), GAP_WINDOW);
+                atomicMin(min_gap, (unsigned long long)__double_as_longlong(gap));  // gap >= 0: bits order
+            }
+        }
+        __syncthreads();
+        if (tid == 0) p.gaps[g] = __longlong_as_double((long long)*min_gap);
+    }
     if (rank == 0) {
         int64_t* out_rows = p.out_rows + (int64_t)g * p.take;
         double* out_scores = p.out_scores + (int64_t)g * p.take;
@@ -786,7 +831,7 @@ int SEL_FN(wave)(int64_t L, int G) {
 
 bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
-                     cudaStream_t s) {
+                     double* gaps, double* gap_rec, cudaStream_t s) {
     if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 ||
         (reinterpret_cast<uintptr_t>(g.X) & 15) != 0 || g.L < 1)
         return false;
@@ -824,9 +869,11 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
                 gb.G = rem;
                 gb.X = g.X + (int64_t)full * g.gstride;
                 const int64_t o = (int64_t)full * take;
-                return SEL_FN(launch)(ga, attn, cen, take, lambda, flags, pick_rows, pick_scores, rows, scores, s) &&
+                return SEL_FN(launch)(ga, attn, cen, take, lambda, flags, pick_rows, pick_scores, rows, scores, gaps,
+                                      gap_rec, s) &&
                        SEL_FN(launch)(gb, attn + (int64_t)full * g.L, cen + (int64_t)full * D, take, lambda, flags,
-                                       pick_rows + o, pick_scores + o, rows + o, scores + o, s);
+                                       pick_rows + o, pick_scores + o, rows + o, scores + o,
+                                       gaps ? gaps + full : nullptr, gap_rec ? gap_rec + o * MAXC : nullptr, s);
             }
         }
     }
@@ -854,6 +901,8 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     prm.out_rows = rows;
     prm.out_scores = scores;
     prm.trace = nullptr;
+    prm.gaps = gap_rec ? gaps : nullptr;
+    prm.gap_rec = gap_rec;
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
     if (tr && tr[0] == 'p') prm.trace = (long long*)1;

@@ -815,6 +815,7 @@ void plan_select(ArenaPlan& p, const GroupView& g, int k) {
     p.take<double>((size_t)g.G * g.dim);        // centroids
     p.take<int64_t>((size_t)g.G * take);        // pick rows
     p.take<double>((size_t)g.G * take);         // pick scores
+    p.take<double>((size_t)g.G * take * kGapRecStride);  // gap-monitor records
 }
 
 void centroid_launch(const GroupView& g, double* cen, cudaStream_t s) {
@@ -842,14 +843,27 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     double* cen = ctx->arena.take<double>((size_t)g.G * g.dim);
     int64_t* pr = ctx->arena.take<int64_t>((size_t)g.G * take);
     double* ps = ctx->arena.take<double>((size_t)g.G * take);
+    double* grec = ctx->arena.take<double>((size_t)g.G * take * kGapRecStride);
 
     if (cen_in) cen = const_cast<double*>(cen_in);
     else centroid_launch(g, cen, s);
 
+    // decision-gap monitor output (cx_selection_gaps): one value per group, ctx-owned so it
+    // outlives the call's arena scratch
+    if (ctx->gaps_cap < g.G) {
+        if (ctx->gaps) CX_CUDA(cudaFree(ctx->gaps));
+        ctx->gaps = nullptr;
+        ctx->gaps_cap = 0;
+        CX_CUDA(cudaMalloc(&ctx->gaps, sizeof(double) * (size_t)g.G));
+        ctx->gaps_cap = g.G;
+    }
+    ctx->gaps_n = g.G;
     if (!(flags & CX_SELECT_GENERIC) &&
-        (select64_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, s) ||
-         select128_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, s)))
+        (select64_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s) ||
+         select128_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s)))
         return;
+    // the generic kernel does not monitor: NaN (all-ones bits) = not measured
+    CX_CUDA(cudaMemsetAsync(ctx->gaps, 0xFF, sizeof(double) * (size_t)g.G, s));
 
     SelectPlan pl = plan_select_shape(g);
     SelectParams prm;

@@ -231,5 +231,15 @@ def gate_decide(h: torch.Tensor, t: torch.Tensor, theta: float):
     return scores, acc.bool(), deg.bool()
 
 
+def selection_gaps(n_groups: int, device: int | None = None) -> torch.Tensor:
+    """Decision-gap monitor of the most recent selection on this device's ctx
+    (cx_selection_gaps): per group, the smallest top-1 / top-2 exact hybrid gap
+    over the greedy rounds, capped at 1e-10; NaN = not monitored."""
+    dev = torch.cuda.current_device() if device is None else device
+    out = torch.empty(n_groups, dtype=torch.float64, device=torch.device("cuda", dev))
+    check(lib.cx_selection_gaps(ctx(dev), int(n_groups), out.data_ptr(), _stream()), "selection_gaps")
+    return out
+
+
 def kernel_launch_count() -> int:
     return int(lib.cx_kernel_launch_count())

@@ -189,3 +189,28 @@ def test_gate_oracle_bitwise_vs_reference(orc, ref):
         with pytest.raises(oracle.OracleError) as e:
             be.gate_score(np.zeros(4, f), np.array([1, 0, 0, 0], f))
         assert e.value.code == 7  # degenerate_input_error
+
+
+def test_batched_decode_oracle_is_attend_per_q_head(orc, ref):
+    """orc_decode_attend_agents (the checker of the batched decode) == the
+    reference's own kernels::attend (n_heads = 1) called per (agent, layer,
+    q-head) over [synapse rows || private rows], bit for bit, on ragged tails
+    (empty tail included)."""
+    rs = np.random.default_rng(3)
+    N, Lr, H, Q, dk, k, tc = 5, 2, 2, 6, 16, 9, 7
+    sk = rs.standard_normal((Lr, H, k, dk), dtype=np.float32)
+    sv = rs.standard_normal((Lr, H, k, dk), dtype=np.float32)
+    tk = rs.standard_normal((N, Lr, H, tc, dk), dtype=np.float32)
+    tv = rs.standard_normal((N, Lr, H, tc, dk), dtype=np.float32)
+    tl = np.array([0, 7, 3, 1, 5], np.int32)
+    q = rs.standard_normal((N, Lr, Q, dk), dtype=np.float32)
+    got = orc.decode_attend(sk, sv, tk, tv, tl, q, n_threads=3)
+    back = ref if ref is not None else orc
+    for a in range(N):
+        for l in range(Lr):
+            for h in range(Q):
+                g = h // (Q // H)
+                kk = np.concatenate([sk[l, g], tk[a, l, g, :tl[a]]])
+                vv = np.concatenate([sv[l, g], tv[a, l, g, :tl[a]]])
+                exp = back.attend(q[a, l, h], kk, vv, k + int(tl[a]), 1, dk)
+                assert got[a, l, h].tobytes() == exp.tobytes(), (a, l, h)
