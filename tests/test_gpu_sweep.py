@@ -54,6 +54,7 @@ def test_grouped_compress_random_sweep(dev, orc, seed):
     vt = torch.from_numpy(np.stack(vs)).cuda()
     qt = torch.from_numpy(np.stack(qs)).cuda()
     rows, scores, sk, sv = dev.compress_grouped(kt, vt, qt, k, lam)
+    gaps = dev.selection_gaps(G).cpu().numpy()
     a = dev.attention_grouped(kt, qt)
     torch.cuda.synchronize()
     rows, scores = rows.cpu().numpy(), scores.cpu().numpy()
@@ -63,13 +64,19 @@ def test_grouped_compress_random_sweep(dev, orc, seed):
         assert rows[gi].tobytes() == idx.tobytes(), (seed, gi, d, L, k, lam)
         assert scores[gi].tobytes() == sc.tobytes(), (seed, gi)
         assert np.array_equal(sk[gi], ks[gi][idx]) and np.array_equal(sv[gi], vs[gi][idx])
-        # end to end on unperturbed N(0,1) data: the oracle's own attention gives the same index
-        # set (the decision gaps dwarf the last-ulp exp differences); the
-        # artificial near-duplicate clusters above may create genuine near-ties, so not there
-        if seed % 3 != 0:
+        # end to end: the oracle's own attention gives the same index set whenever the
+        # decision-gap monitor certifies it (every round's top-1 / top-2 gap > 1e-11, far above
+        # the attention's last-ulp exp differences), which includes the near-duplicate
+        # clusters above; on unmonitored (generic-dim) groups only unperturbed N(0,1) data
+        # is checked end to end (its gaps dwarf the exp noise)
+        certified = bool(gaps[gi] > 1e-11)
+        if certified or (np.isnan(gaps[gi]) and seed % 3 != 0):
             a_ref = oracle.group_attention(orc, ks[gi], qs[gi])
             idx_ref, _ = orc.select_landmarks_points(ks[gi], a_ref, k, lam)
-            assert np.array_equal(rows[gi], idx_ref), (seed, gi)
+            assert np.array_equal(rows[gi], idx_ref), (seed, gi, float(gaps[gi]))
+        elif d in (64, 128):
+            # monitored and NOT certified: only exact ties from the duplicated rows may do that
+            assert seed % 3 == 0 and gaps[gi] == 0.0, (seed, gi, float(gaps[gi]))
 
 
 @pytest.mark.parametrize("seed", list(range(12)))
