@@ -144,6 +144,23 @@ cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* a
                                 int k, double lambda, unsigned flags,
                                 int64_t* out_rows, double* out_scores, void* stream);
 
+/* Path pinning for tests and tuning (defaults: the cost models).  Options are
+ * per context and read at launch time; they never change results (every
+ * pinned path is bit-exact / within tolerance like the default), only which
+ * kernel configuration computes them.  CX_INVALID_ARGUMENT for an unknown
+ * option or out-of-range value. */
+#define CX_OPT_SELECT_CLUSTER 1     /* selection cluster size 1..16; 0 = cost model */
+#define CX_OPT_SELECT_NO_SKETCH 2   /* 1 = never keep rows as the fp16 sketch */
+#define CX_OPT_DECODE_IMPL 3        /* CX_DECODE_* below */
+#define CX_OPT_DECODE_CTAS_PER_LH 4 /* tcgen05 decode CTAs per (layer, KV head); 0 = auto */
+#define CX_OPT_HOST_UPLOAD_VALUES 5 /* 1 = host path uploads all values even if pinned */
+#define CX_DECODE_AUTO 0            /* tcgen05, then v2, then the generic kernel */
+#define CX_DECODE_TC 1              /* pinned: an error if the shape does not apply */
+#define CX_DECODE_V2 2
+#define CX_DECODE_V1 3
+cx_status cx_ctx_set_option(cx_ctx* ctx, int option, int64_t value);
+cx_status cx_ctx_get_option(cx_ctx* ctx, int option, int64_t* value);
+
 /* Decision-gap monitor (SURVEY.md §7 "per-round gap monitor").  Writes, for
  * each of the n_groups groups of this ctx's most recent selection launch (the
  * last cx_select_grouped_dev / cx_compress_grouped_dev call, or the last chunk
@@ -205,7 +222,28 @@ typedef struct cx_decode_batch {
     float* out;                /* [N][n_layers][n_q][d_k] */
 } cx_decode_batch;
 
+/* Stream-ordered: never synchronizes.  Precondition per agent (the reference
+ * KvCache's capacity check, model.cpp:124-140): 0 <= tail_len[a] <= t_cap - 1
+ * when new_keys is set (room for the appended row), <= t_cap otherwise.  The
+ * kernels check it on the device: an agent outside it sets
+ * CX_DEVERR_TAIL_RANGE (cx_ctx_device_errors), appends nothing, and attends
+ * over its rows clamped to that range (its outputs are then unspecified);
+ * no write ever leaves the agent's own tail. */
 cx_status cx_decode_step_dev(cx_ctx* ctx, const cx_decode_batch* b, void* stream);
+
+/* Device-detected precondition failures of the stream-ordered *_dev calls
+ * on this ctx (a bitmask, accumulated since the last clear): the reference
+ * throws for these, a device kernel can only record them.  Synchronizes
+ * `stream` (the stream the checked calls ran on), then writes the mask and,
+ * if clear != 0, resets it.
+ *   CX_DEVERR_NONFINITE   a non-finite attention score (kernels.cpp:70; the
+ *                         reference's precondition_error)
+ *   CX_DEVERR_TAIL_RANGE  a decode tail_len outside its range (above)
+ * A ctx is meant to be driven from one stream at a time: its scratch arena,
+ * side stream and this flag are shared by all of its *_dev calls. */
+#define CX_DEVERR_NONFINITE 1u
+#define CX_DEVERR_TAIL_RANGE 2u
+cx_status cx_ctx_device_errors(cx_ctx* ctx, void* stream, unsigned* flags, int clear);
 
 /* gate.hpp:26 / gate.cpp:45-61 decide(h_main, t_side, theta) for n_pairs (row h[i], row t[i])
  * device pairs (row strides in floats): scores[i] (NaN when degenerate), accepted[i] =

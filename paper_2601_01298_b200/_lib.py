@@ -88,6 +88,9 @@ _SIGS = [
      [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp]),
     ("cx_gather_grouped_dev", C.c_int, [c_vp, C.POINTER(CxGroups), c_vp, c_vp, C.c_int, c_vp, c_vp]),
     ("cx_selection_gaps", C.c_int, [c_vp, C.c_int, c_vp, c_vp]),
+    ("cx_ctx_set_option", C.c_int, [c_vp, C.c_int, C.c_int64]),
+    ("cx_ctx_device_errors", C.c_int, [c_vp, c_vp, C.POINTER(C.c_uint), C.c_int]),
+    ("cx_ctx_get_option", C.c_int, [c_vp, C.c_int, C.POINTER(C.c_int64)]),
     ("cx_compress_grouped_dev", C.c_int,
      [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp, c_vp, c_vp]),
     ("cx_decode_step_dev", C.c_int, [c_vp, C.POINTER(CxDecodeBatch), c_vp]),

@@ -105,8 +105,9 @@ __host__ __device__ inline DecodeSmem decode_layout(int k_syn, int t_rows, int d
 }
 
 __global__ void __launch_bounds__(256) decode_step_kernel(cx_decode_batch b, int apb, int agents_per_cta,
-                                                         float inv_sqrt_dk) {
+                                                         float inv_sqrt_dk, int* flag) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int tlen_s[8];  // rows each agent of the batch attends (apb <= 8)
     const int qpg = b.n_q / b.n_kv;
     const int lh = blockIdx.x;
     const int l = lh / b.n_kv, g = lh % b.n_kv;
@@ -142,7 +143,13 @@ __global__ void __launch_bounds__(256) decode_step_kernel(cx_decode_batch b, int
         for (int s = 0; s < apb; ++s) {
             const int a = a0 + s;
             if (a >= a_end) break;
-            const int len = min(b.tail_len[a], b.t_cap - (b.new_keys ? 1 : 0));
+            int len = __ldg(b.tail_len + a);  // validated like decode_tc (FLAG_TAIL_RANGE)
+            const bool len_ok = len >= 0 && len <= b.t_cap - (b.new_keys ? 1 : 0);
+            if (!len_ok) {
+                if (tid == 0) atomicOr(flag, FLAG_TAIL_RANGE);
+                len = len < 0 ? 0 : b.t_cap - (b.new_keys ? 1 : 0);
+            }
+            if (tid == 0) tlen_s[s] = len_ok ? len + (b.new_keys ? 1 : 0) : len;  // rows attended
             const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * dk;
             float* tk = Tk + (size_t)s * t_rows * pitch;
             float* tv = Tv + (size_t)s * t_rows * pitch;
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(256) decode_step_kernel(cx_decode_batch b, int
                 tk[j * pitch + c] = __ldg(b.tail_keys + toff + e);
                 tv[j * pitch + c] = __ldg(b.tail_values + toff + e);
             }
-            if (b.new_keys) {
+            if (b.new_keys && len_ok) {
                 const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * dk;
                 for (int c = tid; c < dk; c += nt) {
                     const float nk = __ldg(b.new_keys + noff + c), nv = __ldg(b.new_values + noff + c);
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(256) decode_step_kernel(cx_decode_batch b, int
         const int a = a0 + a_slot;
         if (a < a_end) {
             const int h = g * qpg + hh;
-            const int tn = min(b.tail_len[a], b.t_cap - (b.new_keys ? 1 : 0)) + (b.new_keys ? 1 : 0);
+            const int tn = tlen_s[a_slot];
             const int n = b.k_syn + tn;
             const size_t qoff = (((size_t)a * b.n_layers + l) * b.n_q + h) * dk;
             float* qv = Qv + (size_t)warp * dk;
@@ -250,7 +257,7 @@ __host__ __device__ inline DecodeV2Smem decode_v2_layout(int k_syn, int t_cap) {
 
 template <int QPG>
 __global__ void __launch_bounds__(DV2_WARPS * 32, 1) decode_v2_kernel(cx_decode_batch b, int agents_per_cta,
-                                                                    float scale) {
+                                                                    float scale, int* flag) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DecodeV2Smem lay = decode_v2_layout(b.k_syn, b.t_cap);
     float* Ks = reinterpret_cast<float*>(smem + lay.ks);
@@ -274,9 +281,15 @@ __global__ void __launch_bounds__(DV2_WARPS * 32, 1) decode_v2_kernel(cx_decode_
 
     const int a_begin = blockIdx.y * agents_per_cta;
     const int a_end = min(b.n_agents, a_begin + agents_per_cta);
-    const bool app = b.new_keys != nullptr;
+    const bool app_all = b.new_keys != nullptr;
     for (int a = a_begin + warp; a < a_end; a += DV2_WARPS) {
-        const int len = min(b.tail_len[a], b.t_cap - (app ? 1 : 0));
+        int len = __ldg(b.tail_len + a);  // validated like decode_tc (FLAG_TAIL_RANGE)
+        const bool len_ok = len >= 0 && len <= b.t_cap - (app_all ? 1 : 0);
+        if (!len_ok) {
+            if (lane == 0) atomicOr(flag, FLAG_TAIL_RANGE);
+            len = len < 0 ? 0 : b.t_cap - (app_all ? 1 : 0);
+        }
+        const bool app = app_all && len_ok;
         const int nt = len + (app ? 1 : 0);
         const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * DV2_DK;
         const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * DV2_DK;
@@ -506,23 +519,23 @@ static bool launch_decode_v2(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t
     chunks = std::min(chunks, (b.n_agents + DV2_WARPS - 1) / DV2_WARPS);
     chunks = std::max(chunks, 1);
     const int per = (b.n_agents + chunks - 1) / chunks;
-    CX_CUDA(cudaFuncSetAttribute(decode_v2_kernel<QPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    kernel_smem(decode_v2_kernel<QPG>, lay.total);
     decode_v2_kernel<QPG><<<dim3((unsigned)n_lh, (unsigned)chunks), DV2_WARPS * 32, lay.total, s>>>(
-        b, per, (float)(1.0 / std::sqrt((double)b.d_k)));
+        b, per, (float)(1.0 / std::sqrt((double)b.d_k)), ctx->d_flag);
     check_launch("decode_v2_kernel");
     return true;
 }
 
 void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int qpg = b.n_q / b.n_kv;
-    // CX_DECODE=tc|v2|v1 pins an implementation (testing; a pinned kernel that does
-    // not apply to the shape is an error, not a silent fallback).  Default: the
-    // tcgen05 kernel (decode_tc.cu), then v2 (CUDA cores), then the generic v1.
-    const char* pin = getenv("CX_DECODE");
-    const bool allow_tc = !pin || !strcmp(pin, "tc");
-    const bool allow_v2 = !pin || !strcmp(pin, "v2");
+    // CX_OPT_DECODE_IMPL pins an implementation (tests; a pinned kernel that does not
+    // apply to the shape is an error, not a silent fallback).  Default: the tcgen05
+    // kernel (decode_tc.cu), then v2 (CUDA cores), then the generic v1.
+    const int pin = ctx->opt.decode_impl;
+    const bool allow_tc = pin == CX_DECODE_AUTO || pin == CX_DECODE_TC;
+    const bool allow_v2 = pin == CX_DECODE_AUTO || pin == CX_DECODE_V2;
     if (allow_tc && decode_tc_launch(ctx, b, s)) return;
-    if (pin && !strcmp(pin, "tc")) fail(CX_PRECONDITION_ERROR, "decode_step: CX_DECODE=tc does not apply to this shape");
+    if (pin == CX_DECODE_TC) fail(CX_PRECONDITION_ERROR, "decode_step: the pinned tcgen05 kernel does not apply to this shape");
     auto al = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
     const bool v2_aligned = al(b.syn_keys, 16) && al(b.syn_values, 16) && al(b.q, 16) && al(b.tail_keys, 16) &&
                             al(b.tail_values, 16) && al(b.new_keys, 16) && al(b.new_values, 16) && al(b.out, 8);
@@ -538,7 +551,7 @@ void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
         }
         if (done) return;
     }
-    if (pin && !strcmp(pin, "v2")) fail(CX_PRECONDITION_ERROR, "decode_step: CX_DECODE=v2 does not apply to this shape");
+    if (pin == CX_DECODE_V2) fail(CX_PRECONDITION_ERROR, "decode_step: the pinned v2 kernel does not apply to this shape");
     int apb = std::max(1, 8 / qpg);
     const int warps = apb * qpg;
     const int t_rows = b.t_cap + 1;
@@ -558,9 +571,9 @@ void decode_step(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     int per = (b.n_agents + chunks - 1) / chunks;
     per = ((per + apb - 1) / apb) * apb;
     chunks = (b.n_agents + per - 1) / per;
-    CX_CUDA(cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    kernel_smem(decode_step_kernel, lay.total);
     decode_step_kernel<<<dim3((unsigned)n_lh, (unsigned)chunks), warps * 32, lay.total, s>>>(
-        b, apb, per, (float)(1.0 / std::sqrt((double)b.d_k)));
+        b, apb, per, (float)(1.0 / std::sqrt((double)b.d_k)), ctx->d_flag);
     check_launch("decode_step_kernel");
 }
 

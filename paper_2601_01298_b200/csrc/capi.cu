@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <map>
 #include <memory>
 
 #include "cx_internal.cuh"
@@ -18,6 +19,32 @@ namespace cx {
 std::atomic<uint64_t> g_launches{0};
 static thread_local std::string t_last_error;
 void set_last_error(const std::string& m) { t_last_error = m; }
+
+void kernel_smem_attr(const void* fn, size_t bytes, bool nonportable_cluster) {
+    struct Key {
+        const void* fn;
+        int dev;
+        bool operator<(const Key& o) const { return fn != o.fn ? fn < o.fn : dev < o.dev; }
+    };
+    struct Set {
+        size_t bytes = 0;
+        bool nonportable = false;
+    };
+    static std::mutex mu;
+    static std::map<Key, Set> done;  // attributes already set per (kernel, device)
+    int dev = 0;
+    CX_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    Set& st = done[{fn, dev}];
+    if (st.bytes < bytes) {
+        CX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        st.bytes = bytes;
+    }
+    if (nonportable_cluster && !st.nonportable) {
+        CX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        st.nonportable = true;
+    }
+}
 
 namespace {
 
@@ -519,6 +546,51 @@ extern "C" cx_status cx_select_grouped_dev(cx_ctx* c, const cx_groups* gr, const
     });
 }
 
+extern "C" cx_status cx_ctx_set_option(cx_ctx* c, int option, int64_t value) {
+    return guard([&] {
+        if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
+        auto in = [&](int64_t lo, int64_t hi) {
+            if (value < lo || value > hi) fail(CX_INVALID_ARGUMENT, "ctx_set_option: value out of range");
+            return (int)value;
+        };
+        switch (option) {
+            case CX_OPT_SELECT_CLUSTER: c->opt.select_cluster = in(0, 16); break;
+            case CX_OPT_SELECT_NO_SKETCH: c->opt.select_no_sketch = in(0, 1); break;
+            case CX_OPT_DECODE_IMPL: c->opt.decode_impl = in(CX_DECODE_AUTO, CX_DECODE_V1); break;
+            case CX_OPT_DECODE_CTAS_PER_LH: c->opt.decode_ctas_per_lh = in(0, 1 << 16); break;
+            case CX_OPT_HOST_UPLOAD_VALUES: c->opt.host_upload_values = in(0, 1); break;
+            default: fail(CX_INVALID_ARGUMENT, "ctx_set_option: unknown option");
+        }
+        if (c->aux) c->aux->opt = c->opt;  // the host path's prologue context follows
+    });
+}
+
+extern "C" cx_status cx_ctx_get_option(cx_ctx* c, int option, int64_t* value) {
+    return guard([&] {
+        if (!c || !value) fail(CX_INVALID_ARGUMENT, "null ctx/value");
+        switch (option) {
+            case CX_OPT_SELECT_CLUSTER: *value = c->opt.select_cluster; break;
+            case CX_OPT_SELECT_NO_SKETCH: *value = c->opt.select_no_sketch; break;
+            case CX_OPT_DECODE_IMPL: *value = c->opt.decode_impl; break;
+            case CX_OPT_DECODE_CTAS_PER_LH: *value = c->opt.decode_ctas_per_lh; break;
+            case CX_OPT_HOST_UPLOAD_VALUES: *value = c->opt.host_upload_values; break;
+            default: fail(CX_INVALID_ARGUMENT, "ctx_get_option: unknown option");
+        }
+    });
+}
+
+extern "C" cx_status cx_ctx_device_errors(cx_ctx* c, void* stream, unsigned* flags, int clear) {
+    return guard([&] {
+        if (!c || !flags) fail(CX_INVALID_ARGUMENT, "null ctx/flags");
+        int f = 0;
+        cudaStream_t s = (cudaStream_t)stream;
+        CX_CUDA(cudaMemcpyAsync(&f, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        if (clear) CX_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+        CX_CUDA(cudaStreamSynchronize(s));
+        *flags = (unsigned)f;
+    });
+}
+
 extern "C" cx_status cx_selection_gaps(cx_ctx* c, int n_groups, double* out, void* stream) {
     return guard([&] {
         if (!c || !out) fail(CX_INVALID_ARGUMENT, "null ctx/out");
@@ -622,7 +694,7 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         {
             cudaPointerAttributes pa{};
             if (cudaPointerGetAttributes(&pa, values) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-                pa.devicePointer != nullptr && !getenv("CX_HOST_UPLOAD_VALUES"))
+                pa.devicePointer != nullptr && !c->opt.host_upload_values)
                 vdev = reinterpret_cast<const float*>(pa.devicePointer);
             cudaGetLastError();
         }
@@ -659,7 +731,12 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         const int w = dim == 64 ? select64_wave(count, n_groups) : 0;
         const int WAVE = w > 0 ? w : 15;
         std::vector<int> start;
-        if (const char* ch = getenv("CX_E2E_CHUNKS")) {  // tuning only: explicit chunk sizes "a,b,c"
+#ifdef CX_EXPERIMENTS
+        const char* ch = getenv("CX_E2E_CHUNKS");  // tuning only: explicit chunk sizes "a,b,c"
+#else
+        const char* ch = nullptr;
+#endif
+        if (ch) {
             int g0 = 0;
             for (const char* q = ch; *q && g0 < n_groups;) {
                 const int n = std::max(1, atoi(q));
@@ -697,6 +774,7 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
             c->aux = a;
         }
         cx_ctx* x = c->aux;
+        x->opt = c->opt;
         {
             int maxg = 0;
             for (int i = 0; i < nch; ++i) maxg = std::max(maxg, start[i + 1] - start[i]);
@@ -793,9 +871,24 @@ struct cx_kvcache {
     bool entry_open = false;
     int layers_written = 0;
     cudaStream_t stream = nullptr;  // ordering for all of this cache's device work
+    cudaEvent_t ev = nullptr;       // cross-stream ordering with appends on caller streams
 };
 
 namespace {
+
+// Appends may run on a caller stream s.  Before: s waits for the cache's own pending work
+// (a regrow's copies).  After: the cache's stream waits for s, so a later regrow, read or
+// selection (all on c->stream) is ordered after the append.
+void kv_before(cx_kvcache* c, cudaStream_t s) {
+    if (s == c->stream) return;
+    CX_CUDA(cudaEventRecord(c->ev, c->stream));
+    CX_CUDA(cudaStreamWaitEvent(s, c->ev, 0));
+}
+void kv_after(cx_kvcache* c, cudaStream_t s) {
+    if (s == c->stream) return;
+    CX_CUDA(cudaEventRecord(c->ev, s));
+    CX_CUDA(cudaStreamWaitEvent(c->stream, c->ev, 0));
+}
 
 void kv_grow(cx_kvcache* c, int64_t need) {
     if (need <= c->capacity) return;
@@ -861,6 +954,7 @@ extern "C" cx_status cx_kvcache_create(int n_layers, int n_heads, int d_model, i
         c->max_positions = max_positions;
         try {
             CX_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            CX_CUDA(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
             kv_grow(c, std::max<int64_t>(1, capacity));
         } catch (...) {
             delete c;
@@ -876,6 +970,7 @@ extern "C" cx_status cx_kvcache_destroy(cx_kvcache* c) {
         cudaStreamSynchronize(c->stream);
         if (c->keys) cudaFree(c->keys);
         if (c->values) cudaFree(c->values);
+        if (c->ev) cudaEventDestroy(c->ev);
         cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -977,13 +1072,7 @@ extern "C" cx_status cx_kvcache_append_context_dev(cx_kvcache* c, const float* k
             cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
             const int64_t row0 = (int64_t)c->positions.size();
             kv_grow(c, row0 + n_ok);
-            if (s != c->stream) {  // order after the cache's own pending work (e.g. a regrow)
-                cudaEvent_t ev;
-                CX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                CX_CUDA(cudaEventRecord(ev, c->stream));
-                CX_CUDA(cudaStreamWaitEvent(s, ev, 0));
-                cudaEventDestroy(ev);
-            }
+            kv_before(c, s);
             if (n_ok == count) {  // the whole block: one launch for all layers
                 kv_append_rows(c->keys, c->values, c->capacity, c->n_layers, c->d_model, keys, values, n_ok, row0, s);
             } else {
@@ -993,6 +1082,7 @@ extern "C" cx_status cx_kvcache_append_context_dev(cx_kvcache* c, const float* k
                                    keys + (size_t)l * count * c->d_model, values + (size_t)l * count * c->d_model,
                                    n_ok, row0, s);
             }
+            kv_after(c, s);
             for (int64_t t = 0; t < n_ok; ++t) {
                 c->positions.push_back(base_position + t);
                 c->origins.push_back((uint8_t)CX_ORIGIN_CONTEXT);
@@ -1047,6 +1137,7 @@ void inject_apply(cx_kvcache* c, const float* dk, const float* dv, int64_t block
                   cudaStream_t s) {
     const int64_t row0 = (int64_t)c->positions.size();
     kv_grow(c, row0 + n_ok);
+    kv_before(c, s);
     // copy tokens [0, n_ok) of every layer: block layout [layer][block_T][d_model]
     if (n_ok == block_T) {
         kv_append_rows(c->keys, c->values, c->capacity, c->n_layers, c->d_model, dk, dv, n_ok, row0, s);
@@ -1056,6 +1147,7 @@ void inject_apply(cx_kvcache* c, const float* dk, const float* dv, int64_t block
                            c->values + (size_t)l * c->capacity * c->d_model, c->capacity, 1, c->d_model,
                            dk + (size_t)l * block_T * c->d_model, dv + (size_t)l * block_T * c->d_model, n_ok, row0, s);
     }
+    kv_after(c, s);
     for (int64_t t = 0; t < n_ok; ++t) {
         c->positions.push_back(base + t);
         c->origins.push_back((uint8_t)CX_ORIGIN_INJECTED);
@@ -1107,13 +1199,6 @@ extern "C" cx_status cx_inject_dev(cx_kvcache* c, const float* keys, const float
         if (n_ok > 0) {
             if (!keys || !values) fail(CX_INVALID_ARGUMENT, "null block");
             cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-            if (s != c->stream) {  // order after the cache's own pending work
-                cudaEvent_t ev;
-                CX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                CX_CUDA(cudaEventRecord(ev, c->stream));
-                CX_CUDA(cudaStreamWaitEvent(s, ev, 0));
-                cudaEventDestroy(ev);
-            }
             inject_apply(c, keys, values, token_count, n_ok, base_position, s);
         }
         if (err != CX_OK) fail(err, msg);

@@ -42,6 +42,23 @@ inline void check_launch(const char* what) {
 
 void set_last_error(const std::string& m);
 
+// Raises a kernel's dynamic shared memory limit (and, for clusters > 8, allows the
+// non-portable size) once per (kernel, device) and size, not on every launch.
+void kernel_smem_attr(const void* fn, size_t bytes, bool nonportable_cluster = false);
+template <class K>
+inline void kernel_smem(K* fn, size_t bytes, bool nonportable_cluster = false) {
+    kernel_smem_attr(reinterpret_cast<const void*>(fn), bytes, nonportable_cluster);
+}
+
+// Path pinning for tests and tuning (cx_ctx_set_option; defaults = the cost models).
+struct Options {
+    int select_cluster = 0;      // CX_OPT_SELECT_CLUSTER: force the selection cluster size (0 = cost model)
+    int select_no_sketch = 0;    // CX_OPT_SELECT_NO_SKETCH: never use the fp16 sketch row mode
+    int decode_impl = 0;         // CX_OPT_DECODE_IMPL: CX_DECODE_{AUTO,TC,V2,V1}
+    int decode_ctas_per_lh = 0;  // CX_OPT_DECODE_CTAS_PER_LH: tcgen05 decode CTAs per (layer, KV head) (0 = auto)
+    int host_upload_values = 0;  // CX_OPT_HOST_UPLOAD_VALUES: host path uploads all values even when pinned
+};
+
 // Runs f, mapping exceptions to cx_status (the C boundary).
 template <class F>
 cx_status guard(F&& f) {
@@ -113,6 +130,7 @@ struct cx_ctx {
     double* gaps = nullptr;         // decision-gap monitor: [gaps_n] of the last selection (device)
     int gaps_cap = 0, gaps_n = 0;
     int num_sms = 0;
+    cx::Options opt;                // cx_ctx_set_option
     std::mutex mu;
 };
 
@@ -122,7 +140,11 @@ namespace cx {
 cx_ctx* default_ctx();
 
 // Device error flags written by kernels (bitmask in ctx->d_flag).
-enum : int { FLAG_NONFINITE = 1 };
+enum : int {
+    FLAG_NONFINITE = 1,    // CX_DEVERR_NONFINITE: a non-finite attention score (softmax precondition)
+    FLAG_TAIL_RANGE = 2,   // CX_DEVERR_TAIL_RANGE: decode tail_len outside [0, t_cap - append]
+};
+static_assert(FLAG_NONFINITE == CX_DEVERR_NONFINITE && FLAG_TAIL_RANGE == CX_DEVERR_TAIL_RANGE, "flag bits");
 
 // ---- launch helpers implemented in the .cu files ----------------------------
 struct GroupView {  // device-side view of cx_groups
@@ -147,8 +169,8 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
                     unsigned flags, int64_t* rows, double* scores, cudaStream_t s,
                     const double* centroids = nullptr /* [G][dim], computed here when null */);
 // d = 128 instantiation (select128.cu): the reference-mode cloud of a 2-head MHA cache
-bool select128_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
-                      unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
+bool select128_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
+                      double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                       double* gaps, double* gap_rec, cudaStream_t s);
 int select128_wave(int64_t L, int G);
 // gate.cpp:27-61 for n (h, t) pairs (row strides in floats): score (NaN when degenerate),
@@ -161,8 +183,8 @@ int select64_wave(int64_t L, int G);
 void centroid_launch(const GroupView& g, double* cen, cudaStream_t s);
 void plan_select(ArenaPlan& p, const GroupView& g, int k);
 // dim-64 fast path (select64.cu); false when it does not apply
-bool select64_launch(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
-                     unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
+bool select64_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
+                     double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                      double* gaps, double* gap_rec, cudaStream_t s);
 
 // gather selected rows from a (values or keys) tensor with the group addressing.

@@ -263,17 +263,27 @@ __host__ __device__ inline TcLayout tc_layout(int k_syn, int qpg) {
     return L;
 }
 
+#ifdef CX_EXPERIMENTS
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 
-// trc (CX_TC_TRACE=1, debugging only): phase timestamps of CTA (0, 0)
+// build-time debugging only (CX_NVCC_EXTRA=-DCX_EXPERIMENTS): trc (CX_TC_TRACE=1) = phase
+// timestamps of CTA (0, 0); skip (CX_TC_SKIP=1|2) = skip one role's math (timing only:
+// the outputs are NOT valid then).  The release library compiles both out.
 #define TC_TRACE(slot)                                                                  \
     do {                                                                                \
         if (trc && blockIdx.x == 0 && blockIdx.y == 0) trc[(slot)] = gtime();            \
     } while (0)
+#define TC_SKIP(bit) (skip & (bit))
+#else
+#define TC_TRACE(slot) \
+    do {               \
+    } while (0)
+#define TC_SKIP(bit) false
+#endif
 
 // ---- private-row helpers (warp per agent) ----
 // L1PF: private rows go through L1 (ld.global.nc) and each 16-row batch is
@@ -389,7 +399,7 @@ __device__ __forceinline__ void mix_rows(const float* tv, int r0, int nt, const 
 
 template <int QPG>
 __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch b, float scale,
-                                                                 unsigned long long* trc, int skip) {
+                                                                 int* flag, unsigned long long* trc, int skip) {
     extern __shared__ __align__(1024) unsigned char smem[];
     if (threadIdx.x == 0) TC_TRACE(1001);  // kernel start (debugging only)
     const TcLayout lay = tc_layout(b.k_syn, QPG);
@@ -536,7 +546,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             }
         };
         // the first tile's scores are issued before the loop; tile i+1's while tile i's P.V runs
-        if (!(skip & 1) && (int)blockIdx.y < n_tiles) {
+        if (!TC_SKIP(1) && (int)blockIdx.y < n_tiles) {
             stage_q(blockIdx.y);
             issue_s();
         }
@@ -572,7 +582,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             const int a0 = tile * AT;
             const int rows = min(AT, b.n_agents - a0) * QPG;
             const int next = tile + (int)gridDim.y;
-            if (skip & 1) {  // debugging only (CX_TC_SKIP): keep the hand-off protocol, skip the math
+            if (TC_SKIP(1)) {  // debugging only (CX_TC_SKIP): keep the hand-off protocol, skip the math
                 mbar_wait_sleep(&mbar[2 + tpar], (uint32_t)(ti >> 1) & 1u);
                 bar_sync(1, SWARPS * 32);
                 if (tid == 0) *epi_done = ti + 1;
@@ -724,10 +734,19 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
             // tile: with 18 agents per tile and 12 warps no warp takes 2 every tile
             const int first = (pw - (ti * AT) % PWARPS + PWARPS) % PWARPS;
             for (int ai = first; ai < na; ai += PWARPS) {
-                if (skip & 2) continue;  // debugging only (CX_TC_SKIP)
+                if (TC_SKIP(2)) continue;  // debugging only (CX_TC_SKIP)
                 const int a = a0 + ai;
-                const int len = min(b.tail_len[a], b.t_cap - (app ? 1 : 0));
-                const int nt = len + (app ? 1 : 0);
+                // stored rows, validated (model.cpp:124-140 capacity check): out of range ->
+                // FLAG_TAIL_RANGE, the agent's rows clamped and nothing appended
+                int len = __ldg(b.tail_len + a);
+                const int cap = b.t_cap - (app ? 1 : 0);
+                const bool len_ok = len >= 0 && len <= cap;
+                if (!len_ok) {
+                    if (lane == 0) atomicOr(flag, FLAG_TAIL_RANGE);
+                    len = len < 0 ? 0 : cap;
+                }
+                const bool appa = app && len_ok;  // this agent appends its new token
+                const int nt = len + (appa ? 1 : 0);
                 const size_t toff = ((((size_t)a * b.n_layers + l) * b.n_kv + g) * b.t_cap) * TD;
                 const size_t noff = (((size_t)a * b.n_layers + l) * b.n_kv + g) * TD;
                 const float* tk = b.tail_keys + toff;
@@ -742,7 +761,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 }
                 float4 nka = make_float4(0.f, 0.f, 0.f, 0.f), nkb = nka;
                 float2 nvv = make_float2(0.f, 0.f);
-                if (app) {
+                if (appa) {
                     ld_row8(b.new_keys + noff + 8 * (lane & 7), nka, nkb);
                     nvv = __ldg(reinterpret_cast<const float2*>(b.new_values + noff) + lane);
                 }  // (appended at the end of the agent: a store here would hold back every load below)
@@ -758,7 +777,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     score_rows<QPG, PB / 4, false>(tk, r0, len, qa, qb, Sw, lane, scale);
                 }
                 for (; r0 < len; r0 += 4) score_rows<QPG, 1, true>(tk, r0, len, qa, qb, Sw, lane, scale);
-                if (app) score_group<QPG>(nka, nkb, len, lane < 8, qa, qb, Sw, lane, scale);
+                if (appa) score_group<QPG>(nka, nkb, len, lane < 8, qa, qb, Sw, lane, scale);
                 if (pw == 0 && lane == 0) TC_TRACE(ti * 16 + (ai == first ? 9 : 12));
                 __syncwarp();
                 // this tile's (Mp, Lp, O_priv) buffers were last read by the epilogue two
@@ -825,7 +844,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     mix_rows<QPG, PB, false>(tv, r0, len, Sw, o, lane);
                 }
                 for (; r0 < len; r0 += 4) mix_rows<QPG, 4, true>(tv, r0, len, Sw, o, lane);
-                if (app)
+                if (appa)
 #pragma unroll
                     for (int h = 0; h < QPG; ++h) {
                         const float p = Sw[h * SST + len];
@@ -842,7 +861,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                     const int r = ai * QPG + h;
                     reinterpret_cast<float2*>(Op + ((size_t)(OP_BUFS == 2 ? tpar : 0) * TM + r) * OPS)[lane] = o[h];
                 }
-                if (app) {  // the fused append of the new token's K/V (row len; never read above)
+                if (appa) {  // the fused append of the new token's K/V (row len; never read above)
                     if (lane < 8) {
                         reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[2 * lane] = nka;
                         reinterpret_cast<float4*>(b.tail_keys + toff + (size_t)len * TD)[2 * lane + 1] = nkb;
@@ -884,7 +903,7 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
         cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     }
     if (lay.total > (size_t)max_optin) return false;
-    void (*kern)(cx_decode_batch, float, unsigned long long*, int) = nullptr;
+    void (*kern)(cx_decode_batch, float, int*, unsigned long long*, int) = nullptr;
     switch (qpg) {
         case 1: kern = decode_tc_kernel<1>; break;
         case 2: kern = decode_tc_kernel<2>; break;
@@ -899,19 +918,23 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     const int sms = ctx->num_sms > 0 ? ctx->num_sms : 148;
     // one resident CTA per SM: fill the SMs in a single wave
     int per_lh = std::max(1, std::min(n_tiles, sms / n_lh));
-    if (const char* f = getenv("CX_TC_PER_LH")) per_lh = std::max(1, std::min(n_tiles, atoi(f)));  // tuning only
-    // debugging only (CX_TC_SMEM_PAD=bytes): reserve extra shared memory, i.e. shrink the L1
-    // carveout, to measure how the private-row stream depends on L1 capacity
-    const size_t smem = lay.total + (getenv("CX_TC_SMEM_PAD") ? (size_t)atol(getenv("CX_TC_SMEM_PAD")) : 0);
+    if (ctx->opt.decode_ctas_per_lh > 0) per_lh = std::max(1, std::min(n_tiles, ctx->opt.decode_ctas_per_lh));
+    size_t smem = lay.total;
+    unsigned long long* trc_arg = nullptr;
+    int skip = 0;
+#ifdef CX_EXPERIMENTS
+    // CX_TC_SMEM_PAD=bytes: reserve extra shared memory, i.e. shrink the L1 carveout, to
+    // measure how the private-row stream depends on L1 capacity
+    if (getenv("CX_TC_SMEM_PAD")) smem += (size_t)atol(getenv("CX_TC_SMEM_PAD"));
     if (smem > (size_t)max_optin) return false;
-    CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     static unsigned long long* trc = nullptr;
     const bool tracing = getenv("CX_TC_TRACE") != nullptr;
     if (tracing && !trc) {
         CX_CUDA(cudaMalloc(&trc, 2048 * sizeof(unsigned long long)));
         CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
     }
-    const int skip = getenv("CX_TC_SKIP") ? atoi(getenv("CX_TC_SKIP")) : 0;
+    if (tracing) trc_arg = trc;
+    skip = getenv("CX_TC_SKIP") ? atoi(getenv("CX_TC_SKIP")) : 0;
     if (skip) {  // timing experiments only: say so once, loudly
         static bool warned = false;
         if (!warned) {
@@ -920,9 +943,12 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
             warned = true;
         }
     }
+#endif
+    kernel_smem(kern, smem);
     kern<<<dim3((unsigned)n_lh, (unsigned)per_lh), TTHREADS, smem, s>>>(b, (float)(1.0 / std::sqrt((double)b.d_k)),
-                                                                             tracing ? trc : nullptr, skip);
+                                                                             ctx->d_flag, trc_arg, skip);
     check_launch("decode_tc_kernel");
+#ifdef CX_EXPERIMENTS
     if (tracing) {  // debugging only: per-tile phase times of CTA (0, 0), us since the staging ended
         std::vector<unsigned long long> h(2048);
         CX_CUDA(cudaStreamSynchronize(s));
@@ -940,6 +966,7 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
         }
         CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
     }
+#endif
     return true;
 }
 

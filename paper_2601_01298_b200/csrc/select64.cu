@@ -150,11 +150,17 @@ struct Sel64Params {
     double* gap_rec;     // [G][take][MAXC] scratch: per round, each CTA's runner-up candidate
 };
 
+#ifdef CX_EXPERIMENTS  // per-round phase cycles (CX_SEL_TRACE=1; debugging builds only)
 #define STAMP(k)                                                        \
     do {                                                                \
         if (p.trace && p.trace != (long long*)1 && tid == 0 && rank == 0 && g == 0 && round < 4096) \
             p.trace[round * 16 + (k)] = clock64();                      \
     } while (0)
+#else
+#define STAMP(k) \
+    do {         \
+    } while (0)
+#endif
 
 // X2 payload header: (score, row) + (|b|^2 of the candidate row, the CTA's second-best
 // exact score in its gap window, -1 if none)
@@ -626,9 +632,11 @@ __global__ void __launch_bounds__(NT, 1) select64_kernel(Sel64Params p) {
         }
         __syncthreads();
         const unsigned long long rbest = *hrow;
+#ifdef CX_EXPERIMENTS
         if (p.trace == (long long*)1 && round < 3 && tid < 64 && (remm & 1u))
             printf("r%d tid%d a=%.17g m=%.17g happ=%.17g hex=%.17g | amin=%.17g amax=%.17g cmin=%.17g cmax=%.17g hmax=%.17g kbest=%llx rbest=%llx\n",
                    round, tid, a[0], m[0], happ[0], hex[0], amin, amax, cmin, cmax, hmax, kbest, rbest);
+#endif
         if (rbest != ~0ull) {  // owner of the local winner publishes its coordinates
             const int li = (int)((long long)rbest - r0);
             if (REG && li < NT) {
@@ -761,8 +769,13 @@ static int active_clusters(int C, int Rs, int S, int mode = ROWS_SMEM) {
     const int rpt = (S + NT - 1) / NT;
     void (*kern)(Sel64Params) = sel64_kernel_for(rpt, mode);
     int n = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess) {
-        if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    bool attr_ok = true;
+    try {
+        kernel_smem(kern, smem, C > 8);  // the attribute only ever grows (a later launch may need more)
+    } catch (const Failure&) {
+        attr_ok = false;
+    }
+    if (attr_ok) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)C, 1, 1);
         cfg.blockDim = dim3(NT, 1, 1);
@@ -786,9 +799,9 @@ static int active_clusters(int C, int Rs, int S, int mode = ROWS_SMEM) {
 // on B200 (C=8: 7.4 us, C=9: 7.2 us, C=16: 5.5 us at L=8192); waves = ceil(G /
 // co-resident clusters).  cfg2 (G=48): C=9 (4.71 vs 4.86 ms at C=8); G <= 7 (one
 // group, or cfg2 over 8 GPUs): C=16.  Returns the estimated cost (us per round).
-static double best_cluster(int G, int64_t L, size_t budget, int* C, int* S, int* Rs, int* mode, int* act_out) {
+static double best_cluster(int G, int64_t L, size_t budget, int* C, int* S, int* Rs, int* mode, int* act_out,
+                           bool sketch_ok = true) {
     double best = 1e300;
-    const bool sketch_ok = !getenv("CX_SEL_NOSKETCH");
     for (int c = 1; c <= MAXC; ++c) {
         const int s_ = (int)((L + c - 1) / c), rs = std::max(0, s_ - RR);
         if (s_ > MAXRPT_ALL * NT) continue;
@@ -829,8 +842,8 @@ int SEL_FN(wave)(int64_t L, int G) {
     return C > 0 ? act : 0;
 }
 
-bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, int take, double lambda,
-                     unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
+bool SEL_FN(launch)(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
+                     double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
                      double* gaps, double* gap_rec, cudaStream_t s) {
     if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 ||
         (reinterpret_cast<uintptr_t>(g.X) & 15) != 0 || g.L < 1)
@@ -848,32 +861,34 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     // wave (e.g. 48 = 15 + 15 + 15 + 3 clusters) runs as its own launch with the
     // configuration best for that many groups, after the full waves.
     int C = 0, S = 0, Rs = 0, mode = ROWS_SMEM, act = 0;
-    if (const char* force = getenv("CX_SEL_C")) {  // debugging / tuning: force a cluster size
-        const int c = atoi(force);
+    if (o.select_cluster > 0) {  // CX_OPT_SELECT_CLUSTER (tests / tuning): force a cluster size
+        const int c = o.select_cluster;
         const int s_ = (int)((g.L + c - 1) / c), rs = std::max(0, s_ - RR);
         if (c >= 1 && c <= MAXC && s_ <= MAXRPT_ALL * NT) {
             C = c; S = s_; Rs = rs;
-            mode = sel64_layout(rs, ROWS_SMEM).total <= budget ? ROWS_SMEM
-                   : sel64_layout(rs, ROWS_SKETCH).total <= budget ? ROWS_SKETCH : ROWS_L2;
+            mode = sel64_layout(rs, ROWS_SMEM).total <= budget                        ? ROWS_SMEM
+                   : !o.select_no_sketch && sel64_layout(rs, ROWS_SKETCH).total <= budget ? ROWS_SKETCH
+                                                                                         : ROWS_L2;
         }
     } else {
-        const double cost = best_cluster(g.G, g.L, budget, &C, &S, &Rs, &mode, &act);
+        const bool sk = !o.select_no_sketch;
+        const double cost = best_cluster(g.G, g.L, budget, &C, &S, &Rs, &mode, &act, sk);
         const int full = act > 0 ? (g.G / act) * act : 0, rem = g.G - full;
         if (C > 0 && full > 0 && rem > 0) {
             int c1, s1, r1, m1, a1, c2, s2, r2, m2, a2;
-            const double cost2 = best_cluster(full, g.L, budget, &c1, &s1, &r1, &m1, &a1) +
-                                 best_cluster(rem, g.L, budget, &c2, &s2, &r2, &m2, &a2);
+            const double cost2 = best_cluster(full, g.L, budget, &c1, &s1, &r1, &m1, &a1, sk) +
+                                 best_cluster(rem, g.L, budget, &c2, &s2, &r2, &m2, &a2, sk);
             if (cost2 < cost * 0.98) {
                 GroupView ga = g, gb = g;
                 ga.G = full;
                 gb.G = rem;
                 gb.X = g.X + (int64_t)full * g.gstride;
-                const int64_t o = (int64_t)full * take;
-                return SEL_FN(launch)(ga, attn, cen, take, lambda, flags, pick_rows, pick_scores, rows, scores, gaps,
-                                      gap_rec, s) &&
-                       SEL_FN(launch)(gb, attn + (int64_t)full * g.L, cen + (int64_t)full * D, take, lambda, flags,
-                                       pick_rows + o, pick_scores + o, rows + o, scores + o,
-                                       gaps ? gaps + full : nullptr, gap_rec ? gap_rec + o * MAXC : nullptr, s);
+                const int64_t off = (int64_t)full * take;
+                return SEL_FN(launch)(ga, o, attn, cen, take, lambda, flags, pick_rows, pick_scores, rows, scores,
+                                      gaps, gap_rec, s) &&
+                       SEL_FN(launch)(gb, o, attn + (int64_t)full * g.L, cen + (int64_t)full * D, take, lambda, flags,
+                                       pick_rows + off, pick_scores + off, rows + off, scores + off,
+                                       gaps ? gaps + full : nullptr, gap_rec ? gap_rec + off * MAXC : nullptr, s);
             }
         }
     }
@@ -903,14 +918,15 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     prm.trace = nullptr;
     prm.gaps = gap_rec ? gaps : nullptr;
     prm.gap_rec = gap_rec;
+#ifdef CX_EXPERIMENTS  // build-time debugging only (CX_NVCC_EXTRA=-DCX_EXPERIMENTS): per-phase cycles
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
     if (tr && tr[0] == 'p') prm.trace = (long long*)1;
+#endif
     const size_t smem = sel64_layout(Rs, mode).total;
     const int rpt = (S + NT - 1) / NT;
     void (*kern)(Sel64Params) = sel64_kernel_for(rpt, mode);
-    CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (C > 8) CX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    kernel_smem(kern, smem, C > 8);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)C, (unsigned)g.G, 1);
     cfg.blockDim = dim3(NT, 1, 1);
@@ -923,13 +939,16 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+#ifdef CX_EXPERIMENTS
     if (getenv("CX_SEL_OCC")) {  // debugging: co-resident clusters for this configuration
         int ncl = 0;
         cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
         fprintf(stderr, "select64: C=%d S=%d Rs=%d smem=%zu max active clusters=%d groups=%d\n", C, S, Rs, smem, ncl, g.G);
     }
+#endif
     CX_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
     count_launch();
+#ifdef CX_EXPERIMENTS
     const char* dump = getenv("CX_SEL_DUMP");
     if (dump && dump[0] == '1') {  // debugging aid: picks in selection order (group 0)
         CX_CUDA(cudaStreamSynchronize(s));
@@ -960,6 +979,7 @@ bool SEL_FN(launch)(const GroupView& g, const double* attn, const double* cen, i
                     acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
         cudaFree(prm.trace);
     }
+#endif
     return true;
 }
 

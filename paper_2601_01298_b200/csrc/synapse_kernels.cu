@@ -827,7 +827,7 @@ void centroid_launch(const GroupView& g, double* cen, cudaStream_t s) {
     } else if (g.dim <= 256) {
         const size_t smem = sizeof(float) * 2 * kCenRows * g.dim;
         if (smem > 48 * 1024)
-            CX_CUDA(cudaFuncSetAttribute(centroid_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kernel_smem(centroid_staged_kernel, smem);
         centroid_staged_kernel<<<g.G, 256, smem, s>>>(g, cen);
         check_launch("centroid_staged_kernel");
     } else {
@@ -859,8 +859,8 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     }
     ctx->gaps_n = g.G;
     if (!(flags & CX_SELECT_GENERIC) &&
-        (select64_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s) ||
-         select128_launch(g, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s)))
+        (select64_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s) ||
+         select128_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s)))
         return;
     // the generic kernel does not monitor: NaN (all-ones bits) = not measured
     CX_CUDA(cudaMemsetAsync(ctx->gaps, 0xFF, sizeof(double) * (size_t)g.G, s));
@@ -880,8 +880,7 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     prm.out_rows = rows;
     prm.out_scores = scores;
 
-    CX_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    if (pl.C > 8) CX_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    kernel_smem(select_kernel, pl.smem, pl.C > 8);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.C, (unsigned)g.G, 1);
     cfg.blockDim = dim3(512, 1, 1);
@@ -926,7 +925,7 @@ void hausdorff(const float* cloud, int64_t count, int dim, const float* lm, int6
     if (dim <= HD_MAXDIM) {
         const size_t smem = sizeof(double) * (size_t)(HD_ROWS + HD_T) * (size_t)(dim + 1);
         if (smem > 48 * 1024)
-            CX_CUDA(cudaFuncSetAttribute(hausdorff_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kernel_smem(hausdorff_tile_kernel, smem);
         hausdorff_tile_kernel<<<(unsigned)((count + HD_ROWS - 1) / HD_ROWS), HD_ROWS, smem, s>>>(
             cloud, count, dim, lm, m, rows, reinterpret_cast<unsigned long long*>(out_worst_sq));
         check_launch("hausdorff_tile_kernel");
@@ -961,7 +960,7 @@ void mean_pairwise(const float* pts, int64_t count, int dim, const int64_t* rows
     check_launch("to_f64_kernel");
     const size_t smem = sizeof(double) * 2 * MP_T * (size_t)(dim + 1);
     if (smem > 48 * 1024)
-        CX_CUDA(cudaFuncSetAttribute(mean_pairwise_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kernel_smem(mean_pairwise_tile_kernel, smem);
     mean_pairwise_tile_kernel<<<dim3((unsigned)nt, (unsigned)nt), 256, smem, s>>>(p64, count, dim, partial);
     check_launch("mean_pairwise_tile_kernel");
     sum_partials_kernel<<<1, 1024, 0, s>>>(partial, nt * nt, out_sum);

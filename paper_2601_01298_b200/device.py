@@ -231,6 +231,36 @@ def gate_decide(h: torch.Tensor, t: torch.Tensor, theta: float):
     return scores, acc.bool(), deg.bool()
 
 
+OPTIONS = {"select_cluster": 1, "select_no_sketch": 2, "decode_impl": 3, "decode_ctas_per_lh": 4,
+           "host_upload_values": 5}
+DECODE_IMPLS = {"auto": 0, "tc": 1, "v2": 2, "v1": 3}
+
+
+def set_option(name: str, value, device: int | None = None) -> int:
+    """Path pinning for tests / tuning (cx_ctx_set_option) on this device's ctx;
+    returns the previous value.  decode_impl takes "auto" | "tc" | "v2" | "v1"."""
+    dev = torch.cuda.current_device() if device is None else device
+    code = OPTIONS[name]
+    if name == "decode_impl" and isinstance(value, str):
+        value = DECODE_IMPLS[value]
+    old = C.c_int64()
+    check(lib.cx_ctx_get_option(ctx(dev), code, C.byref(old)), "ctx_get_option")
+    check(lib.cx_ctx_set_option(ctx(dev), code, int(value)), "ctx_set_option")
+    return int(old.value)
+
+
+DEVERR_NONFINITE, DEVERR_TAIL_RANGE = 1, 2
+
+
+def device_errors(clear: bool = True, device: int | None = None) -> int:
+    """Device-detected precondition failures of this device's ctx (cx_ctx_device_errors):
+    DEVERR_NONFINITE | DEVERR_TAIL_RANGE bits.  Synchronizes the current stream."""
+    dev = torch.cuda.current_device() if device is None else device
+    f = C.c_uint()
+    check(lib.cx_ctx_device_errors(ctx(dev), _stream(), C.byref(f), int(clear)), "ctx_device_errors")
+    return int(f.value)
+
+
 def selection_gaps(n_groups: int, device: int | None = None) -> torch.Tensor:
     """Decision-gap monitor of the most recent selection on this device's ctx
     (cx_selection_gaps): per group, the smallest top-1 / top-2 exact hybrid gap

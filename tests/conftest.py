@@ -41,3 +41,19 @@ def ref():
     if r is None:
         pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
     return r
+
+
+@pytest.fixture
+def cx_option():
+    """Pin a kernel path on the device ctx for one test (cx_ctx_set_option);
+    restored afterwards.  Usage: cx_option("select_cluster", 4)."""
+    saved = []
+
+    def pin(name, value):
+        from paper_2601_01298_b200 import device
+        saved.append((name, device.set_option(name, value)))
+
+    yield pin
+    from paper_2601_01298_b200 import device
+    for name, old in reversed(saved):
+        device.set_option(name, old)

@@ -159,3 +159,15 @@ def test_plain_c_consumer_compiles_and_links(tmp_path):
                         "-Wl,-rpath," + libdir, "-o", str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert exe.exists()
+
+
+def test_release_library_has_no_debug_knobs():
+    """The experiment switches (phase tracing, skipping a decode role's math, the
+    L1 carveout pad, chunk overrides) are compiled out of the release library
+    (-DCX_EXPERIMENTS builds only); path pinning goes through cx_ctx_set_option."""
+    from paper_2601_01298_b200 import _lib
+    with open(_lib.LIB_PATH, "rb") as f:
+        blob = f.read()
+    for knob in (b"CX_TC_SKIP", b"CX_TC_TRACE", b"CX_TC_SMEM_PAD", b"CX_SEL_TRACE", b"CX_SEL_DUMP", b"CX_SEL_OCC",
+                 b"CX_E2E_CHUNKS", b"CX_SEL_C", b"CX_DECODE", b"CX_TC_PER_LH", b"CX_HOST_UPLOAD_VALUES"):
+        assert knob not in blob, knob

@@ -154,3 +154,63 @@ def test_compress_grouped_host_mha_d128(cx):
     assert torch.equal(sk, dsk.cpu()) and torch.equal(sv, dsv.cpu())
     gi = torch.arange(G)[:, None]
     assert torch.equal(sk, hk[gi, rows]) and torch.equal(sv, hv[gi, rows])
+
+
+def test_append_on_a_caller_stream_orders_before_regrow(cx):
+    """An append enqueued on a caller stream behind a long kernel, then a host
+    append that regrows the cache (its copies run on the cache's own stream):
+    the regrow must wait for the caller-stream append, or its rows are lost."""
+    import torch
+    cfg = cx.ModelConfig(n_layers=2, n_heads=1, d_model=16, d_k=16, max_positions=64)
+    c = cx.KvCache(cfg, capacity=4)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    k = torch.randn(2, 4, 16, device="cuda", generator=g)
+    v = torch.randn(2, 4, 16, device="cuda", generator=g)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(50_000_000)  # ~25 ms: the append below is still queued when the host moves on
+        c.append_context_dev(k.data_ptr(), v.data_ptr(), 0, 4, side.cuda_stream)
+    nk, nv = np.full(32, 7.0, np.float32), np.full(32, -7.0, np.float32)
+    c.append_entry(4, cx.Origin.context, nk, nv)  # capacity 4 -> regrow
+    for layer in range(2):
+        lk = c.layer_keys(layer).reshape(5, 16)
+        assert np.array_equal(lk[:4], k[layer].cpu().numpy()), "rows appended on the caller stream were lost"
+        assert np.array_equal(lk[4], nk[16 * layer:16 * layer + 16])
+        assert np.array_equal(c.layer_values(layer).reshape(5, 16)[:4], v[layer].cpu().numpy())
+
+
+@pytest.mark.parametrize("impl", ["tc", "v2", "v1"])
+def test_decode_tail_len_out_of_range_is_flagged(cx_option, impl):
+    """tail_len == t_cap with an append (no room) and tail_len < 0 raise
+    CX_DEVERR_TAIL_RANGE; the offending agents append nothing and no other
+    agent's tail changes; a valid batch raises nothing (model.cpp:124-140)."""
+    import torch
+
+    from paper_2601_01298_b200 import device
+    cx_option("decode_impl", impl)
+    N, Lr, H, Q, dk, k, tc = 6, 2, 2, 14, 64, 32, 8
+    g = torch.Generator(device="cuda").manual_seed(4)
+    sk = torch.randn(Lr, H, k, dk, device="cuda", generator=g)
+    sv = torch.randn(Lr, H, k, dk, device="cuda", generator=g)
+    tk = torch.randn(N, Lr, H, tc, dk, device="cuda", generator=g)
+    tv = torch.randn(N, Lr, H, tc, dk, device="cuda", generator=g)
+    nk = torch.randn(N, Lr, H, dk, device="cuda", generator=g)
+    nv = torch.randn(N, Lr, H, dk, device="cuda", generator=g)
+    q = torch.randn(N, Lr, Q, dk, device="cuda", generator=g)
+    out = torch.empty_like(q)
+    device.device_errors(clear=True)
+    tl = torch.tensor([3, tc - 1, 0, 5, 2, 1], dtype=torch.int32, device="cuda")
+    device.decode_step(sk, sv, tk, tv, tl, q, out, nk, nv)
+    assert device.device_errors() == 0
+    tl_bad = torch.tensor([3, tc, -1, 5, 2, 1], dtype=torch.int32, device="cuda")
+    tk0, tv0 = tk.clone(), tv.clone()
+    device.decode_step(sk, sv, tk, tv, tl_bad, q, out, nk, nv)
+    assert device.device_errors() == device.DEVERR_TAIL_RANGE
+    assert torch.equal(tk[1], tk0[1]) and torch.equal(tk[2], tk0[2]), "a flagged agent appended"
+    for a in (0, 3, 4, 5):  # the valid agents appended their row and nothing else
+        r = int(tl_bad[a])
+        assert torch.equal(tk[a][:, :, r], nk[a]) and torch.equal(tv[a][:, :, r], nv[a])
+        keep = [i for i in range(tc) if i != r]
+        assert torch.equal(tk[a][:, :, keep], tk0[a][:, :, keep])
+    device.decode_step(sk, sv, tk, tv, tl, q, out)  # no append: tail_len == t_cap would be valid
+    assert device.device_errors() == 0

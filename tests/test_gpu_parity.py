@@ -174,13 +174,13 @@ def test_mha_mode_matches_reference_cloud(dev, orc):
     (2, 1500, 40, "1"),    # 1500 rows per CTA: rows re-read from L2
     (3, 5, 9, None),       # k > L
 ])
-def test_select128_matches_reference(dev, orc, monkeypatch, G, L, k, force):
+def test_select128_matches_reference(dev, orc, cx_option, G, L, k, force):
     """The d = 128 instantiation of the cluster selection (select128.cu) on the
     head-concatenated cloud of a 2-head MHA cache: rows and scores bit-exact
     against the reference per group and against the generic kernel."""
     import torch
     if force:
-        monkeypatch.setenv("CX_SEL_C", force)
+        cx_option("select_cluster", int(force))
     dm = 128
     ks, qs = [], []
     for gi in range(G):
@@ -202,12 +202,12 @@ def test_select128_matches_reference(dev, orc, monkeypatch, G, L, k, force):
 
 
 @pytest.mark.parametrize("force", ["3", "5"])
-def test_sketch_rows_fp16_overflow(dev, orc, monkeypatch, force):
+def test_sketch_rows_fp16_overflow(dev, orc, cx_option, force):
     """Sketch-row mode with coordinates beyond the fp16 range (+-65504): the sketch dot
     becomes +-inf / NaN, and the filter must then evaluate exactly (a -inf dot would
     otherwise make the lower bound +inf and skip the row)."""
     import torch
-    monkeypatch.setenv("CX_SEL_C", force)
+    cx_option("select_cluster", int(force))
     L, d, k = 4000, 64, 40
     r = orc.rng(515)
     keys = r.gaussian_f32(L * d).reshape(L, d)
@@ -446,14 +446,14 @@ def test_synapse_buffer(cx):
     # every q-heads-per-KV-head instantiation (reduce-scatter widths 1, 2, 4, 8), t_cap / k_syn edges
     ("tc", 7, 17, 2, 2, 2, 5), ("tc", 11, 1, 2, 2, 4, 64), ("tc", 30, 176, 2, 1, 4, 20), ("tc", 5, 64, 2, 2, 16, 33),
     ("v2", 9, 164, 3, 2, 14, 33), ("v2", 100, 164, 24, 2, 14, 33), ("v1", 5, 164, 3, 2, 14, 33)])
-def test_decode_step_vs_oracle(dev, orc, monkeypatch, impl, N, k, Lr, H, Q, Tc):
+def test_decode_step_vs_oracle(dev, orc, cx_option, impl, N, k, Lr, H, Q, Tc):
     """Batched decode (append + attend) == kernels::attend(n_heads=1) per (agent, layer, q-head)
     over [synapse rows of its KV head || private rows] (scheduler.cpp:245-262), 1e-3 rel.
     impl: tc = tcgen05 synapse GEMMs, v2 = CUDA-core register-tiled, v1 = generic.
     Lr=24, N=100: 48 (layer, KV head) pairs -> several 18-agent tiles per CTA with a
     ragged last tile (the cross-tile barrier protocol of decode_tc.cu)."""
     import torch
-    monkeypatch.setenv("CX_DECODE", impl)
+    cx_option("decode_impl", impl)
     gen = torch.Generator(device="cuda").manual_seed(11)
     dk = 64
     syn_k = torch.randn(Lr, H, k, dk, device="cuda", generator=gen)

@@ -80,8 +80,8 @@ def test_grouped_compress_random_sweep(dev, orc, seed):
 
 
 @pytest.mark.parametrize("seed", list(range(12)))
-def test_grouped_compress_forced_row_modes(dev, orc, monkeypatch, seed):
-    """The same check with the cluster size forced small (CX_SEL_C), so the rows beyond
+def test_grouped_compress_forced_row_modes(dev, orc, cx_option, seed):
+    """The same check with the cluster size forced small (CX_OPT_SELECT_CLUSTER), so the rows beyond
     the register rows live in shared memory as fp32 or as the fp16 sketch."""
     import torch
     rs = np.random.default_rng(500 + seed)
@@ -92,7 +92,7 @@ def test_grouped_compress_forced_row_modes(dev, orc, monkeypatch, seed):
     lam = float(rs.choice([0.3, 0.5, 0.8]))
     if (L + C - 1) // C > 2048:
         C = (L + 2047) // 2048
-    monkeypatch.setenv("CX_SEL_C", str(C))
+    cx_option("select_cluster", C)
     G = 2
     ks, vs, qs = zip(*[oracle.synthetic_group(orc, 9100 + 7 * seed + gi, L, d, 2) for gi in range(G)])
     kt = torch.from_numpy(np.stack(ks)).cuda()

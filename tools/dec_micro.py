@@ -1,14 +1,14 @@
 """Micro-timing of the decode step (tools only)."""
 import os, sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("CX_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_01298_b200 import device as cxd
 torch.cuda.set_device(0)
 g = torch.Generator(device="cuda").manual_seed(0)
 impls = os.environ.get("IMPLS", "tc,v2").split(",")
 for impl in impls:
-  os.environ["CX_DECODE"] = impl
-  for N in (100, 1000):
+  cxd.set_option("decode_impl", impl)
+  for N in [int(x) for x in os.environ.get("NS", "100,1000").split(",")]:
       sk = torch.randn(24, 2, 164, 64, device="cuda", generator=g); sv = torch.randn_like(sk)
       tk = torch.randn(N, 24, 2, 33, 64, device="cuda", generator=g); tv = torch.randn_like(tk)
       tl = torch.full((N,), 32, dtype=torch.int32, device="cuda")

@@ -1,7 +1,7 @@
 """One decode configuration, a few launches (tools only; for ncu)."""
 import os, sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("CX_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_01298_b200 import device as cxd
 N = int(os.environ.get("N", "1000"))
 torch.cuda.set_device(0)

@@ -1,7 +1,7 @@
 """Decode step time vs agent count (tools only): N up to 10,000 agents, T=32, cfg2 shape."""
 import os, sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("CX_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_01298_b200 import device as cxd
 torch.cuda.set_device(0)
 g = torch.Generator(device="cuda").manual_seed(0)

@@ -1,7 +1,7 @@
 """e2e compression timing (host buffers) per chunking (tools only; CX_E2E_CHUNKS)."""
 import os, sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("CX_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_01298_b200 import device as cxd
 torch.cuda.set_device(0)
 G, L, D, K = 48, 8192, 64, 164

@@ -1,7 +1,7 @@
 """Metric kernels (A7: hausdorff / mean-pairwise reduction) at scale (tools only)."""
 import os, sys, time
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("CX_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2601_01298_b200 as cx
 for L, m in [(2048, 40), (8192, 164)]:
     rng = np.random.default_rng(0)

@@ -4,7 +4,7 @@ import sys
 
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("CX_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_01298_b200 import device as cxd  # noqa: E402
 
 G, L, k = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (1, 8192, 164)))
