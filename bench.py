@@ -18,9 +18,12 @@ D2H of the synapse inside the timed region).
 (oracle/_ref, compiled from the unmodified reference sources) on the host
 cores, on a bounded sample of the same workload.
 
-Multi-GPU (torchrun): the 48 groups are sharded across ranks (strong scaling of
-one compression), followed by the single NCCL all-gather of the synapse; the
-decode leg shards agents (N per rank).
+Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run, one
+process per GPU) unless it already runs under torchrun.  The 48 groups are
+sharded across ranks (strong scaling of one compression) and one C-ABI call
+per rank (cx_compress_sharded_dev) runs the local selections and the single
+NCCL all-gather of the packed synapse; the decode leg shards agents (N per
+rank, no exchange).  NCCL_DEBUG=INFO (INIT) prints the communicator lines.
 """
 from __future__ import annotations
 
@@ -57,6 +60,18 @@ def load_peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -118,39 +133,42 @@ def dist_env():
 # ----------------------------------------------------------------------------
 # CPU baseline / reference arm (oracle/_ref = unmodified reference sources)
 # ----------------------------------------------------------------------------
-def cpu_compress_sample(n_threads, groups, seconds_target=10.0):
+def cpu_compress_sample(n_threads, groups, seconds_target=10.0, length=L, k=K, max_reps=50):
     """Time the reference's per-group compression (attention over the group's
-    7 q-heads + select_landmarks_points) over `groups` groups on n_threads
-    host threads.  Returns (compressions/s, sample description)."""
+    7 q-heads + select_landmarks_points, oracle/_ref = the unmodified reference
+    sources) over `groups` groups of `length` rows on n_threads host threads.
+    Returns (compressions/s of all 48 groups, kind, sample description)."""
     import ctypes as C
 
     import numpy as np
 
     import oracle
     ref = oracle.load_ref()
-    kind = "reference"
-    rs = np.random.default_rng(0)
-    clouds = rs.standard_normal((groups, L, D), dtype=np.float32)
-    qs = rs.standard_normal((groups, N_Q // N_KV, D), dtype=np.float32)
-    idx = np.empty((groups, K), np.int64)
     if ref is None:
         raise RuntimeError("oracle/_ref/libcortex_ref.so not built (run build() where /root/reference exists)")
+    rs = np.random.default_rng(0)
+    clouds = rs.standard_normal((groups, length, D), dtype=np.float32)
+    qs = rs.standard_normal((groups, N_Q // N_KV, D), dtype=np.float32)
+    idx = np.empty((groups, min(k, length)), np.int64)
     P = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
     reps, t0 = 0, time.perf_counter()
     while True:
-        st = ref.lib.ref_compress_groups_mt(groups, P(clouds, C.c_float), C.c_int64(L), D, P(qs, C.c_float),
-                                            N_Q // N_KV, K, C.c_double(LAM), n_threads, P(idx, C.c_int64))
+        st = ref.lib.ref_compress_groups_mt(groups, P(clouds, C.c_float), C.c_int64(length), D, P(qs, C.c_float),
+                                            N_Q // N_KV, k, C.c_double(LAM), n_threads, P(idx, C.c_int64))
         if st != 0:
             raise RuntimeError("reference compression failed")
         reps += 1
         el = time.perf_counter() - t0
-        if el >= seconds_target or reps >= 50:
+        if el >= seconds_target or reps >= max_reps:
             break
     value = reps * groups / G / el
-    return value, kind, f"{reps} x {groups} of 48 groups (L=8192, k=164, 7 q-heads) on {n_threads} threads, {el:.1f} s"
+    return value, "reference", (f"{reps} x {groups} of 48 groups (L={length}, k={k}, 7 q-heads) on {n_threads} "
+                                f"threads, {el:.1f} s")
 
 
 def cpu_decode_sample(n_threads, n_agents, seconds_target=5.0):
+    """The reference's kernels::attend per (agent, layer, q-head) over [synapse
+    rows || the agent's T+1 private rows], agents over n_threads host threads."""
     import ctypes as C
 
     import numpy as np
@@ -176,7 +194,27 @@ def cpu_decode_sample(n_threads, n_agents, seconds_target=5.0):
         el = time.perf_counter() - t0
         if el >= seconds_target or reps >= 100:
             break
-    return reps * n_agents / el, f"{reps} x {n_agents} agents x 24 layers x 14 q-heads, n={K}+{T}, {n_threads} threads"
+    return reps * n_agents / el, (f"{reps} x {n_agents} agents x 24 layers x 14 q-heads, n={K}+{T}, "
+                                  f"{n_threads} threads, {el:.1f} s")
+
+
+def cpu_extra_baselines(threads, decode_agents=(100, 1000)):
+    """The other BASELINE configurations' reference CPU numbers, timed on this host in the
+    same run: cfg4 compression (16 sampled groups at L=32768 -> k=656) and agent decode."""
+    out = {"cpu_model": cpu_model(), "cores": threads}
+    try:
+        v, _, sample = cpu_compress_sample(threads, min(G, max(threads, 8)), seconds_target=0.0, length=32768, k=656,
+                                           max_reps=1)
+        out["cfg4"] = {"value": v, "unit": "compressions/s", "sample": sample}
+    except Exception as e:  # noqa: BLE001
+        out["cfg4"] = {"value": None, "sample": f"unavailable: {e}"}
+    for n in decode_agents:
+        try:
+            v, sample = cpu_decode_sample(threads, n, seconds_target=1.0)
+            out[f"decode_N{n}"] = {"value": v, "unit": "agent-steps/s", "sample": sample}
+        except Exception as e:  # noqa: BLE001
+            out[f"decode_N{n}"] = {"value": None, "sample": f"unavailable: {e}"}
+    return out
 
 
 def run_reference(args):
@@ -191,7 +229,7 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
-    dec, dsample = cpu_decode_sample(threads, args.n_agents, seconds_target=1.0)
+    extra = cpu_extra_baselines(threads, decode_agents=sorted({args.n_agents, 1000}))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "compressions/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
@@ -200,8 +238,10 @@ def run_reference(args):
                                f"decode N={args.n_agents}, T={T_PRIV}",
                    "sample_groups_per_step": groups},
         "cpu_baseline": {"value": value, "unit": "compressions/s", "cores": threads, "kind": "reference",
-                         "sample": f"{groups} of 48 groups per step on {threads} threads"},
-        "decode": {"agent_steps_per_s": dec, "n_agents": args.n_agents, "sample": dsample},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{groups} of 48 groups per step on {threads} threads (x 48/{groups})"},
+        "decode": {k: v for k, v in extra.items() if k.startswith("decode_")},
+        "cfg4": extra["cfg4"],
         "e2e": {"value": value, "unit": "compressions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -216,12 +256,14 @@ def run_b200(args):
     import torch.distributed as dist
 
     from paper_2601_01298_b200 import device as cxd
-    from paper_2601_01298_b200.parallel import all_gather_groups, shard_range
+    from paper_2601_01298_b200.parallel import Comm, shard_range
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = Comm.from_torch(device=local)  # the C-ABI's own NCCL communicator (cx_comm)
     dev = torch.device("cuda", local)
     gb, ge = shard_range(G, rank, world)
     g_local = ge - gb
@@ -229,27 +271,26 @@ def run_b200(args):
     keys = torch.randn(g_local, L, D, device=dev, generator=gen)
     values = torch.randn(g_local, L, D, device=dev, generator=gen)
     queries = torch.randn(g_local, N_Q // N_KV, D, device=dev, generator=gen)
-    take = K
-    rows = torch.empty(g_local, take, dtype=torch.int64, device=dev)
-    scores = torch.empty(g_local, take, dtype=torch.float64, device=dev)
-    sk = torch.empty(g_local, take, D, device=dev)
-    sv = torch.empty(g_local, take, D, device=dev)
-    attn = torch.empty(g_local, L, dtype=torch.float64, device=dev)
+    out = (torch.empty(G, K, dtype=torch.int64, device=dev), torch.empty(G, K, dtype=torch.float64, device=dev),
+           torch.empty(G, K, D, device=dev), torch.empty(G, K, D, device=dev))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    # one full compression through the single C-ABI call (attention + select + gather)
+    # one full compression: ONE C-ABI call per rank.  N = 1: cx_compress_grouped_dev
+    # (centroid || attention, greedy selection, landmark K/V gather); N > 1:
+    # cx_compress_sharded_dev (the same on this rank's groups + the NCCL all-gather)
     def full_compress():
-        return cxd.compress_grouped(keys, values, queries, K, LAM, out=(rows, scores, sk, sv))
+        if comm is None:
+            return cxd.compress_grouped(keys, values, queries, K, LAM, out=out)
+        return comm.compress_sharded(cxd.ctx(local), keys, values, queries, K, LAM, G, out=out)
 
-    # warm-up
     for _ in range(max(args.warmup, 3)):
         full_compress()
     torch.cuda.synchronize()
+    # decision-gap monitor of this rank's groups (every round's top-1 / top-2 gap)
+    min_gap = float(cxd.selection_gaps(g_local).min()) if g_local else float("inf")
 
-    # ---- timed: compression with inputs resident in HBM, L2 flushed between steps.
-    # One step = ONE C-ABI call (cx_compress_grouped_dev: centroid || attention,
-    # greedy selection, landmark K/V gather) + the synapse all-gather when N > 1.
+    # ---- timed: compression with inputs resident in HBM, L2 flushed between steps
     launches0 = cxd.kernel_launch_count()
     times = []
     with ClockSampler(local) as clk:
@@ -261,8 +302,6 @@ def run_b200(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             full_compress()
-            if world > 1:
-                all_gather_groups([rows, scores, sk, sv], G)
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -282,29 +321,33 @@ def run_b200(args):
         sel_times.append(e0.elapsed_time(e1))
     ms = statistics.mean(times)
     sel_ms = statistics.mean(sel_times)
+    fp64_rate = cxd.probe_fp64_rate(local)
     if world > 1:
-        t = torch.tensor([ms, sel_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms, sel_ms, -min_gap], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, sel_ms = float(t[0]), float(t[1])
+        ms, sel_ms, min_gap = float(t[0]), float(t[1]), -float(t[2])
     value = 1000.0 / ms  # one compression of all 48 groups per step (strong scaling)
-    return finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, values, queries)
+    return finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, min_gap, fp64_rate, comm)
 
 
-def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, values, queries):
-    import torch
-
-    from paper_2601_01298_b200 import device as cxd
+def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, min_gap, fp64_rate, comm):
     hbm, peak_kind = load_peaks()
-    # roofline of the dominant kernel (greedy selection) against HBM
+    # HBM roofline of the dominant kernel (greedy selection): the
+    # compression's algorithmic bytes over the selection's event time
     bytes_per_launch = COMPRESS_BYTES * keys.shape[0] / G
     achieved = bytes_per_launch / (sel_ms * 1e-3) / 1e9
+    # fp64 roofline: the reference's exact distance work (3 G k L d unfused fp64 add / sub /
+    # mul + G k L sqrt) per second against the on-box DADD / DMUL rate.  The
+    # conservative fp32 filter skips ~97% of it, so this can exceed 1 as the kernel improves.
+    fp64_ops = (3 * G * K * L * D + G * K * L) * keys.shape[0] / G
+    fp64_achieved = fp64_ops / (sel_ms * 1e-3)
     # clocks keep being sampled through the other timed legs (the compression
     # region alone is ~40 ms, shorter than one nvidia-smi query)
     with ClockSampler(local_rank()) as clk2:
         dec = run_decode(args, dev, rank, world)
         e2e = run_e2e(args, dev, rank, world)
         cfg5 = run_cfg5(args, dev) if rank == 0 else None
-        cfg4 = run_cfg4(args, dev, rank, world)
+        cfg4 = run_cfg4(args, dev, rank, world, comm)
     clk.samples += clk2.samples
     line = {
         "metric": METRIC, "value": value, "unit": "compressions/s", "n_gpus": world, "steps": args.steps,
@@ -312,20 +355,30 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (torch.randn N(0,1) keys/values/queries)",
         "config": {"workload": "cfg2 (BASELINE configs[1]): 24 layers x 2 KV heads x d=64, 14 q-heads, "
                                f"L=8192 -> k=164 (98%), lambda=0.5; decode N={args.n_agents} agents, T={T_PRIV}",
-                   "groups": G, "parallelism": f"groups sharded over {world} GPU(s)",
+                   "groups": G, "parallelism": f"groups sharded over {world} GPU(s)" +
+                   (" + one NCCL all-gather (cx_compress_sharded_dev)" if world > 1 else ""),
                    "l2": "flushed (256 MB write) between timed steps"},
         "roofline": {"kernel": "select64_kernel (greedy max-min selection, thread-block clusters)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_source": peak_kind, "traffic": ncu_traffic("select64_kernel"),
-                     "traffic_unit": "bytes per step: all select64 launches of one compression (ncu --set full, profiles/r1_ncu_full_summary.json)",
-                     "note": "selection is fp64/FMA-issue + barrier-latency bound (SURVEY.md §8(d)); "
-                             "HBM fraction reported as required"},
+                     "traffic_unit": "bytes per step: all select64 launches of one compression (ncu --set full)",
+                     "note": "selection is fp64-issue + per-round latency bound (SURVEY.md §8(d)); see roofline_fp64"},
+        "roofline_fp64": {"kernel": "select64_kernel", "bound": "fp64 add/mul issue",
+                          "achieved": fp64_achieved / 1e12, "peak": fp64_rate / 1e12, "unit": "T fp64 op/s",
+                          "frac": fp64_achieved / fp64_rate, "algorithmic_ops_per_step": fp64_ops,
+                          "peak_source": "measured on this GPU (cx_probe_fp64_rate: unfused DADD/DMUL chains)",
+                          "latency_model": {"rounds": K, "us_per_round": sel_ms * 1e3 / K,
+                                            "note": "k dependent rounds, each two cluster-wide exchanges"}},
         "select_ms": sel_ms,
+        "selection_min_decision_gap": min_gap,
         "gpu_launches": launches,
+        "gpu_launches_per_step": launches / max(1, args.steps),
         "clocks": dict(clk.summary(), regions="compression, decode, e2e, cfg5 and cfg4 timed legs"),
     }
     if dec is not None:
         line["decode"] = dec
+        if "N1000" in dec:
+            line["roofline_decode"] = dict(dec["N1000"]["roofline"], kernel=dec["N1000"]["kernel"] + ", N=1000")
     if e2e is not None:
         line["e2e"] = e2e
     if cfg5 is not None:
@@ -336,10 +389,14 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
         try:
             v, kind, sample = cpu_compress_sample(threads, min(G, max(threads, 8)), seconds_target=8.0)
             line["cpu_baseline"] = {"value": v, "unit": "compressions/s", "cores": threads, "kind": kind,
-                                    "sample": sample}
+                                    "cpu_model": cpu_model(), "sample": sample}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": "compressions/s", "cores": threads, "kind": "reference",
-                                    "sample": f"unavailable: {e}"}
+                                    "cpu_model": cpu_model(), "sample": f"unavailable: {e}"}
+        if world == 1:
+            line["cpu_baseline_other_configs"] = cpu_extra_baselines(threads)
+    if comm is not None:
+        comm.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -554,23 +611,31 @@ def run_cfg5(args, dev, tokens=600, n_agents=100, inj_every=10, push_every=10, t
             "river_entries": river.size(), "river_context_count": river.context_count()}
 
 
-def run_cfg4(args, dev, rank=0, world=1, steps=3):
+def run_cfg4(args, dev, rank=0, world=1, comm=None, steps=3):
     """BASELINE configs[3]: long context L=32768 -> k=656 (98%), 48 groups sharded
-    by (layer, head) over the ranks, synapse all-gathered (NCCL) when N > 1."""
+    by (layer, head) over the ranks; N > 1: cx_compress_sharded_dev (the local
+    selections + the NCCL all-gather of the synapse)."""
     import torch
     import torch.distributed as dist
 
     from paper_2601_01298_b200 import device as cxd
-    from paper_2601_01298_b200.parallel import all_gather_groups, shard_range
+    from paper_2601_01298_b200.parallel import shard_range
     l4, k4 = 32768, 656
     gb, ge = shard_range(G, rank, world)
     gen = torch.Generator(device=dev).manual_seed(77 + rank)
     keys = torch.randn(ge - gb, l4, D, device=dev, generator=gen)
     values = torch.randn(ge - gb, l4, D, device=dev, generator=gen)
     queries = torch.randn(ge - gb, N_Q // N_KV, D, device=dev, generator=gen)
-    out = (torch.empty(ge - gb, k4, dtype=torch.int64, device=dev), torch.empty(ge - gb, k4, dtype=torch.float64, device=dev),
-           torch.empty(ge - gb, k4, D, device=dev), torch.empty(ge - gb, k4, D, device=dev))
-    cxd.compress_grouped(keys, values, queries, k4, LAM, out=out)
+    out = (torch.empty(G, k4, dtype=torch.int64, device=dev), torch.empty(G, k4, dtype=torch.float64, device=dev),
+           torch.empty(G, k4, D, device=dev), torch.empty(G, k4, D, device=dev))
+
+    def step():
+        if comm is None:
+            cxd.compress_grouped(keys, values, queries, k4, LAM, out=out)
+        else:
+            comm.compress_sharded(cxd.ctx(dev.index), keys, values, queries, k4, LAM, G, out=out)
+
+    step()
     torch.cuda.synchronize()
     if world > 1:  # rank 0 comes from the e2e / cfg5 legs: align the ranks before timing
         dist.barrier()
@@ -579,9 +644,7 @@ def run_cfg4(args, dev, rank=0, world=1, steps=3):
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        cxd.compress_grouped(keys, values, queries, k4, LAM, out=out)
-        if world > 1:
-            all_gather_groups(list(out), G)
+        step()
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
@@ -642,6 +705,23 @@ def run_e2e(args, dev, rank=0, world=1):
             "ms_per_step": ms}
 
 
+def spawn_ranks(n):
+    """`--gpus N` outside torchrun: relaunch this command as N ranks, one process per
+    GPU (torch.distributed.run, rendezvous on 127.0.0.1).  Fails loudly when fewer
+    than N devices are visible."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} requested but only {have} CUDA device(s) are visible"}), flush=True)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr",
+           "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -653,8 +733,17 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.impl == "reference":  # host cores only: rank 0 of a torchrun launch runs it, the others exit 0
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        return 2
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     run_b200(args)
     return 0
 

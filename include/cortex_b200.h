@@ -105,6 +105,12 @@ typedef struct cx_ctx cx_ctx; /* device workspace + default stream; one per host
 cx_status cx_ctx_create(int device, cx_ctx** out);
 cx_status cx_ctx_destroy(cx_ctx* ctx);
 
+/* On-box peak of the selection's exact arithmetic: unfused fp64 add / mul
+ * operations per second over the whole device (independent dependency chains on
+ * every SM; a few ms).  The bench uses it as the fp64 roofline of the greedy
+ * selection. */
+cx_status cx_probe_fp64_rate(cx_ctx* ctx, double* ops_per_s);
+
 /* Priority lanes (SURVEY.md §8(b) threading row): the River's
  * work (injection appends, synapse pushes) goes on the highest-priority stream,
  * Stream agents' decode on a medium-priority one.  Replaces the reference's
@@ -350,6 +356,69 @@ cx_status cx_synapse_buffer_wait_nonempty(cx_synapse_buffer* b, int64_t timeout_
                                           const cx_snapshot** out);
 cx_status cx_synapse_buffer_shutdown(cx_synapse_buffer* b);
 cx_status cx_snapshot_release(const cx_snapshot* s);
+
+/* ======================================================================
+ * Multi-GPU (the reference has none -- SPEC.md:15).
+ * Selection groups are sharded by (layer, KV head): rank r of R owns the
+ * balanced contiguous block [b_r, e_r) of the G groups (the first G % R ranks
+ * one more) and runs its selections with no collective; the ONE exchange step
+ * is an all-gather of the packed per-group synapse records over NVLink.
+ * Decode shards by agent against local synapse replicas (no exchange).
+ * NCCL is loaded at first use (dlopen libnccl.so.2); without it these calls
+ * return CX_DEVICE_ERROR and cx_nccl_version() returns 0.
+ * ====================================================================== */
+typedef struct cx_comm cx_comm;
+#define CX_COMM_ID_BYTES 128
+int cx_nccl_version(void);
+cx_status cx_comm_unique_id(void* id /* CX_COMM_ID_BYTES */);
+/* one process per GPU (ids shared out of band, e.g. torch.distributed) */
+cx_status cx_comm_init_rank(int nranks, const void* id, int rank, int device, cx_comm** out);
+/* one process driving ndev GPUs (ncclCommInitAll): out[ndev]; drive the ranks'
+ * collective calls between cx_comm_group_start / cx_comm_group_end */
+cx_status cx_comm_init_all(int ndev, const int* devices, cx_comm** out);
+cx_status cx_comm_destroy(cx_comm* c);
+cx_status cx_comm_info(const cx_comm* c, int* rank, int* nranks, int* device);
+cx_status cx_comm_group_start(void);
+cx_status cx_comm_group_end(void);
+
+/* Sharded compression: `local` holds exactly this rank's block of the
+ * n_groups_total groups (CX_PRECONDITION_ERROR otherwise), `values` the same
+ * rows' values.  Outputs (device, ALL groups, every rank): rows/scores
+ * [G][take], syn_keys/syn_values [G][take][dim]; take = min(k, count).  One
+ * compression of the local groups, then one all-gather; bitwise equal to a
+ * single-GPU cx_compress_grouped_dev of all G groups.  dim % 4 == 0. */
+cx_status cx_compress_sharded_dev(cx_ctx* ctx, cx_comm* comm, const cx_groups* local,
+                                  const float* values, int n_groups_total, int k, double lambda,
+                                  unsigned flags, int64_t* out_rows, double* out_scores,
+                                  float* syn_keys, float* syn_values, void* stream);
+
+/* The exchange step's record format, for callers with their own transport:
+ * one record per group (rows | scores | keys | values, padded to 256 B).
+ * pack: groups [g_begin, g_begin + n_groups) of the [G] arrays -> n_groups
+ * consecutive records at dst.  unpack: nranks blocks of ceil(G / nranks)
+ * records each (rank r's groups first in its block) -> the [G] arrays. */
+size_t cx_synapse_record_bytes(int take, int dim);
+cx_status cx_synapse_pack_dev(const int64_t* rows, const double* scores, const float* syn_keys,
+                              const float* syn_values, int g_begin, int n_groups, int take, int dim,
+                              void* dst, void* stream);
+cx_status cx_synapse_unpack_dev(const void* src, int n_groups, int nranks, int take, int dim,
+                                int64_t* rows, double* scores, float* syn_keys, float* syn_values,
+                                void* stream);
+/* the same on host memory (no device work) */
+cx_status cx_synapse_pack_host(const int64_t* rows, const double* scores, const float* syn_keys,
+                               const float* syn_values, int g_begin, int n_groups, int take, int dim,
+                               void* dst);
+cx_status cx_synapse_unpack_host(const void* src, int n_groups, int nranks, int take, int dim,
+                                 int64_t* rows, double* scores, float* syn_keys, float* syn_values);
+
+/* Accepted-thought K/V to the river GPU (drain_injections, scheduler.cpp:139-156
+ * consumes them there with cx_inject_dev): a KvBlock [n_layers][T][d_model]
+ * keys + values as one NCCL send / receive pair. */
+cx_status cx_thought_send_dev(cx_comm* comm, const float* keys, const float* values,
+                              int64_t token_count, int n_layers, int d_model, int river_rank,
+                              void* stream);
+cx_status cx_thought_recv_dev(cx_comm* comm, float* keys, float* values, int64_t token_count,
+                              int n_layers, int d_model, int src_rank, void* stream);
 
 #ifdef __cplusplus
 }

@@ -89,6 +89,24 @@ _SIGS = [
     ("cx_gather_grouped_dev", C.c_int, [c_vp, C.POINTER(CxGroups), c_vp, c_vp, C.c_int, c_vp, c_vp]),
     ("cx_selection_gaps", C.c_int, [c_vp, C.c_int, c_vp, c_vp]),
     ("cx_ctx_set_option", C.c_int, [c_vp, C.c_int, C.c_int64]),
+    ("cx_nccl_version", C.c_int, []),
+    ("cx_probe_fp64_rate", C.c_int, [c_vp, C.POINTER(C.c_double)]),
+    ("cx_comm_unique_id", C.c_int, [c_vp]),
+    ("cx_comm_init_rank", C.c_int, [C.c_int, c_vp, C.c_int, C.c_int, C.POINTER(c_vp)]),
+    ("cx_comm_init_all", C.c_int, [C.c_int, c_i32p, C.POINTER(c_vp)]),
+    ("cx_comm_destroy", C.c_int, [c_vp]),
+    ("cx_comm_info", C.c_int, [c_vp, c_i32p, c_i32p, c_i32p]),
+    ("cx_comm_group_start", C.c_int, []),
+    ("cx_comm_group_end", C.c_int, []),
+    ("cx_compress_sharded_dev", C.c_int,
+     [c_vp, c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    ("cx_synapse_record_bytes", C.c_size_t, [C.c_int, C.c_int]),
+    ("cx_synapse_pack_dev", C.c_int, [c_vp, c_vp, c_vp, c_vp, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_vp]),
+    ("cx_synapse_unpack_dev", C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    ("cx_synapse_pack_host", C.c_int, [c_vp, c_vp, c_vp, c_vp, C.c_int, C.c_int, C.c_int, C.c_int, c_vp]),
+    ("cx_synapse_unpack_host", C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_vp, c_vp, c_vp]),
+    ("cx_thought_send_dev", C.c_int, [c_vp, c_vp, c_vp, C.c_int64, C.c_int, C.c_int, C.c_int, c_vp]),
+    ("cx_thought_recv_dev", C.c_int, [c_vp, c_vp, c_vp, C.c_int64, C.c_int, C.c_int, C.c_int, c_vp]),
     ("cx_ctx_device_errors", C.c_int, [c_vp, c_vp, C.POINTER(C.c_uint), C.c_int]),
     ("cx_ctx_get_option", C.c_int, [c_vp, C.c_int, C.POINTER(C.c_int64)]),
     ("cx_compress_grouped_dev", C.c_int,

@@ -271,5 +271,13 @@ def selection_gaps(n_groups: int, device: int | None = None) -> torch.Tensor:
     return out
 
 
+def probe_fp64_rate(device: int | None = None) -> float:
+    """Unfused fp64 add / mul operations per second of this device (cx_probe_fp64_rate)."""
+    dev = torch.cuda.current_device() if device is None else device
+    r = C.c_double()
+    check(lib.cx_probe_fp64_rate(ctx(dev), C.byref(r)), "probe_fp64_rate")
+    return float(r.value)
+
+
 def kernel_launch_count() -> int:
     return int(lib.cx_kernel_launch_count())

@@ -1,5 +1,8 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): group / agent sharding
-and the single synapse all-gather exchange."""
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): group / agent
+sharding and the single synapse all-gather exchange through
+the product's host record pack / unpack.  The device path (product selection on
+each shard, device pack / unpack, the NCCL communicator) is covered by
+tests/test_gpu_parallel.py."""
 import os
 import socket
 
@@ -8,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2601_01298_b200.parallel import all_gather_groups, shard_range
+from paper_2601_01298_b200.parallel import all_gather_synapse, record_bytes, shard_range
 
 
 def test_shard_range_covers_exactly():
@@ -39,22 +42,32 @@ def _worker(rank, world, port, n_groups, q):
     try:
         b, e = shard_range(n_groups, rank, world)
         # each rank "selects" its own groups: rows = group id * 1000 + s, K/V encode (g, s)
-        take, d = 5, 3
+        take, d = 5, 4
         g = torch.arange(b, e, dtype=torch.int64)[:, None]
         rows = g * 1000 + torch.arange(take)[None]
         scores = rows.to(torch.float64) / 7
         sk = rows[..., None].to(torch.float32).expand(-1, -1, d).contiguous()
-        full = all_gather_groups([rows, scores, sk], n_groups)
+        sv = -sk
+        full = all_gather_synapse(rows, scores, sk, sv, n_groups)
         exp_rows = torch.arange(n_groups)[:, None] * 1000 + torch.arange(take)[None]
+        exp_k = exp_rows[..., None].to(torch.float32).expand(-1, -1, d)
         ok = (torch.equal(full[0], exp_rows) and torch.equal(full[1], exp_rows.to(torch.float64) / 7)
-              and torch.equal(full[2], exp_rows[..., None].to(torch.float32).expand(-1, -1, d)))
+              and torch.equal(full[2], exp_k) and torch.equal(full[3], -exp_k))
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
 
+def test_record_layout():
+    """cx_synapse_record_bytes: rows + scores + K + V of one group, padded to 256 B."""
+    assert record_bytes(164, 64) == ((164 * 16 + 164 * 64 * 8 + 255) // 256) * 256
+    assert record_bytes(1, 4) == 256
+
+
 @pytest.mark.parametrize("n_groups", [48, 7])
 def test_all_gather_synapse_world2(n_groups):
+    """The exchange step over gloo: the product's host pack / unpack
+    (cx_synapse_pack_host / unpack_host) around ONE all_gather."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -91,7 +104,7 @@ def _select_worker(rank, world, port, n_groups, q):
                for x, s in ((rows, (k,)), (scores, (k,)), (sk, (k, d)), (sv, (k, d)))]
         loc[0] = loc[0].to(torch.int64)
         loc[1] = loc[1].to(torch.float64)
-        full = all_gather_groups(loc, n_groups)
+        full = all_gather_synapse(*loc, n_groups)
         ok = True
         for gi in range(n_groups):  # every rank checks every group against a local recompute
             keys, values, queries = oracle.synthetic_group(orc, 100 + gi, L, d, 3)
