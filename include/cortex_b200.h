@@ -91,6 +91,18 @@ cx_status cx_mean_pairwise_reduction_subset(const float* cloud, int64_t count, i
  * CX_DEGENERATE_INPUT_ERROR for a zero-norm input.  Host pointers; computed on the device. */
 cx_status cx_gate_score(const float* h_main, const float* t_side, int64_t n, double* out);
 
+/* kernels.hpp:31-32 softmax(span<const double>) / softmax(span<const float>)
+ * (kernels.cpp:66-92): max-subtracted exp in fp64, the sum in index order;
+ * CX_PRECONDITION_ERROR on empty or non-finite input.  Within 1e-15 relative of
+ * the reference (CUDA exp vs glibc exp: <= 1 ulp).  out: n doubles (host). */
+cx_status cx_softmax(const double* scores, int64_t n, double* out);
+cx_status cx_softmax_f32(const float* scores, int64_t n, double* out);
+
+/* kernels.hpp:35 argmax(span<const float>) (kernels.cpp:94-101): the lowest
+ * index of the maximum (a NaN never wins, except at index 0);
+ * CX_PRECONDITION_ERROR on empty input (the reference asserts it). */
+cx_status cx_argmax(const float* v, int64_t n, int* out);
+
 /* kernels.hpp:40-42 attend(q, keys, values, n_entries, n_heads, d_k, out)
  * fp64 accumulation like the reference (tolerance 1e-6, test_kernels.cpp:159). */
 cx_status cx_attend(const float* q, const float* keys, const float* values,

@@ -161,6 +161,14 @@ class Backend:
         self._check(self._fn("softmax")(_p(s, _f64p), C.c_int64(s.size), _p(out, _f64p)), "softmax")
         return out
 
+    def argmax(self, v) -> int:
+        vv = _f32(v).reshape(-1)
+        if self.is_ref:
+            out = C.c_int()
+            self._check(self.lib.ref_argmax(_p(vv, _f32p), C.c_int64(vv.size), C.byref(out)), "argmax")
+            return int(out.value)
+        return int(self.lib.orc_argmax(_p(vv, _f32p), C.c_int64(vv.size)))
+
     def attention_scores_points(self, keys, query, n_heads: int) -> np.ndarray:
         k = _f32(keys)
         count, dim = (k.shape[0], k.shape[1]) if k.ndim == 2 else (0, int(k.shape[-1]) if k.ndim else 0)

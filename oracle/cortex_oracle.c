@@ -99,6 +99,14 @@ int orc_softmax(const double* scores, int64_t n, double* out) {
     return ORC_OK;
 }
 
+/* ---- kernels.cpp:94-101 (argmax): best = 0; i wins iff v[i] > v[best] ---- */
+int orc_argmax(const float* v, int64_t n) {
+    int best = 0;
+    for (int i = 1; i < (int)n; ++i)
+        if (v[i] > v[best]) best = i;
+    return best;
+}
+
 /* ---- synapse.cpp:63-93 ------------------------------------------------ */
 
 int orc_attention_scores_points(const float* keys, int64_t count, int dim,

@@ -56,6 +56,9 @@ void orc_rng_fill_gaussian_f32(orc_rng* r, float* dst, int64_t n, double mean, d
 /* kernels.cpp:66-81 (softmax_impl). */
 int orc_softmax(const double* scores, int64_t n, double* out);
 
+/* kernels.cpp:94-101 (argmax): lowest index of the maximum (n >= 1). */
+int orc_argmax(const float* v, int64_t n);
+
 /* synapse.cpp:63-93. */
 int orc_attention_scores_points(const float* keys, int64_t count, int dim,
                                 const float* query, int64_t query_len, int n_heads,

@@ -93,6 +93,10 @@ int ref_softmax(const double* s, int64_t n, double* out) {
     });
 }
 
+int ref_argmax(const float* v, int64_t n, int* out) {
+    return guarded([&] { *out = kernels::argmax(std::span<const float>(v, static_cast<size_t>(n))); });
+}
+
 int ref_attention_scores_points(const float* keys, int64_t count, int dim, const float* q,
                                 int64_t qlen, int n_heads, double* out) {
     return guarded([&] {

@@ -6,7 +6,7 @@ Layout:
                  + the C++ cortex:: drop-in shim (include/cortex/*.hpp)
   _lib.py        ctypes binding of libcortex_b200.so
   synapse.py     cortex::synapse API (synapse.hpp)
-  kernels.py     cortex::kernels::attend (kernels.hpp)
+  kernels.py     cortex::kernels::softmax / argmax / attend (kernels.hpp)
   gate.py        cortex::gate_score / decide (gate.hpp)
   model.py       Origin, ModelConfig, KvCache (model.hpp, config.hpp)
   injector.py    KvBlock, inject, VirtualPositionPlanner (injector.hpp)

@@ -73,6 +73,9 @@ _SIGS = [
     ("cx_hausdorff_to_subset", C.c_int, [c_f32p, C.c_int64, C.c_int, c_i64p, C.c_int64, c_f64p]),
     ("cx_mean_pairwise_reduction", C.c_int, [c_f32p, C.c_int64, C.c_int, c_f32p, C.c_int64, C.c_int, c_f64p]),
     ("cx_mean_pairwise_reduction_subset", C.c_int, [c_f32p, C.c_int64, C.c_int, c_i64p, C.c_int64, c_f64p]),
+    ("cx_softmax", C.c_int, [c_f64p, C.c_int64, c_f64p]),
+    ("cx_softmax_f32", C.c_int, [c_f32p, C.c_int64, c_f64p]),
+    ("cx_argmax", C.c_int, [c_f32p, C.c_int64, C.POINTER(C.c_int)]),
     ("cx_attend", C.c_int, [c_f32p, c_f32p, c_f32p, C.c_int64, C.c_int, C.c_int, c_f32p]),
     ("cx_gate_score", C.c_int, [c_f32p, c_f32p, C.c_int64, c_f64p]),
     ("cx_gate_decide_dev", C.c_int,

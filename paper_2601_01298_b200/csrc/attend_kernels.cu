@@ -10,6 +10,8 @@
 //   245-262) -- here the synapse is shared, not copied.  The new token's K/V
 //   is appended to the private tail first (fused), then attended, fp32
 //   accumulate (north_star tolerance 1e-3 relative).
+#include <climits>
+
 #include "cx_internal.cuh"
 
 namespace cx {
@@ -496,6 +498,96 @@ __global__ void kv_append_kernel(float* __restrict__ ck, float* __restrict__ cv,
 }
 
 }  // namespace
+
+// kernels::softmax (kernels.cpp:66-81): max-subtracted exp in fp64, the sum taken
+// SEQUENTIALLY in index order (the reference's order) by one thread, then the
+// divisions.  A non-finite input sets FLAG_NONFINITE (the reference throws
+// precondition_error before any output).  One CTA: a host-API call on a vector.
+__global__ void __launch_bounds__(1024) softmax_fp64_kernel(const double* __restrict__ s, int64_t n,
+                                                            double* __restrict__ out, int* flag) {
+    __shared__ double red[32];
+    __shared__ double sum_s;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    double mx = -INFINITY;
+    bool bad = false;
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+        const double v = s[i];
+        bad |= !isfinite(v);
+        mx = (mx < v) ? v : mx;  // std::max
+    }
+    if (__syncthreads_or(bad)) {
+        if (tid == 0) atomicOr(flag, FLAG_NONFINITE);
+        return;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = (mx < t) ? t : mx;
+    }
+    if (lane == 0) red[wid] = mx;
+    __syncthreads();
+    if (wid == 0) {
+        double v = lane < (int)(blockDim.x >> 5) ? red[lane] : -INFINITY;
+        for (int o = 16; o; o >>= 1) {
+            const double t = __shfl_xor_sync(0xffffffffu, v, o);
+            v = (v < t) ? t : v;
+        }
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    mx = red[0];
+    for (int64_t i = tid; i < n; i += blockDim.x) out[i] = exp(__dsub_rn(s[i], mx));
+    __syncthreads();
+    if (tid == 0) {
+        double acc = 0.0;
+        for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, out[i]);
+        sum_s = acc;
+    }
+    __syncthreads();
+    const double sum = sum_s;
+    for (int64_t i = tid; i < n; i += blockDim.x) out[i] = __ddiv_rn(out[i], sum);
+}
+
+// kernels::argmax (kernels.cpp:94-101): best = 0, then i wins iff v[i] > v[best]:
+// the lowest index of the maximum; a NaN never wins, except v[0] (nothing beats it)
+__global__ void __launch_bounds__(1024) argmax_f32_kernel(const float* __restrict__ v, int64_t n, int* out) {
+    __shared__ float bv[32];
+    __shared__ int bi[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    float best = NAN;
+    int idx = INT_MAX;
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+        const float x = v[i];
+        if (isnan(x)) continue;
+        if (idx == INT_MAX || x > best) { best = x; idx = (int)i; }  // i ascending per thread: first max kept
+    }
+    for (int o = 16; o; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (oi != INT_MAX && (idx == INT_MAX || ob > best || (ob == best && oi < idx))) { best = ob; idx = oi; }
+    }
+    if (lane == 0) { bv[wid] = best; bi[wid] = idx; }
+    __syncthreads();
+    if (wid == 0) {
+        best = lane < (int)(blockDim.x >> 5) ? bv[lane] : NAN;
+        idx = lane < (int)(blockDim.x >> 5) ? bi[lane] : INT_MAX;
+        for (int o = 16; o; o >>= 1) {
+            const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (oi != INT_MAX && (idx == INT_MAX || ob > best || (ob == best && oi < idx))) { best = ob; idx = oi; }
+        }
+        if (lane == 0) *out = (isnan(v[0]) || idx == INT_MAX) ? 0 : idx;
+    }
+}
+
+void softmax_fp64(const double* s, int64_t n, double* out, int* flag, cudaStream_t st) {
+    softmax_fp64_kernel<<<1, 1024, 0, st>>>(s, n, out, flag);
+    check_launch("softmax_fp64_kernel");
+}
+
+void argmax_f32(const float* v, int64_t n, int* out, cudaStream_t st) {
+    argmax_f32_kernel<<<1, 1024, 0, st>>>(v, n, out);
+    check_launch("argmax_f32_kernel");
+}
 
 void attend_fp64_ws(const float* q, const float* k, const float* v, int64_t n, int H, int dk, double* w,
                     float* out, cudaStream_t s) {

@@ -467,6 +467,60 @@ extern "C" cx_status cx_attend(const float* q, const float* keys, const float* v
     });
 }
 
+// kernels::softmax (kernels.cpp:66-92): precondition_error on empty or non-finite input
+extern "C" cx_status cx_softmax(const double* scores, int64_t n, double* out) {
+    return guard([&] {
+        if (n < 1) fail(CX_PRECONDITION_ERROR, "softmax: empty input");
+        if (!scores || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
+        cx_ctx* c = default_ctx();
+        std::lock_guard<std::mutex> lk(c->mu);
+        ArenaPlan pl;
+        pl.take<double>((size_t)n);
+        pl.take<double>((size_t)n);
+        c->arena.reserve(pl.used);
+        c->arena.reset();
+        double* ds = c->arena.take<double>((size_t)n);
+        double* dout = c->arena.take<double>((size_t)n);
+        CX_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        h2d(ds, scores, sizeof(double) * n, c->stream);
+        softmax_fp64(ds, n, dout, c->d_flag, c->stream);
+        d2h(out, dout, sizeof(double) * n, c->stream);
+        check_flag_and_sync(c);
+    });
+}
+
+// the float overload widens first (kernels.cpp:89-92)
+extern "C" cx_status cx_softmax_f32(const float* scores, int64_t n, double* out) {
+    return guard([&] {
+        if (n < 1) fail(CX_PRECONDITION_ERROR, "softmax: empty input");
+        if (!scores || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
+        std::vector<double> w(scores, scores + n);
+        const cx_status st = cx_softmax(w.data(), n, out);
+        if (st != CX_OK) fail(st, cx_last_error());
+    });
+}
+
+// kernels::argmax (kernels.cpp:94-101); the reference asserts a non-empty input
+extern "C" cx_status cx_argmax(const float* v, int64_t n, int* out) {
+    return guard([&] {
+        if (n < 1) fail(CX_PRECONDITION_ERROR, "argmax: empty input");
+        if (!v || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
+        cx_ctx* c = default_ctx();
+        std::lock_guard<std::mutex> lk(c->mu);
+        ArenaPlan pl;
+        pl.take<float>((size_t)n);
+        pl.take<int>(1);
+        c->arena.reserve(pl.used);
+        c->arena.reset();
+        float* dv = c->arena.take<float>((size_t)n);
+        int* di = c->arena.take<int>(1);
+        h2d(dv, v, sizeof(float) * n, c->stream);
+        argmax_f32(dv, n, di, c->stream);
+        d2h(out, di, sizeof(int), c->stream);
+        CX_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
 // gate.cpp:27-43 gate_score for one (h_main, t_side) pair, on the device
 extern "C" cx_status cx_gate_score(const float* h_main, const float* t_side, int64_t n, double* out) {
     return guard([&] {

@@ -353,6 +353,24 @@ void SynapseBuffer::shutdown() {
 
 // ---- kernels.hpp ---------------------------------------------------------------
 namespace kernels {
+std::vector<double> softmax(std::span<const double> scores) {
+    std::vector<double> out(scores.size());
+    ck(cx_softmax(scores.data(), static_cast<int64_t>(scores.size()), out.data()));
+    return out;
+}
+
+std::vector<double> softmax(std::span<const float> scores) {
+    std::vector<double> out(scores.size());
+    ck(cx_softmax_f32(scores.data(), static_cast<int64_t>(scores.size()), out.data()));
+    return out;
+}
+
+int argmax(std::span<const float> v) {
+    int out = 0;
+    ck(cx_argmax(v.data(), static_cast<int64_t>(v.size()), &out));
+    return out;
+}
+
 void attend(std::span<const float> q, std::span<const float> keys, std::span<const float> values, int64_t n_entries,
             int n_heads, int d_k, std::span<float> out) {
     ck(cx_attend(q.data(), keys.data(), values.data(), n_entries, n_heads, d_k, out.data()));

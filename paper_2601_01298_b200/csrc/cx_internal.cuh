@@ -205,6 +205,9 @@ size_t mean_pairwise_scratch(int64_t count, int dim);
 void mean_pairwise(const float* pts, int64_t count, int dim, const int64_t* rows, double* out_sum,
                    cudaStream_t s);
 
+// kernels::softmax / argmax (kernels.cpp:66-101), one vector per call
+void softmax_fp64(const double* s, int64_t n, double* out, int* flag, cudaStream_t st);
+void argmax_f32(const float* v, int64_t n, int* out, cudaStream_t st);
 // attend (reference-shaped, fp64 accumulate)
 void attend_fp64_ws(const float* q, const float* k, const float* v, int64_t n, int H, int dk,
                     double* w /* [H][n] scratch */, float* out, cudaStream_t s);

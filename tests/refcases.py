@@ -5,12 +5,12 @@ and run against any implementation with the point-level API:
   * the B200 product (GPU, tests/test_gpu_parity.py) -- parity.
 
 Sources (file:line under /root/reference/proj/tests):
-  test_synapse.cpp:87-396, test_kernels.cpp:131-163, acceptance.cpp:147-187.
+  test_synapse.cpp:87-396, test_kernels.cpp:72-163, acceptance.cpp:147-187.
 
 An ``api`` object provides: attention_scores_points, coverage_scores_points,
 select_landmarks_points -> (idx, scores), hausdorff_distance,
 hausdorff_to_subset, mean_pairwise_reduction, mean_pairwise_reduction_subset,
-attend, rng(seed) (cortex::Rng), and error_kind(exc) -> reference type name.
+attend, softmax, argmax, rng(seed) (cortex::Rng), and error_kind(exc) -> reference type name.
 """
 from __future__ import annotations
 
@@ -232,6 +232,39 @@ def case_attend(api):
             assert abs(out[h * dk + c] - acc[c]) <= 1e-6 * max(1.0, abs(acc[c]))
 
 
+# ---- test_kernels.cpp:72-114: softmax / argmax known answers --------------------
+
+def case_softmax_uniform(api):  # :72-76
+    p = api.softmax(np.full(7, 4.2))
+    assert all(_approx(v, 1.0 / 7.0) for v in p)
+
+
+def case_softmax_scalar(api):  # :78-90
+    p = api.softmax(np.array([1.0, 2.0, 3.0]))
+    e1, e2, e3 = math.exp(1.0 - 3.0), math.exp(2.0 - 3.0), 1.0
+    z = e1 + e2 + e3
+    assert abs(p[0] - e1 / z) < 1e-12 and abs(p[1] - e2 / z) < 1e-12 and abs(p[2] - e3 / z) < 1e-12
+    assert abs(sum(p) - 1.0) < 1e-9
+
+
+def case_softmax_gap(api):  # :92-101
+    prev = 0.0
+    for gap in range(1, 31):
+        p = api.softmax(np.array([0.0, float(gap)]))
+        assert p[1] > prev
+        prev = p[1]
+    assert prev > 1.0 - 1e-12
+
+
+def case_softmax_errors(api):  # :103-110
+    expect_error(api, "precondition_error", api.softmax, np.zeros(0))
+    expect_error(api, "precondition_error", api.softmax, np.array([1.0, math.inf]))
+
+
+def case_argmax_ties(api):  # :112-115
+    assert api.argmax(np.array([0.5, 2.0, 2.0, -1.0], np.float32)) == 1
+
+
 # ---- acceptance.cpp:147-187 (AC3) ---------------------------------------------
 
 def paired_cluster_cloud(dim, per_cluster):
@@ -269,4 +302,5 @@ ALL_CASES = [
     case_uniform_attention, case_two_key_attention, case_per_head_sum, case_empty_attention, case_coverage,
     case_saturation, case_config_errors, case_lambda0_topk, case_ties, case_two_clusters,
     case_incremental_equals_scratch, case_hausdorff, case_mean_pairwise, case_attend, case_ac3,
+    case_softmax_uniform, case_softmax_scalar, case_softmax_gap, case_softmax_errors, case_argmax_ties,
 ]

@@ -73,6 +73,12 @@ class ProductApi:
     def attend(self, q, k, v, n, H, dk):
         return self.cx.attend(q, k, v, n, H, dk)
 
+    def softmax(self, s):
+        return self.cx.kernels.softmax(s)
+
+    def argmax(self, v):
+        return self.cx.kernels.argmax(v)
+
 
 def rel_close(a, b, rtol):
     a = np.asarray(a, np.float64)
