@@ -172,6 +172,10 @@ cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* a
 #define CX_OPT_DECODE_IMPL 3        /* CX_DECODE_* below */
 #define CX_OPT_DECODE_CTAS_PER_LH 4 /* tcgen05 decode CTAs per (layer, KV head); 0 = auto */
 #define CX_OPT_HOST_UPLOAD_VALUES 5 /* 1 = host path uploads all values even if pinned */
+#define CX_OPT_SELECT_IMPL 6        /* CX_SELECT_IMPL_* below */
+#define CX_SELECT_IMPL_AUTO 0       /* tensor-core filter (d = 64), then CUDA-core, then generic */
+#define CX_SELECT_IMPL_TC 1         /* pinned: an error if the shape does not apply */
+#define CX_SELECT_IMPL_CUDA_CORE 2  /* the CUDA-core filter kernels (select64 / select128) */
 #define CX_DECODE_AUTO 0            /* tcgen05, then v2, then the generic kernel */
 #define CX_DECODE_TC 1              /* pinned: an error if the shape does not apply */
 #define CX_DECODE_V2 2

@@ -54,6 +54,7 @@ inline void kernel_smem(K* fn, size_t bytes, bool nonportable_cluster = false) {
 struct Options {
     int select_cluster = 0;      // CX_OPT_SELECT_CLUSTER: force the selection cluster size (0 = cost model)
     int select_no_sketch = 0;    // CX_OPT_SELECT_NO_SKETCH: never use the fp16 sketch row mode
+    int select_impl = 0;         // CX_OPT_SELECT_IMPL: CX_SELECT_IMPL_{AUTO,TC,CUDA_CORE}
     int decode_impl = 0;         // CX_OPT_DECODE_IMPL: CX_DECODE_{AUTO,TC,V2,V1}
     int decode_ctas_per_lh = 0;  // CX_OPT_DECODE_CTAS_PER_LH: tcgen05 decode CTAs per (layer, KV head) (0 = auto)
     int host_upload_values = 0;  // CX_OPT_HOST_UPLOAD_VALUES: host path uploads all values even when pinned
@@ -182,6 +183,12 @@ int select64_wave(int64_t L, int G);
 // centroid_of for every group (synapse.cpp:36-44), bit-exact sequential sums
 void centroid_launch(const GroupView& g, double* cen, cudaStream_t s);
 void plan_select(ArenaPlan& p, const GroupView& g, int k);
+// d = 64 with the tensor-core filter and TMEM-resident rows (select_tc.cu); false when it
+// does not apply
+bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
+                      double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows,
+                      double* scores, double* gaps, double* gap_rec, cudaStream_t s);
+int select_tc_wave(int64_t L, int G);
 // dim-64 fast path (select64.cu); false when it does not apply
 bool select64_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
                      double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,

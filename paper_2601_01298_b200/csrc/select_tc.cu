@@ -1,0 +1,978 @@
+// select_tc.cu -- the greedy hybrid selection (SURVEY.md §8(a) A4/A6,
+// synapse.cpp:216-284) for d = 64 with the distance filter on the 5th-generation
+// tensor cores and every row on chip, so that cfg2's 48 groups run in ONE wave.
+//
+// Why: the selection is k dependent rounds; per round every remaining row needs
+// min(m_i, |x_i - b|) against the new pick b.  On-chip capacity decides the wave
+// count: cfg2 holds 48 x 8192 rows, 2657 rows per SM for a single wave -- 340 KB
+// as fp16, more than shared memory.  Here a CTA keeps its rows as an fp16 SKETCH
+// split between shared memory (UMMA core-matrix tiles) and TENSOR MEMORY (the A
+// operand of tcgen05.mma may live in TMEM), up to 22 tiles of 128 rows = 2816
+// rows per CTA.  Per round ONE thread issues the filter GEMV on the tensor cores:
+// D[row] = x~ . [b_hi | b_lo] (M = 128 rows per MMA, N = 8, K = 64 in 4 steps,
+// fp32 accumulate in TMEM), every thread reads its rows' dots with tcgen05.ld and
+// forms the conservative lower bound of the Gram form; only rows
+// the bound cannot rule out are evaluated exactly -- in fp64, in the reference's
+// operation order, from the fp32 row in global memory (L2).  No fp32 row is kept
+// in registers, so the 512 threads carry just the per-row state.
+//
+// The cluster exchanges (X1 min / max, X2 candidates) and the exact hybrid argmax
+// are the select64 protocol: every decision is bit-identical to
+// the reference.
+//
+// Rows: thread (warp w, lane l) owns rows tile*128 + 32 (w % 4) + l of the tiles
+// j = w / 4 + 4 k, k = 0..RPT-1 (tcgen05.ld: a warp reads the TMEM lanes of its
+// sub-partition w % 4).  Tiles [0, n_smem) are in shared memory, [n_smem, n_tiles)
+// in TMEM columns [tm_rows_col + 32 (j - n_smem), +32).
+#include <cooperative_groups.h>
+#include <cuda_fp16.h>
+
+#include <map>
+#include <mutex>
+
+#include "cx_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace cx {
+
+namespace {
+
+constexpr int D = 64;
+constexpr int NT = 512;
+constexpr int NW = NT / 32;
+constexpr int TILE = 128;         // rows per MMA (M)
+constexpr int MAXT = 22;          // tiles per CTA: 2816 rows
+constexpr int DC = 8;             // TMEM columns of one tile's D (N = 8)
+constexpr int MAXC = 16;
+constexpr int TILE_BYTES = TILE * D * 2;  // one fp16 A tile: 16 KB
+constexpr double GAP_WINDOW = 1e-10;      // as select64.cu (gap monitor + exact window)
+static_assert(MAXC == kGapRecStride, "gap-monitor record stride");
+static_assert(MAXT * DC <= 512 - 32 * 10, "D and 10 row tiles fill TMEM at 22 tiles");
+// first TMEM column of the row tiles: after the tiles' D columns (8 per tile)
+__host__ __device__ inline int tm_rows_col(int n_tiles) { return (DC * n_tiles + 31) / 32 * 32; }
+
+__device__ __forceinline__ double dmin_std(double a, double b) { return (b < a) ? b : a; }
+// Every value reduced below is a non-negative double (attention mass, distances, hybrid
+// scores in [0, 1]; never -0.0), and those order like their bit patterns as unsigned
+// integers: warp min / max are two redux.sync on the 32-bit halves.
+__device__ __forceinline__ unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }
+__device__ __forceinline__ double bitsd(unsigned long long b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ unsigned long long wmax64(unsigned long long v) {
+    const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+    const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned long long wmin64(unsigned long long v) {
+    const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+    const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return ((unsigned long long)mh << 32) | ml;
+}
+constexpr unsigned long long BITS_INF = 0x7FF0000000000000ull;  // +inf: the min identity (max: 0)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+    const uint32_t a = su32(m);
+    uint32_t ok = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+// TMA bulk copy global -> shared completing on an mbarrier (transaction bytes)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(mbar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(su32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(m)) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint64_t a, uint64_t b, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "l"(a), "l"(b), "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+                 "r"(__float_as_uint(v.w)), "r"(rmbar)
+                 : "memory");
+}
+
+// ---- tcgen05 helpers ----
+// K-major SWIZZLE_NONE core-matrix layout: 8 rows x 16 B core matrices, row groups
+// 128 B apart (SBO), 8-element K chunks (R / 8) * 128 B apart (LBO)
+__host__ __device__ __forceinline__ uint32_t cm_off(int r, int k, int R) {
+    return (uint32_t)((((k >> 3) * (R >> 3) + (r >> 3)) << 7) + ((r & 7) << 4) + ((k & 7) << 1));
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    return d;                // SWIZZLE_NONE, base offset 0
+}
+// kind::f16 instruction descriptor: A = B = fp16 (format 0), D = fp32, K-major A and B
+__host__ __device__ __forceinline__ uint32_t idesc_f16_f32(int m, int n) {
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_ss(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(dt),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ts(uint32_t dt, uint32_t at, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(dt),
+        "r"(at), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// warp-uniform issue: the whole warp runs the code (operands stay in uniform registers),
+// one elected lane issues -- ~10x cheaper per MMA than a divergent single thread (measured)
+__device__ __forceinline__ void mma_ss_elect(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{ .reg .pred p, e; setp.ne.b32 p, %4, 0; elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(dt),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ts_elect(uint32_t dt, uint32_t at, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{ .reg .pred p, e; setp.ne.b32 p, %4, 0; elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(dt),
+        "r"(at), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* mbar) {
+    asm volatile(
+        "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(su32(mbar))
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mbar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+        "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+        "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr));
+}
+
+// exact sq_dist(x, b) in the reference's order (synapse.cpp:18-25); x read as float4
+template <class Get4>
+__device__ __forceinline__ double exact_sq(Get4 get4, const float* b) {
+    double acc = 0.0;
+#pragma unroll
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 v = get4(c4);
+        const float4 w = reinterpret_cast<const float4*>(b)[c4];
+        double d = __dsub_rn((double)v.x, (double)w.x);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.y, (double)w.y);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.z, (double)w.z);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        d = __dsub_rn((double)v.w, (double)w.w);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    return acc;
+}
+
+// Lower bound of the fp64 squared distance from the tensor-core Gram form.
+// dot = x~ . (b_hi + b_lo): x~ = fp16(x) (|x_c - x~_c| <= 2^-11 |x_c| + 2^-25), b_hi + b_lo
+// = b to 2^-22 |b_c| + 2^-25, products exact in fp32, 64 fp32 accumulations (<= 2^-17 of the
+// absolute sum even with truncating adds).  With 2 |x.b| <= |x|^2 + |b|^2 and |x| + |b| <=
+// 1 + (|x|^2 + |b|^2) / 2, every term is covered by 2^-9.9 (|x|^2 + |b|^2) + 2^-19, plus the
+// fp32 roundings of the bound itself.  An fp16 overflow (|x_c| or |b_c| > 65504) makes the
+// dot non-finite: then nothing is bounded and the row is evaluated exactly.
+__device__ __forceinline__ float tc_lower_bound(float nx, float nb, float dot) {
+    const float sum = __fadd_rn(nx, nb);
+    const float s = __fsub_rn(sum, __fmul_rn(2.0f, dot));
+    const float e = __fmaf_ru(0x1.1p-10f, sum, 0x1p-19f);
+    return isfinite(dot) ? __fsub_rd(s, e) : -INFINITY;
+}
+
+struct SelxParams {
+    const float* X;
+    int64_t gstride, rstride;
+    int64_t L;
+    const double* attn;  // [G][L]
+    const double* cen;   // [G][D]
+    int take;
+    double lambda;
+    int S;               // rows per CTA
+    int n_tiles;         // ceil(S / 128)
+    int n_smem;          // tiles in shared memory (the rest in TMEM)
+    int n_stage;         // staging slots for the exact rows (TMA bulk copies)
+    int filter;
+    int64_t* pick_rows;
+    double* pick_scores;
+    int64_t* out_rows;
+    double* out_scores;
+    double* gaps;
+    long long* trace;  // CX_EXPERIMENTS builds: per-round phase clocks of group 0, rank 0
+};
+
+#ifdef CX_EXPERIMENTS
+#define XSTAMP(k)                                                                         \
+    do {                                                                                  \
+        if (p.trace && tid == 0 && rank == 0 && g == 0 && round < 4096) p.trace[round * 16 + (k)] = clock64(); \
+    } while (0)
+#else
+#define XSTAMP(k) \
+    do {          \
+    } while (0)
+#endif
+
+struct alignas(16) Hdr {
+    double score;
+    long long row;
+    double nb;
+    double second;
+};
+
+struct SelxLayout {
+    size_t mbar, mm, hdr, bc, misc, qrow, qres, bop, stage, tiles, total;
+};
+
+__host__ __device__ inline size_t al(size_t x, size_t a = 16) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline SelxLayout selx_layout(int n_smem, int C, int n_stage) {
+    SelxLayout l;
+    size_t o = 0;
+    l.mbar = o;  o = al(o + 5 * sizeof(uint64_t));
+    l.mm = o;    o = al(o + sizeof(double) * 4 * C * NW);  // X1: one slot per (CTA, warp)
+    l.hdr = o;   o = al(o + sizeof(Hdr) * C * NW);        // X2: one candidate per (CTA, warp)
+    l.bc = o;    o = al(o + sizeof(float) * D * C * NW);
+    l.misc = o;  o = al(o + sizeof(unsigned long long) * 8);
+    l.qrow = o;  o = al(o + sizeof(int) * NT);         // exact-evaluation queue: local row
+    l.qres = o;  o = al(o + sizeof(double) * 2 * NT);  // ... and its (d^2, d)
+    l.bop = o;   o = al(o + 8 * D * 2, 1024);  // B operand: 8 rows (b_hi, b_lo, 0...) x 64 fp16
+    l.stage = o; o = al(o + (size_t)n_stage * D * sizeof(float), 1024);  // exact rows (fp32)
+    l.tiles = o; o = al(o + (size_t)n_smem * TILE_BYTES, 1024);
+    l.total = o;
+    return l;
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const uint32_t C = cluster.num_blocks();
+    const uint32_t rank = cluster.block_rank();
+    const int g = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int sub = wid & 3, quad = wid >> 2;  // TMEM sub-partition, tile phase
+    const int64_t r0 = (int64_t)rank * p.S;
+    const int nrows = (int)max((int64_t)0, min((int64_t)p.S, p.L - r0));
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const SelxLayout lay = selx_layout(p.n_smem, (int)C, p.n_stage);
+    float* stage = reinterpret_cast<float*>(smem + lay.stage);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);  // [0] X1, [1] X2, [2] MMA, [3] TMEM base, [4] stage
+    double* mm = reinterpret_cast<double*>(smem + lay.mm);
+    Hdr* hdr = reinterpret_cast<Hdr*>(smem + lay.hdr);
+    float* bc = reinterpret_cast<float*>(smem + lay.bc);
+    unsigned long long* misc = reinterpret_cast<unsigned long long*>(smem + lay.misc);
+    int* qrow = reinterpret_cast<int*>(smem + lay.qrow);
+    double* qres = reinterpret_cast<double*>(smem + lay.qres);
+    unsigned char* bop = smem + lay.bop;
+    unsigned char* tiles = smem + lay.tiles;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(&mbar[3]);
+    int* qn = reinterpret_cast<int*>(&misc[0]);
+    unsigned long long* min_gap = &misc[5];
+
+    const float* gX = p.X + g * p.gstride + r0 * p.rstride;
+
+    // the CTA's fp32 rows -> L2 (the exact evaluations and the winners' coordinates read them
+    // from global memory every round: an L2 hit instead of an HBM round trip)
+    if (p.rstride == D) {
+        const char* base = reinterpret_cast<const char*>(gX);
+        const size_t bytes = (size_t)nrows * D * sizeof(float);
+        for (size_t o = (size_t)tid * 4096; o < bytes; o += (size_t)NT * 4096)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"((uint32_t)min((size_t)4096, bytes - o))
+                         : "memory");
+    }
+    if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tbase_s)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int e = tid; e < 8 * D * 2 / 16; e += NT) reinterpret_cast<uint4*>(bop)[e] = make_uint4(0, 0, 0, 0);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = *tbase_s;
+
+    // ---- rows: per-row state in registers, fp16 sketch in shared memory / TMEM ----
+    double m[RPT], a[RPT];
+    float th[RPT], nx[RPT];
+    uint32_t remm = 0;
+    {
+        const double* cen = p.cen + (int64_t)g * D;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            m[k] = 0.0; a[k] = 0.0; th[k] = INFINITY; nx[k] = 0.f;
+            const int j = quad + 4 * k;
+            if (j >= p.n_tiles) continue;
+            const int li = j * TILE + 32 * sub + lane;
+            const bool valid = li < nrows;
+            float x[D];
+            if (valid) {
+                const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)li * p.rstride);
+#pragma unroll
+                for (int c4 = 0; c4 < D / 4; ++c4) {
+                    const float4 v = __ldg(src + c4);
+                    x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
+                }
+                a[k] = p.attn[(int64_t)g * p.L + r0 + li];
+                // coverage init: distance to the centroid (synapse.cpp:107-112, sq_dist :27-34)
+                double acc = 0.0, n2 = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const double d = __dsub_rn((double)x[c], cen[c]);
+                    acc = __dadd_rn(acc, __dmul_rn(d, d));
+                    n2 += (double)x[c] * x[c];
+                }
+                m[k] = __dsqrt_rn(acc);
+                nx[k] = (float)n2;
+                remm |= 1u << k;
+            } else {
+#pragma unroll
+                for (int c = 0; c < D; ++c) x[c] = 0.f;
+            }
+            // the fp16 sketch (padding rows are zero and never enter a decision)
+            uint32_t h[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const __half2 v = __floats2half2_rn(x[2 * u], x[2 * u + 1]);
+                h[u] = *reinterpret_cast<const uint32_t*>(&v);
+            }
+            if (j < p.n_smem) {
+                unsigned char* t = tiles + (size_t)j * TILE_BYTES;
+                const int r = 32 * sub + lane;
+#pragma unroll
+                for (int c = 0; c < D / 8; ++c)
+                    *reinterpret_cast<uint4*>(t + cm_off(r, 8 * c, TILE)) =
+                        make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+            } else {
+                tmem_st32(tbase + ((uint32_t)(32 * sub) << 16) + (uint32_t)(tm_rows_col(p.n_tiles) + 32 * (j - p.n_smem)), h);
+            }
+        }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        mbar_init(&mbar[2], (uint32_t)min(p.n_tiles, NW));  // one commit per MMA-issuing warp
+        mbar_init(&mbar[4], 1);  // the exact rows' bulk copies (tx bytes) + one arrival
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        *qn = 0;
+        *min_gap = (unsigned long long)__double_as_longlong(GAP_WINDOW);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster.sync();  // mbarriers visible cluster-wide before any remote push
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tx1 = C * NW * 32u, tx2 = C * NW * (uint32_t)(sizeof(Hdr) + D * sizeof(float));
+    if (tid == 0) {
+        mbar_arrive_expect(&mbar[0], tx1);
+        mbar_arrive_expect(&mbar[1], tx2);
+    }
+
+    const double lam = p.lambda;
+    const double one_m_lam = __dsub_rn(1.0, lam);
+    int64_t* pick_rows = p.pick_rows + (int64_t)g * p.take;
+    double* pick_scores = p.pick_scores + (int64_t)g * p.take;
+    uint32_t ph1 = 0, ph2 = 0, ph3 = 0, ph4 = 0;
+    const float* bw = nullptr;  // the previous round's winner coordinates (in bc)
+    float nbw = 0.f;
+    const uint32_t idesc = idesc_f16_f32(TILE, 8);
+    // MMA operands that never change: B descriptors per k-step, the A descriptor of shared tile 0,
+    // the first TMEM column of the row tiles
+    uint64_t bdesc[D / 16];
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) bdesc[kk] = sdesc(su32(bop) + kk * 2 * 128, 128, 128);
+    const uint64_t adesc0 = sdesc(su32(tiles), (TILE / 8) * 128, 128);
+    const uint32_t tm_col = (uint32_t)tm_rows_col(p.n_tiles);
+
+    for (int round = 0; round < p.take; ++round) {
+        XSTAMP(0);
+        // ======== U: distance update against the previous pick ========
+        if (round > 0) {
+            const bool assign = (round == 1);  // the first pick REPLACES the centroid distances
+            const bool use_tc = !assign && p.filter;
+            if (use_tc) {
+                // B = [b_hi; b_lo; 0 ...] (fp16, K-major core matrices), then one thread issues
+                // the filter GEMV over every tile: D[:, 0] = x~ . b_hi, D[:, 1] = x~ . b_lo
+                if (tid < D) {
+                    const float bcv = bw[tid];
+                    const __half hi = __float2half_rn(bcv);
+                    const __half lo = __float2half_rn(bcv - __half2float(hi));
+                    *reinterpret_cast<__half*>(bop + cm_off(0, tid, 8)) = hi;
+                    *reinterpret_cast<__half*>(bop + cm_off(1, tid, 8)) = lo;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
+                __syncthreads();  // the B operand is written
+                // The filter GEMV.  A tcgen05.mma costs its issuing thread ~200 cycles at this
+                // size (descriptors to uniform registers), so lane 0 of EVERY warp issues the
+                // MMAs of tiles w, w + 16 (k-step major), and commits: the mbarrier counts one
+                // arrival per issuing warp.
+                if (wid < p.n_tiles) {  // warp-uniform: tiles wid, wid + NW, k-step major per tile
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    for (int j = wid; j < p.n_tiles; j += NW) {
+                        const uint32_t dt = tbase + (uint32_t)(DC * j);
+                        if (j >= p.n_smem) {
+                            const uint32_t at = tbase + (uint32_t)(tm_col + 32 * (j - p.n_smem));
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) mma_ts_elect(dt, at + 8 * kk, bdesc[kk], idesc, kk);
+                        } else {
+                            const uint64_t ad = adesc0 + (uint64_t)((j * TILE_BYTES) >> 4);
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk)
+                                mma_ss_elect(dt, ad + (uint64_t)((kk * 2 * (TILE / 8) * 128) >> 4), bdesc[kk], idesc, kk);
+                        }
+                    }
+                    mma_commit_elect(&mbar[2]);
+                }
+                mbar_wait(&mbar[2], ph3);
+                ph3 ^= 1u;
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            XSTAMP(1);
+            float dot[RPT];
+            if (use_tc) {
+                uint32_t dh[RPT], dl[RPT];
+#pragma unroll
+                for (int k = 0; k < RPT; ++k) {
+                    const int j = quad + 4 * k;
+                    dh[k] = dl[k] = 0u;
+                    if (j < p.n_tiles) tmem_ld2(tbase + ((uint32_t)(32 * sub) << 16) + (uint32_t)(DC * j), dh[k], dl[k]);
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < RPT; ++k) dot[k] = __uint_as_float(dh[k]) + __uint_as_float(dl[k]);
+            }
+            // rows the bound cannot rule out are evaluated exactly in fp64 from their fp32 row
+            // in global memory (L2).  Rounds >= 2 (~3% of rows): a block-wide queue, one
+            // evaluator thread per queued row, so all the row reads are one round trip.  Round 1
+            // (every row, it replaces the centroid distances): each owner evaluates its rows.
+            uint32_t need = 0;
+#pragma unroll
+            for (int k = 0; k < RPT; ++k)
+                if ((remm >> k & 1u) && (!use_tc || !(tc_lower_bound(nx[k], nbw, dot[k]) > th[k]))) need |= 1u << k;
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");  // D read before the next MMA
+            int slot[RPT];
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                slot[k] = -1;
+                if (!assign && (need >> k & 1u)) {
+                    const int sl = atomicAdd(qn, 1);
+                    if (sl < NT) {
+                        slot[k] = sl;
+                        const int li = (quad + 4 * k) * TILE + 32 * sub + lane;
+                        qrow[sl] = li;
+                        need &= ~(1u << k);
+                        if (sl < p.n_stage) {  // the row starts moving now (TMA), not after the barrier
+                            mbar_expect_tx(&mbar[4], D * sizeof(float));
+                            bulk_g2s(stage + sl * D, gX + (int64_t)li * p.rstride, D * sizeof(float), &mbar[4]);
+                        }
+                    }
+                }
+            }
+            while (__any_sync(0xffffffffu, need != 0)) {  // round 1, or a queue overflow
+                const int k = need ? __ffs(need) - 1 : 0;
+                const int li = (quad + 4 * k) * TILE + 32 * sub + lane;
+                const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)li * p.rstride);
+                float4 x4[D / 4];
+#pragma unroll
+                for (int c4 = 0; c4 < D / 4; ++c4) x4[c4] = need ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const double d2 = exact_sq([&](int c4) { return x4[c4]; }, bw);
+                const double d = __dsqrt_rn(d2);
+#pragma unroll
+                for (int kk = 0; kk < RPT; ++kk) {
+                    if (need && kk == k && (assign || d < m[kk])) {
+                        m[kk] = d;
+                        th[kk] = __double2float_ru(d2);
+                    }
+                }
+                need &= need - 1;
+            }
+            __syncthreads();
+            XSTAMP(2);
+            const int nq = min(*qn, NT);
+            if (!assign) {
+                if (tid == 0) mbar_arrive(&mbar[4]);  // every expect_tx is in: the phase ends with the copies
+                if (tid < nq) {
+                    double d2;
+                    if (tid < p.n_stage) {
+                        mbar_wait(&mbar[4], ph4);
+                        const float4* st = reinterpret_cast<const float4*>(stage + tid * D);
+                        d2 = exact_sq([&](int c4) { return st[c4]; }, bw);
+                    } else {
+                        const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)qrow[tid] * p.rstride);
+                        float4 x4[D / 4];
+#pragma unroll
+                        for (int c4 = 0; c4 < D / 4; ++c4) x4[c4] = __ldg(src + c4);
+                        d2 = exact_sq([&](int c4) { return x4[c4]; }, bw);
+                    }
+                    qres[2 * tid] = d2;
+                    qres[2 * tid + 1] = __dsqrt_rn(d2);
+                }
+                ph4 ^= 1u;
+            }
+            __syncthreads();
+            XSTAMP(3);
+#ifdef CX_EXPERIMENTS
+            if (p.trace && tid == 0 && rank == 0 && g == 0 && round < 4096) p.trace[round * 16 + 8] = *qn;
+#endif
+            if (tid == 0) *qn = 0;  // next use is after >= 2 more barriers
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                if (slot[k] < 0) continue;
+                const double d2 = qres[2 * slot[k]], d = qres[2 * slot[k] + 1];
+                if (d < m[k]) {  // std::min (round 1 never queues)
+                    m[k] = d;
+                    th[k] = __double2float_ru(d2);
+                }
+            }
+        }
+
+        // ======== X1: cluster-wide min/max over remaining rows ========
+        double amin, amax, cmin, cmax;
+        {
+            unsigned long long b0 = BITS_INF, b1 = 0ull, b2_ = BITS_INF, b3 = 0ull;
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                if (!(remm >> k & 1u)) continue;
+                b0 = min(b0, dbits(a[k]));
+                b1 = max(b1, dbits(a[k]));
+                b2_ = min(b2_, dbits(m[k]));
+                b3 = max(b3, dbits(m[k]));
+            }
+            b0 = wmin64(b0);
+            b1 = wmax64(b1);
+            b2_ = wmin64(b2_);
+            b3 = wmax64(b3);
+            // every warp pushes its partial straight to every CTA of the cluster (no block-level
+            // reduction first): C x NW slots of 32 B, one mbarrier
+            if (lane < (int)C) {
+                const uint32_t dst = mapa(su32(mm + ((int)rank * NW + wid) * 4), lane);
+                const uint32_t mb = mapa(su32(&mbar[0]), lane);
+                st_async_v2(dst, b0, b1, mb);
+                st_async_v2(dst + 16, b2_, b3, mb);
+            }
+            XSTAMP(9);
+            mbar_wait(&mbar[0], ph1);
+            ph1 ^= 1u;
+            XSTAMP(4);
+            if (tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[0], tx1);
+            const unsigned long long* mb64 = reinterpret_cast<const unsigned long long*>(mm);
+            b0 = BITS_INF; b1 = 0ull; b2_ = BITS_INF; b3 = 0ull;
+            for (int e = lane; e < (int)C * NW; e += 32) {
+                b0 = min(b0, mb64[e * 4 + 0]);
+                b1 = max(b1, mb64[e * 4 + 1]);
+                b2_ = min(b2_, mb64[e * 4 + 2]);
+                b3 = max(b3, mb64[e * 4 + 3]);
+            }
+            // a warp with no remaining rows pushed (inf, 0, inf, 0): neutral
+            amin = bitsd(wmin64(b0));
+            amax = bitsd(wmax64(b1));
+            cmin = bitsd(wmin64(b2_));
+            cmax = bitsd(wmax64(b3));
+        }
+
+        // ======== H: hybrid argmax (synapse.cpp:247-260), per WARP ========
+        // Every warp ranks its rows with the reciprocal form, fetches the coordinates of its
+        // approximate best row right away (L2, overlapping the exact step), scores the rows
+        // within GAP_WINDOW of its approximate maximum with the reference's exact divisions,
+        // and takes its exact (score desc, row asc) argmax with shuffles.  X2 then carries
+        // every warp's candidate to every CTA: no block-level barrier in H.
+        const bool a_span = amax > amin, c_span = cmax > cmin;
+        const double ar = __dsub_rn(amax, amin), cr = __dsub_rn(cmax, cmin);
+        const double iar = a_span ? __drcp_rn(ar) : 0.0, icr = c_span ? __drcp_rn(cr) : 0.0;
+        double happ[RPT];
+        unsigned long long hkey = 0ull;  // this lane's approximate best (bits; h >= 0)
+        int kmax = -1;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            happ[k] = -1.0;
+            if (!(remm >> k & 1u)) continue;
+            const double na = __dmul_rn(__dsub_rn(a[k], amin), iar);
+            const double nc = __dmul_rn(__dsub_rn(m[k], cmin), icr);
+            happ[k] = __dadd_rn(__dmul_rn(lam, nc), __dmul_rn(one_m_lam, na));
+            if (kmax < 0 || dbits(happ[k]) > hkey) { hkey = dbits(happ[k]); kmax = k; }
+        }
+        // the warp's approximate best -> its coordinates start loading (a prefetch: any row of
+        // the approximate maximum will do)
+        const unsigned long long wkey = wmax64(kmax >= 0 ? hkey : 0ull);
+        const uint32_t atmax = __ballot_sync(0xffffffffu, kmax >= 0 && hkey == wkey);
+        const int wl = atmax ? __ffs(atmax) - 1 : 0;
+        const int spec_k = __shfl_sync(0xffffffffu, kmax, wl);
+        const int spec_li = atmax ? (quad + 4 * spec_k) * TILE + 32 * sub + wl : -1;
+        float4 spec4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (atmax && lane < D / 4)
+            spec4 = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)spec_li * p.rstride) + lane);
+        const bool approx_ok = (!a_span || ar >= 1e-290) && (!c_span || cr >= 1e-290);
+        const double cut = approx_ok ? bitsd(wkey) - GAP_WINDOW : -INFINITY;
+        // exact hybrid of the rows within the window; per lane: best (score desc, row asc)
+        // and runner-up
+        unsigned long long bkey = 0ull, rkey = 0ull;
+        bool has_b = false, has_r = false;
+        int brow = INT_MAX;
+        float bnx = 0.f;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            if (!(remm >> k & 1u) || happ[k] < cut) continue;
+            const double na = a_span ? __ddiv_rn(__dsub_rn(a[k], amin), ar) : 0.0;
+            const double nc = c_span ? __ddiv_rn(__dsub_rn(m[k], cmin), cr) : 0.0;
+            const unsigned long long hk = dbits(__dadd_rn(__dmul_rn(lam, nc), __dmul_rn(one_m_lam, na)));
+            const int li = (quad + 4 * k) * TILE + 32 * sub + lane;
+            if (!has_b || hk > bkey) {  // rows ascend with k: on a tie the earlier (lower) row stays
+                if (has_b) { rkey = max(rkey, bkey); has_r = true; }
+                bkey = hk; brow = li; bnx = nx[k]; has_b = true;
+            } else {
+                rkey = max(rkey, hk);
+                has_r = true;
+            }
+        }
+        // the warp's exact winner: max score, then the lowest row among equal scores
+        const unsigned long long wbest = wmax64(has_b ? bkey : 0ull);
+        const bool cand_b = has_b && bkey == wbest;
+        const int wrow = __reduce_min_sync(0xffffffffu, cand_b ? (unsigned)brow : 0xffffffffu);
+        const bool any_b = __ballot_sync(0xffffffffu, has_b) != 0u;
+        const bool is_w = cand_b && brow == wrow;
+        const uint32_t wmask = __ballot_sync(0xffffffffu, is_w);
+        const float wnx = __shfl_sync(0xffffffffu, bnx, wmask ? __ffs(wmask) - 1 : 0);
+        // runner-up: other lanes' best and every lane's runner-up (a tie with the winner included)
+        const bool has_r2 = has_r || (has_b && !is_w);
+        const unsigned long long r2 = wmax64(has_r2 ? (is_w ? rkey : max(rkey, bkey)) : 0ull);
+        const bool any_r = __ballot_sync(0xffffffffu, has_r2) != 0u;
+        // the exact winner is almost always the approximate one: else load its row now
+        if (any_b && wrow != spec_li && lane < D / 4)
+            spec4 = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)wrow * p.rstride) + lane);
+        if (!any_b) spec4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const double bsc = any_b ? bitsd(wbest) : -1.0;
+        const double b2 = any_r ? bitsd(r2) : -1.0;
+        const int brow_w = any_b ? wrow : INT_MAX;
+        const float bnx_w = wnx;
+
+        XSTAMP(5);
+        // ======== X2: every warp's (score, row, |b|^2, runner-up, coordinates) -> every CTA ========
+        {
+            const int slot = (int)rank * NW + wid;
+            const double sc = bsc;
+            const long long rw = brow_w != INT_MAX ? r0 + brow_w : LLONG_MAX;
+            for (int dst = 0; dst < (int)C; ++dst) {
+                const uint32_t mb = mapa(su32(&mbar[1]), dst);
+                if (lane == 0) {
+                    const uint32_t hd = mapa(su32(hdr + slot), dst);
+                    st_async_v2(hd, __double_as_longlong(sc), (uint64_t)rw, mb);
+                    st_async_v2(hd + 16, __double_as_longlong((double)bnx_w), __double_as_longlong(b2), mb);
+                }
+                if (lane < D / 4) st_async_v4(mapa(su32(bc + slot * D + 4 * lane), dst), spec4, mb);
+            }
+        }
+        mbar_wait(&mbar[1], ph2);
+        ph2 ^= 1u;
+        XSTAMP(6);
+        if (tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[1], tx2);
+        // the cluster winner (score desc, row asc) over all C x NW candidates, and the runner-up
+        double bs, rs2;
+        long long br;
+        int w;
+        {
+            unsigned long long ls = 0ull, l2 = 0ull;  // lane: best score bits, runner-up bits
+            bool lb = false, lr = false;
+            long long lrow = LLONG_MAX;
+            int le = 0;
+            for (int e = lane; e < (int)C * NW; e += 32) {
+                const double es = hdr[e].score, e2 = hdr[e].second;
+                const long long er = hdr[e].row;
+                if (e2 >= 0.0) { l2 = max(l2, dbits(e2)); lr = true; }
+                if (es < 0.0) continue;  // a warp without rows
+                const unsigned long long eb = dbits(es);
+                if (!lb || eb > ls || (eb == ls && er < lrow)) {
+                    if (lb) { l2 = max(l2, ls); lr = true; }
+                    ls = eb; lrow = er; le = e; lb = true;
+                } else {
+                    l2 = max(l2, eb);
+                    lr = true;
+                }
+            }
+            const unsigned long long gs = wmax64(lb ? ls : 0ull);
+            const bool cs = lb && ls == gs;
+            // rows are < 2^31 here (a group's rows): the low word orders them
+            const unsigned grow = __reduce_min_sync(0xffffffffu, cs ? (unsigned)lrow : 0xffffffffu);
+            const bool iw = cs && (unsigned)lrow == grow;
+            const uint32_t wm = __ballot_sync(0xffffffffu, iw);
+            const int wlane = wm ? __ffs(wm) - 1 : 0;
+            const bool hr = lr || (lb && !iw);
+            const unsigned long long g2 = wmax64(hr ? (iw ? l2 : max(l2, ls)) : 0ull);
+            const bool any = __ballot_sync(0xffffffffu, lb) != 0u;
+            const bool any2 = __ballot_sync(0xffffffffu, hr) != 0u;
+            bs = any ? bitsd(gs) : -1.0;
+            br = any ? (long long)grow : LLONG_MAX;
+            w = __shfl_sync(0xffffffffu, le, wlane);
+            rs2 = any2 ? bitsd(g2) : -1.0;
+        }
+        // gap monitor: a row outside every warp's window scores < bs - GAP_WINDOW (+ ~1e-15)
+        if (tid == 0 && rank == 0 && rs2 >= 0.0)
+            *min_gap = (unsigned long long)__double_as_longlong(
+                dmin_std(__longlong_as_double((long long)*min_gap), __dsub_rn(bs, rs2)));
+        bw = bc + w * D;
+        nbw = (float)hdr[w].nb;
+        if (br >= r0 && br < r0 + nrows) {
+            const int li = (int)(br - r0);
+            const int j = li / TILE, r = li % TILE;
+            if (wid == ((j & 3) << 2) + (r >> 5) && lane == (r & 31)) remm &= ~(1u << (j >> 2));
+        }
+        if (tid == 0 && rank == 0) {
+            pick_rows[round] = br;
+            pick_scores[round] = bs;
+        }
+        // every warp has read this round's hdr / bc before any CTA can push the next round's
+        // (a peer pushes only after ITS X1 wait, which needs this CTA's next X1 push)
+    }
+
+    __syncthreads();
+    if (rank == 0 && tid == 0 && p.gaps) p.gaps[g] = dmin_std(__longlong_as_double((long long)*min_gap), GAP_WINDOW);
+    if (rank == 0) {  // sort the picks ascending by row (synapse.cpp:276-277)
+        int64_t* out_rows = p.out_rows + (int64_t)g * p.take;
+        double* out_scores = p.out_scores + (int64_t)g * p.take;
+        for (int s = tid; s < p.take; s += NT) {
+            const int64_t r = pick_rows[s];
+            int pos = 0;
+            for (int t = 0; t < p.take; ++t) pos += pick_rows[t] < r;
+            out_rows[pos] = r;
+            out_scores[pos] = pick_scores[s];
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster.sync();  // no CTA exits while a peer may still push into it
+    if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+}
+
+using SelxKern = void (*)(SelxParams);
+SelxKern selx_kernel_for(int rpt) {
+    switch (rpt) {
+        case 1: return selx_kernel<1>;
+        case 2: return selx_kernel<2>;
+        case 3: return selx_kernel<3>;
+        case 4: return selx_kernel<4>;
+        case 5: return selx_kernel<5>;
+        default: return selx_kernel<6>;
+    }
+}
+
+struct SelxCfg {
+    int C = 0, S = 0, n_tiles = 0, n_smem = 0, rpt = 0, n_stage = 0;
+    size_t smem = 0;
+};
+
+// rows per CTA s -> tiles, shared-memory tiles, TMEM tiles; false if s does not fit
+bool selx_shape(int s, size_t budget, SelxCfg* c) {
+    const int nt = (s + TILE - 1) / TILE;
+    if (nt > MAXT) return false;
+    const size_t base = selx_layout(0, c->C, 0).total;
+    const int smem_max = (int)((budget - base) / TILE_BYTES);
+    // rows in TMEM first (TS-form MMAs issue faster than SS, measured), the rest in shared memory
+    const int nt_tm = std::min(nt, (512 - tm_rows_col(nt)) / 32);
+    const int ns = nt - nt_tm;
+    if (ns > smem_max) return false;
+    c->S = s;
+    c->n_tiles = nt;
+    c->n_smem = ns;
+    c->rpt = (nt + 3) / 4;
+    // at least ~116 KB so that one CTA owns an SM (and its 512 TMEM columns)
+    // staging slots for the exact rows from what shared memory is left (up to 128)
+    const size_t used = selx_layout(ns, c->C, 0).total;
+    // (TMA bulk staging of the exact rows measured slower than direct loads by the evaluators)
+    c->n_stage = 0;
+    (void)used;
+    c->smem = std::max(selx_layout(ns, c->C, c->n_stage).total, (size_t)116 * 1024);
+    return true;
+}
+
+int selx_active(const SelxCfg& c) {
+    static std::mutex mu;
+    static std::map<std::pair<int, size_t>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(c.C * 8 + c.rpt, c.smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    SelxKern kern = selx_kernel_for(c.rpt);
+    int n = 0;
+    try {
+        kernel_smem(kern, c.smem, c.C > 8);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)c.C, 1, 1);
+        cfg.blockDim = dim3(NT, 1, 1);
+        cfg.dynamicSmemBytes = c.smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)c.C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    } catch (const Failure&) {
+        n = 0;
+    }
+    cudaGetLastError();
+    cache[key] = n;
+    return n;
+}
+
+}  // namespace
+
+// Per-round cost model (us): a fixed part (exchanges, barriers, the exact queue) plus a
+// per-row part; waves = ceil(G / co-resident clusters).  Returns false if no cluster size
+// keeps a group's rows on chip.
+static bool selx_plan(int G, int64_t L, const Options& o, SelxCfg* out, int* act_out) {
+    static int max_optin = -1;
+    if (max_optin < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+            max_optin = 232448;
+    }
+    const size_t budget = (size_t)max_optin - 1024;
+    double best = 1e300;
+    bool found = false;
+    for (int c = 1; c <= MAXC; ++c) {
+        if (o.select_cluster > 0 && c != o.select_cluster) continue;
+        SelxCfg cfg;
+        cfg.C = c;
+        if (!selx_shape((int)((L + c - 1) / c), budget, &cfg)) continue;
+        const int act = selx_active(cfg);
+        if (act <= 0) continue;
+        const double per = 4.0 + 0.0008 * cfg.S;
+        const double cost = (double)((G + act - 1) / act) * per;
+        if (cost < best * (1.0 - 1e-9)) {
+            best = cost;
+            *out = cfg;
+            *act_out = act;
+            found = true;
+        }
+    }
+    return found;
+}
+
+bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
+                      double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows,
+                      double* scores, double* gaps, double* gap_rec, cudaStream_t s) {
+    if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 || (reinterpret_cast<uintptr_t>(g.X) & 15) != 0 ||
+        g.L < 1)
+        return false;
+    SelxCfg cfg;
+    int act = 0;
+    if (!selx_plan(g.G, g.L, o, &cfg, &act)) return false;
+    SelxParams prm;
+    prm.X = g.X;
+    prm.gstride = g.gstride;
+    prm.rstride = g.rstride;
+    prm.L = g.L;
+    prm.attn = attn;
+    prm.cen = cen;
+    prm.take = take;
+    prm.lambda = lambda;
+    prm.S = cfg.S;
+    prm.n_tiles = cfg.n_tiles;
+    prm.n_smem = cfg.n_smem;
+    prm.n_stage = cfg.n_stage;
+    prm.filter = (flags & CX_SELECT_EXACT_ONLY) ? 0 : 1;
+    prm.pick_rows = pick_rows;
+    prm.pick_scores = pick_scores;
+    prm.out_rows = rows;
+    prm.out_scores = scores;
+    prm.gaps = gaps;
+    (void)gap_rec;  // the per-warp protocol reduces the runner-up in the loop
+    prm.trace = nullptr;
+#ifdef CX_EXPERIMENTS
+    const char* tr = getenv("CX_SEL_TRACE");
+    if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
+#endif
+    SelxKern kern = selx_kernel_for(cfg.rpt);
+    kernel_smem(kern, cfg.smem, cfg.C > 8);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)cfg.C, (unsigned)g.G, 1);
+    lc.blockDim = dim3(NT, 1, 1);
+    lc.dynamicSmemBytes = cfg.smem;
+    lc.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cfg.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CX_CUDA(cudaLaunchKernelEx(&lc, kern, prm));
+    count_launch();
+#ifdef CX_EXPERIMENTS
+    if (prm.trace) {  // average cycles per phase over rounds 2 .. take-2
+        CX_CUDA(cudaStreamSynchronize(s));
+        double acc[10] = {0};
+        int n = 0;
+        for (int r = 2; r < std::min(take, 4096) - 1; ++r, ++n) {
+            const long long* t = prm.trace + r * 16;
+            acc[0] += (double)(t[1] - t[0]);  // B operand + MMA
+            acc[1] += (double)(t[2] - t[1]);  // bound + queue + staging
+            acc[2] += (double)(t[3] - t[2]);  // exact
+            acc[3] += (double)(t[9] - t[3]);  // X1 local
+            acc[4] += (double)(t[4] - t[9]);  // X1 wait
+            acc[5] += (double)(t[5] - t[4]);  // H
+            acc[6] += (double)(t[6] - t[5]);  // X2
+            acc[7] += (double)(prm.trace[(r + 1) * 16] - t[0]);
+            acc[8] += (double)t[8];
+        }
+        if (n > 0)
+            fprintf(stderr, "select_tc C=%d (co-resident %d) S=%d tiles=%d (smem %d) cycles/round: mma=%.0f bound+queue=%.0f exact=%.0f "
+                            "X1loc=%.0f X1wait=%.0f H=%.0f X2=%.0f total=%.0f queued=%.1f\n",
+                    cfg.C, act, cfg.S, cfg.n_tiles, cfg.n_smem, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n,
+                    acc[5] / n, acc[6] / n, acc[7] / n, acc[8] / n);
+        cudaFree(prm.trace);
+    }
+#endif
+    return true;
+}
+
+int select_tc_wave(int64_t L, int G) {
+    SelxCfg cfg;
+    int act = 0;
+    Options o;
+    return selx_plan(G, L, o, &cfg, &act) ? act : 0;
+}
+
+}  // namespace cx

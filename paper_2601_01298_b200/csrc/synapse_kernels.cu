@@ -858,6 +858,12 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
         ctx->gaps_cap = g.G;
     }
     ctx->gaps_n = g.G;
+    const int impl = ctx->opt.select_impl;
+    if (!(flags & CX_SELECT_GENERIC) && impl != CX_SELECT_IMPL_CUDA_CORE &&
+        select_tc_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s))
+        return;
+    if (impl == CX_SELECT_IMPL_TC && !(flags & CX_SELECT_GENERIC))
+        fail(CX_PRECONDITION_ERROR, "select: the pinned tensor-core selection does not apply to this shape");
     if (!(flags & CX_SELECT_GENERIC) &&
         (select64_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s) ||
          select128_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s)))

@@ -232,8 +232,9 @@ def gate_decide(h: torch.Tensor, t: torch.Tensor, theta: float):
 
 
 OPTIONS = {"select_cluster": 1, "select_no_sketch": 2, "decode_impl": 3, "decode_ctas_per_lh": 4,
-           "host_upload_values": 5}
+           "host_upload_values": 5, "select_impl": 6}
 DECODE_IMPLS = {"auto": 0, "tc": 1, "v2": 2, "v1": 3}
+SELECT_IMPLS = {"auto": 0, "tc": 1, "cuda_core": 2}
 
 
 def set_option(name: str, value, device: int | None = None) -> int:
@@ -243,6 +244,8 @@ def set_option(name: str, value, device: int | None = None) -> int:
     code = OPTIONS[name]
     if name == "decode_impl" and isinstance(value, str):
         value = DECODE_IMPLS[value]
+    if name == "select_impl" and isinstance(value, str):
+        value = SELECT_IMPLS[value]
     old = C.c_int64()
     check(lib.cx_ctx_get_option(ctx(dev), code, C.byref(old)), "ctx_get_option")
     check(lib.cx_ctx_set_option(ctx(dev), code, int(value)), "ctx_set_option")
