@@ -176,6 +176,8 @@ cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* a
 #define CX_SELECT_IMPL_AUTO 0       /* tensor-core filter (d = 64), then CUDA-core, then generic */
 #define CX_SELECT_IMPL_TC 1         /* pinned: an error if the shape does not apply */
 #define CX_SELECT_IMPL_CUDA_CORE 2  /* the CUDA-core filter kernels (select64 / select128) */
+#define CX_OPT_SELECT_EXCHANGE 7    /* tensor-core selection: 0 cost model, 1 thread-block clusters
+                                       (DSMEM), 2 cooperative launch (global-memory exchanges) */
 #define CX_DECODE_AUTO 0            /* tcgen05, then v2, then the generic kernel */
 #define CX_DECODE_TC 1              /* pinned: an error if the shape does not apply */
 #define CX_DECODE_V2 2

@@ -55,6 +55,7 @@ struct Options {
     int select_cluster = 0;      // CX_OPT_SELECT_CLUSTER: force the selection cluster size (0 = cost model)
     int select_no_sketch = 0;    // CX_OPT_SELECT_NO_SKETCH: never use the fp16 sketch row mode
     int select_impl = 0;         // CX_OPT_SELECT_IMPL: CX_SELECT_IMPL_{AUTO,TC,CUDA_CORE}
+    int select_exchange = 0;     // CX_OPT_SELECT_EXCHANGE: 0 cost model, 1 clusters (DSMEM), 2 cooperative
     int decode_impl = 0;         // CX_OPT_DECODE_IMPL: CX_DECODE_{AUTO,TC,V2,V1}
     int decode_ctas_per_lh = 0;  // CX_OPT_DECODE_CTAS_PER_LH: tcgen05 decode CTAs per (layer, KV head) (0 = auto)
     int host_upload_values = 0;  // CX_OPT_HOST_UPLOAD_VALUES: host path uploads all values even when pinned
@@ -187,8 +188,9 @@ void plan_select(ArenaPlan& p, const GroupView& g, int k);
 // does not apply
 bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
                       double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows,
-                      double* scores, double* gaps, double* gap_rec, cudaStream_t s);
+                      double* scores, double* gaps, void* scratch, cudaStream_t s);
 int select_tc_wave(int64_t L, int G);
+size_t select_tc_scratch(int G);  // bytes of scratch select_tc_launch may use
 // dim-64 fast path (select64.cu); false when it does not apply
 bool select64_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
                      double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,

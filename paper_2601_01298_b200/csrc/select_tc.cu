@@ -28,6 +28,7 @@
 #include <cuda_fp16.h>
 
 #include <map>
+#include <tuple>
 #include <mutex>
 
 #include "cx_internal.cuh"
@@ -137,18 +138,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
 __host__ __device__ __forceinline__ uint32_t idesc_f16_f32(int m, int n) {
     return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
-__device__ __forceinline__ void mma_ss(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(dt),
-        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void mma_ts(uint32_t dt, uint32_t at, uint64_t bd, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(dt),
-        "r"(at), "l"(bd), "r"(idesc), "r"(acc)
-        : "memory");
-}
 // warp-uniform issue: the whole warp runs the code (operands stay in uniform registers),
 // one elected lane issues -- ~10x cheaper per MMA than a divergent single thread (measured)
 __device__ __forceinline__ void mma_ss_elect(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
@@ -170,10 +159,6 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* mbar) {
         "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(su32(mbar))
         : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* mbar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mbar))
-                 : "memory");
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
     asm volatile(
@@ -223,6 +208,13 @@ __device__ __forceinline__ float tc_lower_bound(float nx, float nb, float dot) {
     return isfinite(dot) ? __fsub_rd(s, e) : -INFINITY;
 }
 
+struct alignas(16) Hdr {
+    double score;
+    long long row;
+    double nb;
+    double second;
+};
+
 struct SelxParams {
     const float* X;
     int64_t gstride, rstride;
@@ -241,7 +233,13 @@ struct SelxParams {
     int64_t* out_rows;
     double* out_scores;
     double* gaps;
-    long long* trace;  // CX_EXPERIMENTS builds: per-round phase clocks of group 0, rank 0
+    long long* trace;
+    // cooperative (non-cluster) mode: the exchanges go through global memory
+    unsigned long long* x1g;  // [G][2 parity][C * NW][4]: (amin, amax, cmin, cmax) bits
+    Hdr* x2h;                 // [G][2][C * NW]: (score, row, |b|^2, runner-up)
+    float* x2c;               // [G][2][C * NW][D]: the candidates' coordinates
+    unsigned* cnt;            // [G][2]: monotonic arrival counters (zeroed per launch)
+    int C;                    // CTAs per group  // CX_EXPERIMENTS builds: per-round phase clocks of group 0, rank 0
 };
 
 #ifdef CX_EXPERIMENTS
@@ -255,12 +253,6 @@ struct SelxParams {
     } while (0)
 #endif
 
-struct alignas(16) Hdr {
-    double score;
-    long long row;
-    double nb;
-    double second;
-};
 
 struct SelxLayout {
     size_t mbar, mm, hdr, bc, misc, qrow, qres, bop, stage, tiles, total;
@@ -285,11 +277,16 @@ __host__ __device__ inline SelxLayout selx_layout(int n_smem, int C, int n_stage
     return l;
 }
 
-template <int RPT>
+// CL: the group's CTAs form a thread-block cluster and exchange through DSMEM pushes.
+// !CL: a cooperative launch (all CTAs co-resident, any SMs: one wave when C x G <= 148, which
+// clusters cannot reach -- 45 co-resident clusters of 3 on B200) and the exchanges go through
+// global memory: every warp writes its slot and bumps the group's counter; one poller per CTA
+// waits for the count, then one TMA bulk copy brings the whole exchange into shared memory,
+// completing on the same mbarrier the cluster pushes would.
+template <int RPT, bool CL>
 __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
-    cg::cluster_group cluster = cg::this_cluster();
-    const uint32_t C = cluster.num_blocks();
-    const uint32_t rank = cluster.block_rank();
+    const uint32_t C = CL ? cg::this_cluster().num_blocks() : (uint32_t)p.C;
+    const uint32_t rank = CL ? cg::this_cluster().block_rank() : blockIdx.x;
     const int g = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int sub = wid & 3, quad = wid >> 2;  // TMEM sub-partition, tile phase
@@ -402,13 +399,43 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    cluster.sync();  // mbarriers visible cluster-wide before any remote push
+    if (CL) cg::this_cluster().sync();  // mbarriers visible cluster-wide before any remote push
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tx1 = C * NW * 32u, tx2 = C * NW * (uint32_t)(sizeof(Hdr) + D * sizeof(float));
-    if (tid == 0) {
+    if (CL && tid == 0) {
         mbar_arrive_expect(&mbar[0], tx1);
         mbar_arrive_expect(&mbar[1], tx2);
     }
+    // Cooperative mode.  Every warp writes its slot, then bumps the group's counter with a
+    // release add; one poller per CTA (thread 0) acquires the count, then ONE TMA bulk copy
+    // brings the whole exchange into shared memory, completing on the same mbarrier the
+    // cluster pushes would.  (Polling self-stamped words instead measured slower: ~4K vs ~3K
+    // cycles per exchange, cross-die L2 round trips.)
+    auto bump = [&](int which) {  // after this warp's slot writes
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the warp's writes (observed via the sync)
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.cnt + 2 * g + which) : "memory");
+        }
+    };
+    auto gather = [&](int which, int round_, uint32_t bytes) {
+        if (tid != 0) return;
+        const unsigned target = C * NW * (unsigned)(round_ + 1);
+        const unsigned* c = p.cnt + 2 * g + which;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+        } while ((int)(v - target) < 0);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> the bulk copy
+        const int par = round_ & 1;
+        mbar_arrive_expect(&mbar[which], bytes);
+        if (which == 0) {
+            bulk_g2s(mm, p.x1g + ((size_t)(2 * g + par) * C * NW) * 4, C * NW * 32u, &mbar[0]);
+        } else {
+            bulk_g2s(hdr, p.x2h + (size_t)(2 * g + par) * C * NW, C * NW * (uint32_t)sizeof(Hdr), &mbar[1]);
+            bulk_g2s(bc, p.x2c + (size_t)(2 * g + par) * C * NW * D, C * NW * D * (uint32_t)sizeof(float), &mbar[1]);
+        }
+    };
 
     const double lam = p.lambda;
     const double one_m_lam = __dsub_rn(1.0, lam);
@@ -586,17 +613,27 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             b3 = wmax64(b3);
             // every warp pushes its partial straight to every CTA of the cluster (no block-level
             // reduction first): C x NW slots of 32 B, one mbarrier
-            if (lane < (int)C) {
-                const uint32_t dst = mapa(su32(mm + ((int)rank * NW + wid) * 4), lane);
-                const uint32_t mb = mapa(su32(&mbar[0]), lane);
-                st_async_v2(dst, b0, b1, mb);
-                st_async_v2(dst + 16, b2_, b3, mb);
+            if (CL) {
+                if (lane < (int)C) {
+                    const uint32_t dst = mapa(su32(mm + ((int)rank * NW + wid) * 4), lane);
+                    const uint32_t mb = mapa(su32(&mbar[0]), lane);
+                    st_async_v2(dst, b0, b1, mb);
+                    st_async_v2(dst + 16, b2_, b3, mb);
+                }
+            } else {
+                if (lane == 0) {
+                    unsigned long long* d = p.x1g + ((size_t)(2 * g + (round & 1)) * C * NW + rank * NW + wid) * 4;
+                    reinterpret_cast<ulonglong2*>(d)[0] = make_ulonglong2(b0, b1);
+                    reinterpret_cast<ulonglong2*>(d)[1] = make_ulonglong2(b2_, b3);
+                }
+                bump(0);
+                gather(0, round, tx1);
             }
             XSTAMP(9);
             mbar_wait(&mbar[0], ph1);
             ph1 ^= 1u;
             XSTAMP(4);
-            if (tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[0], tx1);
+            if (CL && tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[0], tx1);
             const unsigned long long* mb64 = reinterpret_cast<const unsigned long long*>(mm);
             b0 = BITS_INF; b1 = 0ull; b2_ = BITS_INF; b3 = 0ull;
             for (int e = lane; e < (int)C * NW; e += 32) {
@@ -693,20 +730,32 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             const int slot = (int)rank * NW + wid;
             const double sc = bsc;
             const long long rw = brow_w != INT_MAX ? r0 + brow_w : LLONG_MAX;
-            for (int dst = 0; dst < (int)C; ++dst) {
-                const uint32_t mb = mapa(su32(&mbar[1]), dst);
-                if (lane == 0) {
-                    const uint32_t hd = mapa(su32(hdr + slot), dst);
-                    st_async_v2(hd, __double_as_longlong(sc), (uint64_t)rw, mb);
-                    st_async_v2(hd + 16, __double_as_longlong((double)bnx_w), __double_as_longlong(b2), mb);
+            if (CL) {
+                for (int dst = 0; dst < (int)C; ++dst) {
+                    const uint32_t mb = mapa(su32(&mbar[1]), dst);
+                    if (lane == 0) {
+                        const uint32_t hd = mapa(su32(hdr + slot), dst);
+                        st_async_v2(hd, __double_as_longlong(sc), (uint64_t)rw, mb);
+                        st_async_v2(hd + 16, __double_as_longlong((double)bnx_w), __double_as_longlong(b2), mb);
+                    }
+                    if (lane < D / 4) st_async_v4(mapa(su32(bc + slot * D + 4 * lane), dst), spec4, mb);
                 }
-                if (lane < D / 4) st_async_v4(mapa(su32(bc + slot * D + 4 * lane), dst), spec4, mb);
+            } else {
+                const size_t base = (size_t)(2 * g + (round & 1)) * C * NW + slot;
+                if (lane == 0) {
+                    Hdr h;
+                    h.score = sc; h.row = rw; h.nb = (double)bnx_w; h.second = b2;
+                    p.x2h[base] = h;
+                }
+                if (lane < D / 4) reinterpret_cast<float4*>(p.x2c + base * D)[lane] = spec4;
+                bump(1);
+                gather(1, round, tx2);
             }
         }
         mbar_wait(&mbar[1], ph2);
         ph2 ^= 1u;
         XSTAMP(6);
-        if (tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[1], tx2);
+        if (CL && tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[1], tx2);
         // the cluster winner (score desc, row asc) over all C x NW candidates, and the runner-up
         double bs, rs2;
         long long br;
@@ -779,24 +828,29 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    cluster.sync();  // no CTA exits while a peer may still push into it
+    if (CL) cg::this_cluster().sync();  // no CTA exits while a peer may still push into it
+    else __syncthreads();
     if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
 }
 
 using SelxKern = void (*)(SelxParams);
+template <bool CL>
 SelxKern selx_kernel_for(int rpt) {
     switch (rpt) {
-        case 1: return selx_kernel<1>;
-        case 2: return selx_kernel<2>;
-        case 3: return selx_kernel<3>;
-        case 4: return selx_kernel<4>;
-        case 5: return selx_kernel<5>;
-        default: return selx_kernel<6>;
+        case 1: return selx_kernel<1, CL>;
+        case 2: return selx_kernel<2, CL>;
+        case 3: return selx_kernel<3, CL>;
+        case 4: return selx_kernel<4, CL>;
+        case 5: return selx_kernel<5, CL>;
+        default: return selx_kernel<6, CL>;
     }
 }
+SelxKern selx_kernel_for(int rpt, bool cl) { return cl ? selx_kernel_for<true>(rpt) : selx_kernel_for<false>(rpt); }
 
 struct SelxCfg {
     int C = 0, S = 0, n_tiles = 0, n_smem = 0, rpt = 0, n_stage = 0;
+    bool cluster = true;  // false: cooperative launch, exchanges through global memory
+    int per_wave = 0;     // groups resident at once
     size_t smem = 0;
 };
 
@@ -814,39 +868,52 @@ bool selx_shape(int s, size_t budget, SelxCfg* c) {
     c->n_tiles = nt;
     c->n_smem = ns;
     c->rpt = (nt + 3) / 4;
+    c->n_stage = 0;  // (TMA staging of the exact rows measured slower than direct loads)
     // at least ~116 KB so that one CTA owns an SM (and its 512 TMEM columns)
-    // staging slots for the exact rows from what shared memory is left (up to 128)
-    const size_t used = selx_layout(ns, c->C, 0).total;
-    // (TMA bulk staging of the exact rows measured slower than direct loads by the evaluators)
-    c->n_stage = 0;
-    (void)used;
     c->smem = std::max(selx_layout(ns, c->C, c->n_stage).total, (size_t)116 * 1024);
     return true;
 }
 
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+// co-resident groups: clusters from the occupancy API; cooperative: blocks per SM x SMs / C
 int selx_active(const SelxCfg& c) {
     static std::mutex mu;
-    static std::map<std::pair<int, size_t>, int> cache;
+    static std::map<std::tuple<int, int, size_t, bool>, int> cache;
     std::lock_guard<std::mutex> lk(mu);
-    const auto key = std::make_pair(c.C * 8 + c.rpt, c.smem);
+    const auto key = std::make_tuple(c.C, c.rpt, c.smem, c.cluster);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
-    SelxKern kern = selx_kernel_for(c.rpt);
+    SelxKern kern = selx_kernel_for(c.rpt, c.cluster);
     int n = 0;
     try {
-        kernel_smem(kern, c.smem, c.C > 8);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)c.C, 1, 1);
-        cfg.blockDim = dim3(NT, 1, 1);
-        cfg.dynamicSmemBytes = c.smem;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = (unsigned)c.C;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+        kernel_smem(kern, c.smem, c.cluster && c.C > 8);
+        if (c.cluster) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)c.C, 1, 1);
+            cfg.blockDim = dim3(NT, 1, 1);
+            cfg.dynamicSmemBytes = c.smem;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)c.C;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+        } else {
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, c.smem) != cudaSuccess) per_sm = 0;
+            n = per_sm * sm_count() / c.C;
+        }
     } catch (const Failure&) {
         n = 0;
     }
@@ -857,10 +924,12 @@ int selx_active(const SelxCfg& c) {
 
 }  // namespace
 
-// Per-round cost model (us): a fixed part (exchanges, barriers, the exact queue) plus a
-// per-row part; waves = ceil(G / co-resident clusters).  Returns false if no cluster size
-// keeps a group's rows on chip.
-static bool selx_plan(int G, int64_t L, const Options& o, SelxCfg* out, int* act_out) {
+// Cost model (us per round): a fixed part (exchanges, barriers, the exact queue) plus a
+// per-row part, x1.15 for the global-memory exchanges of the cooperative mode; times the
+// waves = ceil(G / co-resident groups).  cfg2 (48 groups of 8192 rows): a cluster of 3 CTAs
+// holds a group on chip (22 tiles) but only 45 clusters of 3 are co-resident (two waves);
+// the cooperative mode places the 144 CTAs anywhere: one wave.
+static bool selx_plan(int G, int64_t L, const Options& o, SelxCfg* out) {
     static int max_optin = -1;
     if (max_optin < 0) {
         int dev = 0;
@@ -871,34 +940,45 @@ static bool selx_plan(int G, int64_t L, const Options& o, SelxCfg* out, int* act
     const size_t budget = (size_t)max_optin - 1024;
     double best = 1e300;
     bool found = false;
-    for (int c = 1; c <= MAXC; ++c) {
-        if (o.select_cluster > 0 && c != o.select_cluster) continue;
-        SelxCfg cfg;
-        cfg.C = c;
-        if (!selx_shape((int)((L + c - 1) / c), budget, &cfg)) continue;
-        const int act = selx_active(cfg);
-        if (act <= 0) continue;
-        const double per = 4.0 + 0.0008 * cfg.S;
-        const double cost = (double)((G + act - 1) / act) * per;
-        if (cost < best * (1.0 - 1e-9)) {
-            best = cost;
-            *out = cfg;
-            *act_out = act;
-            found = true;
+    for (int mode = 0; mode < 2; ++mode) {
+        const bool cl = mode == 0;
+        if (o.select_exchange == 1 && !cl) continue;  // pinned: clusters
+        if (o.select_exchange == 2 && cl) continue;   // pinned: cooperative
+        for (int c = 1; c <= MAXC; ++c) {
+            if (o.select_cluster > 0 && c != o.select_cluster) continue;
+            SelxCfg cfg;
+            cfg.C = c;
+            cfg.cluster = cl;
+            if (!selx_shape((int)((L + c - 1) / c), budget, &cfg)) continue;
+            const int act = selx_active(cfg);
+            if (act <= 0) continue;
+            const double per = (4.0 + 0.0008 * cfg.S) * (cl ? 1.0 : 1.15);
+            const double cost = (double)((G + act - 1) / act) * per;
+            if (cost < best * (1.0 - 1e-9)) {
+                best = cost;
+                cfg.per_wave = act;
+                *out = cfg;
+                found = true;
+            }
         }
     }
     return found;
 }
 
+size_t select_tc_scratch(int G) {
+    // cooperative-mode exchange buffers + counters, for any C <= 16
+    return (size_t)G * 2 * MAXC * NW * (4 * sizeof(unsigned long long) + sizeof(Hdr) + D * sizeof(float)) +
+           (size_t)G * 2 * sizeof(unsigned) + 1024;
+}
+
 bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
                       double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows,
-                      double* scores, double* gaps, double* gap_rec, cudaStream_t s) {
+                      double* scores, double* gaps, void* scratch, cudaStream_t s) {
     if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 || (reinterpret_cast<uintptr_t>(g.X) & 15) != 0 ||
         g.L < 1)
         return false;
     SelxCfg cfg;
-    int act = 0;
-    if (!selx_plan(g.G, g.L, o, &cfg, &act)) return false;
+    if (!selx_plan(g.G, g.L, o, &cfg)) return false;
     SelxParams prm;
     prm.X = g.X;
     prm.gstride = g.gstride;
@@ -918,28 +998,62 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
     prm.out_rows = rows;
     prm.out_scores = scores;
     prm.gaps = gaps;
-    (void)gap_rec;  // the per-warp protocol reduces the runner-up in the loop
     prm.trace = nullptr;
+    prm.C = cfg.C;
+    prm.x1g = nullptr;
+    prm.x2h = nullptr;
+    prm.x2c = nullptr;
+    prm.cnt = nullptr;
 #ifdef CX_EXPERIMENTS
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
 #endif
-    SelxKern kern = selx_kernel_for(cfg.rpt);
-    kernel_smem(kern, cfg.smem, cfg.C > 8);
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)cfg.C, (unsigned)g.G, 1);
-    lc.blockDim = dim3(NT, 1, 1);
-    lc.dynamicSmemBytes = cfg.smem;
-    lc.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)cfg.C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    lc.attrs = attr;
-    lc.numAttrs = 1;
-    CX_CUDA(cudaLaunchKernelEx(&lc, kern, prm));
-    count_launch();
+    SelxKern kern = selx_kernel_for(cfg.rpt, cfg.cluster);
+    kernel_smem(kern, cfg.smem, cfg.cluster && cfg.C > 8);
+    // the groups in waves of per_wave (cooperative launches must fit on the GPU at once;
+    // cluster launches are a single grid, the hardware forms the waves)
+    const int wave = cfg.cluster ? g.G : cfg.per_wave;
+    for (int g0 = 0; g0 < g.G; g0 += wave) {
+        const int ng = std::min(wave, g.G - g0);
+        SelxParams pw = prm;
+        pw.X = g.X + (int64_t)g0 * g.gstride;
+        pw.attn = attn + (int64_t)g0 * g.L;
+        pw.cen = cen + (int64_t)g0 * D;
+        pw.pick_rows = pick_rows + (int64_t)g0 * take;
+        pw.pick_scores = pick_scores + (int64_t)g0 * take;
+        pw.out_rows = rows + (int64_t)g0 * take;
+        pw.out_scores = scores + (int64_t)g0 * take;
+        pw.gaps = gaps ? gaps + g0 : nullptr;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)cfg.C, (unsigned)ng, 1);
+        lc.blockDim = dim3(NT, 1, 1);
+        lc.dynamicSmemBytes = cfg.smem;
+        lc.stream = s;
+        cudaLaunchAttribute attr[1];
+        if (cfg.cluster) {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)cfg.C;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+        } else {
+            char* sc = reinterpret_cast<char*>(((uintptr_t)scratch + 255) & ~(uintptr_t)255);
+            const size_t slots = (size_t)ng * 2 * cfg.C * NW;
+            pw.x1g = reinterpret_cast<unsigned long long*>(sc);
+            sc += slots * 4 * sizeof(unsigned long long);
+            pw.x2h = reinterpret_cast<Hdr*>(sc);
+            sc += slots * sizeof(Hdr);
+            pw.x2c = reinterpret_cast<float*>(sc);
+            sc += slots * D * sizeof(float);
+            pw.cnt = reinterpret_cast<unsigned*>(sc);
+            CX_CUDA(cudaMemsetAsync(pw.cnt, 0, sizeof(unsigned) * 2 * ng, s));
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+        }
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        CX_CUDA(cudaLaunchKernelEx(&lc, kern, pw));
+        count_launch();
+    }
 #ifdef CX_EXPERIMENTS
     if (prm.trace) {  // average cycles per phase over rounds 2 .. take-2
         CX_CUDA(cudaStreamSynchronize(s));
@@ -958,9 +1072,9 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
             acc[8] += (double)t[8];
         }
         if (n > 0)
-            fprintf(stderr, "select_tc C=%d (co-resident %d) S=%d tiles=%d (smem %d) cycles/round: mma=%.0f bound+queue=%.0f exact=%.0f "
+            fprintf(stderr, "select_tc %s C=%d (co-resident %d) S=%d tiles=%d (smem %d) cycles/round: mma=%.0f bound+queue=%.0f exact=%.0f "
                             "X1loc=%.0f X1wait=%.0f H=%.0f X2=%.0f total=%.0f queued=%.1f\n",
-                    cfg.C, act, cfg.S, cfg.n_tiles, cfg.n_smem, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n,
+                    cfg.cluster ? "cluster" : "cooperative", cfg.C, cfg.per_wave, cfg.S, cfg.n_tiles, cfg.n_smem, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n,
                     acc[5] / n, acc[6] / n, acc[7] / n, acc[8] / n);
         cudaFree(prm.trace);
     }
@@ -970,9 +1084,8 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
 
 int select_tc_wave(int64_t L, int G) {
     SelxCfg cfg;
-    int act = 0;
     Options o;
-    return selx_plan(G, L, o, &cfg, &act) ? act : 0;
+    return selx_plan(G, L, o, &cfg) ? cfg.per_wave : 0;
 }
 
 }  // namespace cx

@@ -816,6 +816,7 @@ void plan_select(ArenaPlan& p, const GroupView& g, int k) {
     p.take<int64_t>((size_t)g.G * take);        // pick rows
     p.take<double>((size_t)g.G * take);         // pick scores
     p.take<double>((size_t)g.G * take * kGapRecStride);  // gap-monitor records
+    p.take<char>(select_tc_scratch(g.G));               // select_tc cooperative exchanges
 }
 
 void centroid_launch(const GroupView& g, double* cen, cudaStream_t s) {
@@ -844,6 +845,7 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     int64_t* pr = ctx->arena.take<int64_t>((size_t)g.G * take);
     double* ps = ctx->arena.take<double>((size_t)g.G * take);
     double* grec = ctx->arena.take<double>((size_t)g.G * take * kGapRecStride);
+    char* tc_scratch = ctx->arena.take<char>(select_tc_scratch(g.G));
 
     if (cen_in) cen = const_cast<double*>(cen_in);
     else centroid_launch(g, cen, s);
@@ -860,7 +862,7 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     ctx->gaps_n = g.G;
     const int impl = ctx->opt.select_impl;
     if (!(flags & CX_SELECT_GENERIC) && impl != CX_SELECT_IMPL_CUDA_CORE &&
-        select_tc_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s))
+        select_tc_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, tc_scratch, s))
         return;
     if (impl == CX_SELECT_IMPL_TC && !(flags & CX_SELECT_GENERIC))
         fail(CX_PRECONDITION_ERROR, "select: the pinned tensor-core selection does not apply to this shape");

@@ -30,12 +30,14 @@ def _threads():
     return max(1, os.cpu_count() or 1)
 
 
-@pytest.mark.parametrize("seed", [3, 2026])
-def test_cfg2_all_groups_vs_oracle(orc, seed):
+@pytest.mark.parametrize("seed,exchange", [(3, 0), (2026, 0), (11, 1)], ids=["auto", "auto2", "clusters"])
+def test_cfg2_all_groups_vs_oracle(orc, cx_option, seed, exchange):
+    """exchange 0: the cost model (cfg2: the cooperative one-wave launch); 1: thread-block clusters."""
     import torch
 
     from paper_2601_01298_b200 import device
     torch.cuda.set_device(0)
+    cx_option("select_exchange", exchange)
     gen = torch.Generator(device="cuda").manual_seed(seed)
     kt = torch.randn(G, L, D, device="cuda", generator=gen)
     vt = torch.randn(G, L, D, device="cuda", generator=gen)

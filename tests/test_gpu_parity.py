@@ -112,12 +112,14 @@ def test_golden_small_cases(cx, orc):
 
 
 @pytest.mark.parametrize("name", ["cfg1_points.npz", "cfg2_group.npz", "cfg4_group.npz"])
-@pytest.mark.parametrize("flags", [0, 1, 2], ids=["filter", "exact_only", "generic"])
-def test_golden_group_selection(dev, orc, name, flags):
+@pytest.mark.parametrize("flags,impl", [(0, "tc"), (1, "tc"), (0, "cuda_core"), (1, "cuda_core"), (2, "auto")],
+                         ids=["tc", "tc_exact_only", "cuda_core", "cuda_core_exact_only", "generic"])
+def test_golden_group_selection(dev, orc, cx_option, name, flags, impl):
     import torch
+    cx_option("select_impl", impl)
     g = np.load(os.path.join(GOLDEN, name))
-    if name == "cfg4_group.npz" and flags == 1:
-        pytest.skip("exact-only at L=32768 is covered by the filtered run")
+    if name == "cfg4_group.npz" and flags == 1 and impl == "cuda_core":
+        pytest.skip("exact-only at L=32768 is covered by the tensor-core exact-only run")
     keys, values, queries = oracle.synthetic_group(orc, int(g["seed"]), int(g["L"]), int(g["dim"]), int(g["n_q"]))
     kt = torch.from_numpy(keys).cuda()[None]
     qt = torch.from_numpy(queries).cuda()[None]
@@ -207,13 +209,15 @@ def test_select128_matches_reference(dev, orc, cx_option, G, L, k, force):
         assert scores[gi].cpu().numpy().tobytes() == sc.tobytes(), gi
 
 
+@pytest.mark.parametrize("impl", ["cuda_core", "tc"])
 @pytest.mark.parametrize("force", ["3", "5"])
-def test_sketch_rows_fp16_overflow(dev, orc, cx_option, force):
+def test_sketch_rows_fp16_overflow(dev, orc, cx_option, force, impl):
     """Sketch-row mode with coordinates beyond the fp16 range (+-65504): the sketch dot
     becomes +-inf / NaN, and the filter must then evaluate exactly (a -inf dot would
     otherwise make the lower bound +inf and skip the row)."""
     import torch
     cx_option("select_cluster", int(force))
+    cx_option("select_impl", impl)
     L, d, k = 4000, 64, 40
     r = orc.rng(515)
     keys = r.gaussian_f32(L * d).reshape(L, d)

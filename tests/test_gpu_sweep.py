@@ -79,11 +79,19 @@ def test_grouped_compress_random_sweep(dev, orc, seed):
             assert seed % 3 == 0 and gaps[gi] == 0.0, (seed, gi, float(gaps[gi]))
 
 
+@pytest.mark.parametrize("impl", ["cuda_core", "tc_cluster", "tc_coop"])
 @pytest.mark.parametrize("seed", list(range(12)))
-def test_grouped_compress_forced_row_modes(dev, orc, cx_option, seed):
-    """The same check with the cluster size forced small (CX_OPT_SELECT_CLUSTER), so the rows beyond
-    the register rows live in shared memory as fp32 or as the fp16 sketch."""
+def test_grouped_compress_forced_row_modes(dev, orc, cx_option, seed, impl):
+    """The same check with the cluster size forced small (CX_OPT_SELECT_CLUSTER): for the CUDA-core
+    kernel the rows beyond the register rows live in shared memory as fp32 or as the fp16 sketch;
+    for the tensor-core kernel the sketch tiles split between shared memory and TMEM, with the
+    exchanges through DSMEM (clusters) or global memory (cooperative launch)."""
     import torch
+    if impl == "cuda_core":
+        cx_option("select_impl", "cuda_core")
+    else:
+        cx_option("select_impl", "tc")
+        cx_option("select_exchange", 1 if impl == "tc_cluster" else 2)
     rs = np.random.default_rng(500 + seed)
     d = int(rs.choice([64, 64, 128]))
     C = int(rs.integers(2, 7))
@@ -92,6 +100,8 @@ def test_grouped_compress_forced_row_modes(dev, orc, cx_option, seed):
     lam = float(rs.choice([0.3, 0.5, 0.8]))
     if (L + C - 1) // C > 2048:
         C = (L + 2047) // 2048
+    if impl != "cuda_core" and d != 64:
+        pytest.skip("the tensor-core selection is d = 64")
     cx_option("select_cluster", C)
     G = 2
     ks, vs, qs = zip(*[oracle.synthetic_group(orc, 9100 + 7 * seed + gi, L, d, 2) for gi in range(G)])
