@@ -255,7 +255,7 @@ struct SelxParams {
 
 
 struct SelxLayout {
-    size_t mbar, mm, hdr, bc, misc, qrow, qres, bop, stage, tiles, total;
+    size_t mbar, mm, hdr, bc, loc, misc, qrow, qres, bop, stage, tiles, total;
 };
 
 __host__ __device__ inline size_t al(size_t x, size_t a = 16) { return (x + a - 1) / a * a; }
@@ -267,6 +267,7 @@ __host__ __device__ inline SelxLayout selx_layout(int n_smem, int C, int n_stage
     l.mm = o;    o = al(o + sizeof(double) * 4 * C * NW);  // X1: one slot per (CTA, warp)
     l.hdr = o;   o = al(o + sizeof(Hdr) * C * NW);        // X2: one candidate per (CTA, warp)
     l.bc = o;    o = al(o + sizeof(float) * D * C * NW);
+    l.loc = o;   o = al(o + NW * (4 * sizeof(unsigned long long) + sizeof(Hdr) + D * sizeof(float)));  // per-warp partials
     l.misc = o;  o = al(o + sizeof(unsigned long long) * 8);
     l.qrow = o;  o = al(o + sizeof(int) * NT);         // exact-evaluation queue: local row
     l.qres = o;  o = al(o + sizeof(double) * 2 * NT);  // ... and its (d^2, d)
@@ -301,6 +302,9 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     Hdr* hdr = reinterpret_cast<Hdr*>(smem + lay.hdr);
     float* bc = reinterpret_cast<float*>(smem + lay.bc);
     unsigned long long* misc = reinterpret_cast<unsigned long long*>(smem + lay.misc);
+    unsigned long long* loc1 = reinterpret_cast<unsigned long long*>(smem + lay.loc);  // [NW][4]
+    Hdr* locH = reinterpret_cast<Hdr*>(loc1 + 4 * NW);                                 // [NW]
+    float* locC = reinterpret_cast<float*>(locH + NW);                                 // [NW][D]
     int* qrow = reinterpret_cast<int*>(smem + lay.qrow);
     double* qres = reinterpret_cast<double*>(smem + lay.qres);
     unsigned char* bop = smem + lay.bop;
@@ -411,7 +415,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     // brings the whole exchange into shared memory, completing on the same mbarrier the
     // cluster pushes would.  (Polling self-stamped words instead measured slower: ~4K vs ~3K
     // cycles per exchange, cross-die L2 round trips.)
-    auto bump = [&](int which) {  // after this warp's slot writes
+    auto bump = [&](int which) {  // after warp 0's slot writes
         __syncwarp();
         if (lane == 0) {
             asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the warp's writes (observed via the sync)
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     };
     auto gather = [&](int which, int round_, uint32_t bytes) {
         if (tid != 0) return;
-        const unsigned target = C * NW * (unsigned)(round_ + 1);
+        const unsigned target = C * (unsigned)(round_ + 1);  // one slot per CTA
         const unsigned* c = p.cnt + 2 * g + which;
         unsigned v;
         do {
@@ -430,10 +434,10 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         const int par = round_ & 1;
         mbar_arrive_expect(&mbar[which], bytes);
         if (which == 0) {
-            bulk_g2s(mm, p.x1g + ((size_t)(2 * g + par) * C * NW) * 4, C * NW * 32u, &mbar[0]);
+            bulk_g2s(mm, p.x1g + ((size_t)(2 * g + par) * C) * 4, C * 32u, &mbar[0]);
         } else {
-            bulk_g2s(hdr, p.x2h + (size_t)(2 * g + par) * C * NW, C * NW * (uint32_t)sizeof(Hdr), &mbar[1]);
-            bulk_g2s(bc, p.x2c + (size_t)(2 * g + par) * C * NW * D, C * NW * D * (uint32_t)sizeof(float), &mbar[1]);
+            bulk_g2s(hdr, p.x2h + (size_t)(2 * g + par) * C, C * (uint32_t)sizeof(Hdr), &mbar[1]);
+            bulk_g2s(bc, p.x2c + (size_t)(2 * g + par) * C * D, C * D * (uint32_t)sizeof(float), &mbar[1]);
         }
     };
 
@@ -621,13 +625,25 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                     st_async_v2(dst + 16, b2_, b3, mb);
                 }
             } else {
+                // cooperative: the CTA's warps combine first (one slot and one counter add per
+                // CTA: 16x fewer global atomics on the group's counter)
                 if (lane == 0) {
-                    unsigned long long* d = p.x1g + ((size_t)(2 * g + (round & 1)) * C * NW + rank * NW + wid) * 4;
-                    reinterpret_cast<ulonglong2*>(d)[0] = make_ulonglong2(b0, b1);
-                    reinterpret_cast<ulonglong2*>(d)[1] = make_ulonglong2(b2_, b3);
+                    loc1[4 * wid] = b0; loc1[4 * wid + 1] = b1; loc1[4 * wid + 2] = b2_; loc1[4 * wid + 3] = b3;
                 }
-                bump(0);
-                gather(0, round, tx1);
+                __syncthreads();
+                if (wid == 0) {
+                    const unsigned long long c0 = wmin64(lane < NW ? loc1[4 * lane] : BITS_INF);
+                    const unsigned long long c1 = wmax64(lane < NW ? loc1[4 * lane + 1] : 0ull);
+                    const unsigned long long c2 = wmin64(lane < NW ? loc1[4 * lane + 2] : BITS_INF);
+                    const unsigned long long c3 = wmax64(lane < NW ? loc1[4 * lane + 3] : 0ull);
+                    if (lane == 0) {
+                        unsigned long long* d = p.x1g + ((size_t)(2 * g + (round & 1)) * C + rank) * 4;
+                        reinterpret_cast<ulonglong2*>(d)[0] = make_ulonglong2(c0, c1);
+                        reinterpret_cast<ulonglong2*>(d)[1] = make_ulonglong2(c2, c3);
+                    }
+                    bump(0);
+                    gather(0, round, C * 32u);
+                }
             }
             XSTAMP(9);
             mbar_wait(&mbar[0], ph1);
@@ -636,7 +652,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             if (CL && tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[0], tx1);
             const unsigned long long* mb64 = reinterpret_cast<const unsigned long long*>(mm);
             b0 = BITS_INF; b1 = 0ull; b2_ = BITS_INF; b3 = 0ull;
-            for (int e = lane; e < (int)C * NW; e += 32) {
+            for (int e = lane; e < (int)C * (CL ? NW : 1); e += 32) {
                 b0 = min(b0, mb64[e * 4 + 0]);
                 b1 = max(b1, mb64[e * 4 + 1]);
                 b2_ = min(b2_, mb64[e * 4 + 2]);
@@ -741,15 +757,47 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                     if (lane < D / 4) st_async_v4(mapa(su32(bc + slot * D + 4 * lane), dst), spec4, mb);
                 }
             } else {
-                const size_t base = (size_t)(2 * g + (round & 1)) * C * NW + slot;
+                // cooperative: the CTA's best candidate first (score desc, row asc; its runner-up
+                // is the best of the other warps or the winning warp's own runner-up)
                 if (lane == 0) {
                     Hdr h;
                     h.score = sc; h.row = rw; h.nb = (double)bnx_w; h.second = b2;
-                    p.x2h[base] = h;
+                    locH[wid] = h;
                 }
-                if (lane < D / 4) reinterpret_cast<float4*>(p.x2c + base * D)[lane] = spec4;
-                bump(1);
-                gather(1, round, tx2);
+                if (lane < D / 4) reinterpret_cast<float4*>(locC + wid * D)[lane] = spec4;
+                __syncthreads();
+                if (wid == 0) {
+                    const bool has = lane < NW && locH[lane].score >= 0.0;
+                    const unsigned long long sb = has ? dbits(locH[lane].score) : 0ull;
+                    const unsigned long long best = wmax64(sb);
+                    const bool cs = has && sb == best;
+                    const unsigned rmin = __reduce_min_sync(0xffffffffu, cs ? (unsigned)locH[lane].row : 0xffffffffu);
+                    const bool iw = cs && (unsigned)locH[lane].row == rmin;
+                    const uint32_t wm = __ballot_sync(0xffffffffu, iw);
+                    const bool any = __ballot_sync(0xffffffffu, has) != 0u;
+                    const int wsl = wm ? __ffs(wm) - 1 : 0;
+                    const bool hs = lane < NW && locH[lane].second >= 0.0;
+                    const bool hr = hs || (has && !iw);
+                    const unsigned long long rb =
+                        hr ? (iw ? dbits(locH[lane].second)
+                                 : max(has ? sb : 0ull, hs ? dbits(locH[lane].second) : 0ull))
+                           : 0ull;
+                    const unsigned long long r2b = wmax64(rb);
+                    const bool any2 = __ballot_sync(0xffffffffu, hr) != 0u;
+                    const size_t base = (size_t)(2 * g + (round & 1)) * C + rank;
+                    if (lane == 0) {
+                        Hdr h;
+                        h.score = any ? locH[wsl].score : -1.0;
+                        h.row = any ? locH[wsl].row : LLONG_MAX;
+                        h.nb = locH[wsl].nb;
+                        h.second = any2 ? bitsd(r2b) : -1.0;
+                        p.x2h[base] = h;
+                    }
+                    if (lane < D / 4)
+                        reinterpret_cast<float4*>(p.x2c + base * D)[lane] = reinterpret_cast<const float4*>(locC + wsl * D)[lane];
+                    bump(1);
+                    gather(1, round, C * (uint32_t)(sizeof(Hdr) + D * sizeof(float)));
+                }
             }
         }
         mbar_wait(&mbar[1], ph2);
@@ -765,7 +813,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             bool lb = false, lr = false;
             long long lrow = LLONG_MAX;
             int le = 0;
-            for (int e = lane; e < (int)C * NW; e += 32) {
+            for (int e = lane; e < (int)C * (CL ? NW : 1); e += 32) {
                 const double es = hdr[e].score, e2 = hdr[e].second;
                 const long long er = hdr[e].row;
                 if (e2 >= 0.0) { l2 = max(l2, dbits(e2)); lr = true; }
