@@ -458,14 +458,16 @@ def run_decode(args, dev, rank=0, world=1):
             q = torch.randn(n, N_LAYERS, N_Q, D, device=dev, generator=gen)
             sets.append((tk, tv, tl, q, torch.empty_like(q), nk, nv))
         for i in range(3 * n_sets):
-            cxd.decode_step(syn_k, syn_v, *sets[i % n_sets])
+            cxd.decode_step(syn_k, syn_v, *sets[i % n_sets], syn_unchanged=i > 0)
         torch.cuda.synchronize()
-        # steady state: back-to-back steps (a decode loop) rotating over the sets
+        # steady state: back-to-back steps (a decode loop) rotating over the sets; the synapse
+        # is not rewritten between steps (no push here), so each step stages it while the
+        # previous one drains (CX_DECODE_SYN_UNCHANGED, programmatic dependent launch)
         reps = 20 * n_sets
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(reps):
-            cxd.decode_step(syn_k, syn_v, *sets[i % n_sets])
+            cxd.decode_step(syn_k, syn_v, *sets[i % n_sets], syn_unchanged=True)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps

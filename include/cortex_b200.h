@@ -244,7 +244,14 @@ typedef struct cx_decode_batch {
     const float* new_values;
     const float* q;            /* [N][n_layers][n_q][d_k] */
     float* out;                /* [N][n_layers][n_q][d_k] */
+    unsigned flags;            /* CX_DECODE_* below (0 = none) */
 } cx_decode_batch;
+
+/* The caller guarantees syn_keys / syn_values were not written since the previous
+ * decode step on the same stream (the synapse between two pushes): the tcgen05
+ * kernel then stages the synapse while the previous step drains (programmatic
+ * dependent launch); everything else still waits for the previous step. */
+#define CX_DECODE_SYN_UNCHANGED 1u
 
 /* Stream-ordered: never synchronizes.  Precondition per agent (the reference
  * KvCache's capacity check, model.cpp:124-140): 0 <= tail_len[a] <= t_cap - 1

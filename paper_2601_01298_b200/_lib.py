@@ -48,6 +48,7 @@ class CxDecodeBatch(C.Structure):
         ("tail_len", c_vp),
         ("new_keys", c_vp), ("new_values", c_vp),
         ("q", c_vp), ("out", c_vp),
+        ("flags", C.c_uint),
     ]
 
 

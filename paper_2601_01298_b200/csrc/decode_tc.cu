@@ -402,6 +402,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                                                                  int* flag, unsigned long long* trc, int skip) {
     extern __shared__ __align__(1024) unsigned char smem[];
     if (threadIdx.x == 0) TC_TRACE(1001);  // kernel start (debugging only)
+#ifdef CX_EXPERIMENTS
+    if (trc && threadIdx.x == 0) trc[2048 + 2 * (blockIdx.y * gridDim.x + blockIdx.x)] = gtime();
+#endif
     const TcLayout lay = tc_layout(b.k_syn, QPG);
     const int NS = lay.ns;
     unsigned char* Kh = smem + lay.kh;
@@ -419,6 +422,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     const int lh = blockIdx.x;
     const int l = lh / b.n_kv, g = lh % b.n_kv;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // programmatic dependent launch: the next step may start its prologue as soon as SMs free
+    // up; this step's own reads / writes of agent data wait for the previous step
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const bool syn_early = (b.flags & CX_DECODE_SYN_UNCHANGED) != 0;
     const int ks = b.k_syn;
     constexpr int AT = TM / QPG;  // agents per tile
     const bool app = b.new_keys != nullptr;
@@ -440,6 +447,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp >= SWARPS || !syn_early) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (warp < SWARPS) {  // K_syn / V_syn^T staging: synapse warps only (the private rows never read them)
         {  // the first Q tile -> L2 during the staging
             const int a0q = (int)blockIdx.y * AT;
@@ -545,36 +553,44 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
                 mma_commit(&mbar[0]);
             }
         };
+        // V_syn^T is first needed by the first P.V: staged while the first scores run (or, when
+        // the synapse is unchanged since the previous step, before that step has finished)
+        auto stage_v = [&]() {
+            const float* sv = b.syn_values + (size_t)lh * ks * TD;
+            constexpr int ST = SWARPS * 32, IT = (TNS_MAX * 8 + ST - 1) / ST;
+            // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
+            for (int base = 0; base < TD * (NS / 8); base += IT * ST) {
+                float xv[IT][8];
+#pragma unroll
+                for (int k = 0; k < IT; ++k) {
+                    const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = 8 * jc + u;
+                        xv[k][u] = (jc < NS / 8 && j < ks) ? __ldg(sv + (size_t)j * TD + c) : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < IT; ++k) {
+                    const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
+                    // B of O = P V (N = dims, K = keys): hi at N-row c, lo at N-row 64 + c (+1024 B)
+                    if (jc < NS / 8) split8_store(xv[k], Vhl, Vhl + cm_off(TD, 0, 2 * TD), cm_off(c, 8 * jc, 2 * TD));
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_sync(1, SWARPS * 32);
+        };
+        if (syn_early) {
+            stage_v();
+            // the synapse is staged: from here on agent data, which the previous step may write
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+        }
         // the first tile's scores are issued before the loop; tile i+1's while tile i's P.V runs
         if (!TC_SKIP(1) && (int)blockIdx.y < n_tiles) {
             stage_q(blockIdx.y);
             issue_s();
         }
-        {  // V_syn^T is first needed by the first P.V: staged while the first scores run
-            const float* sv = b.syn_values + (size_t)lh * ks * TD;
-            constexpr int ST = SWARPS * 32, IT = (TNS_MAX * 8 + ST - 1) / ST;
-        // V^T: item = (dim c, 8-key chunk jc): 8 strided scalar loads (coalesced across lanes)
-        for (int base = 0; base < TD * (NS / 8); base += IT * ST) {
-            float xv[IT][8];
-#pragma unroll
-            for (int k = 0; k < IT; ++k) {
-                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int j = 8 * jc + u;
-                    xv[k][u] = (jc < NS / 8 && j < ks) ? __ldg(sv + (size_t)j * TD + c) : 0.f;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < IT; ++k) {
-                const int it = base + tid + k * ST, c = it & (TD - 1), jc = it >> 6;
-                // B of O = P V (N = dims, K = keys): hi at N-row c, lo at N-row 64 + c (+1024 B)
-                if (jc < NS / 8) split8_store(xv[k], Vhl, Vhl + cm_off(TD, 0, 2 * TD), cm_off(c, 8 * jc, 2 * TD));
-            }
-        }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bar_sync(1, SWARPS * 32);
-        }
+        if (!syn_early) stage_v();
         int ti = 0;
         for (int tile = blockIdx.y; tile < n_tiles; tile += gridDim.y, ++ti) {
             if (tid == 0) TC_TRACE(ti * 16 + 0);
@@ -882,6 +898,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) decode_tc_kernel(cx_decode_batch 
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+#ifdef CX_EXPERIMENTS
+    if (trc && threadIdx.x == 0) trc[2048 + 2 * (blockIdx.y * gridDim.x + blockIdx.x) + 1] = gtime();
+#endif
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tbase_s), "r"(512));
 }
 
@@ -930,8 +949,8 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     static unsigned long long* trc = nullptr;
     const bool tracing = getenv("CX_TC_TRACE") != nullptr;
     if (tracing && !trc) {
-        CX_CUDA(cudaMalloc(&trc, 2048 * sizeof(unsigned long long)));
-        CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
+        CX_CUDA(cudaMalloc(&trc, 8192 * sizeof(unsigned long long)));
+        CX_CUDA(cudaMemset(trc, 0, 8192 * sizeof(unsigned long long)));
     }
     if (tracing) trc_arg = trc;
     skip = getenv("CX_TC_SKIP") ? atoi(getenv("CX_TC_SKIP")) : 0;
@@ -945,12 +964,23 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
     }
 #endif
     kernel_smem(kern, smem);
-    kern<<<dim3((unsigned)n_lh, (unsigned)per_lh), TTHREADS, smem, s>>>(b, (float)(1.0 / std::sqrt((double)b.d_k)),
-                                                                             ctx->d_flag, trc_arg, skip);
-    check_launch("decode_tc_kernel");
+    {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)n_lh, (unsigned)per_lh);
+        lc.blockDim = dim3(TTHREADS);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol in the kernel)
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        CX_CUDA(cudaLaunchKernelEx(&lc, kern, b, (float)(1.0 / std::sqrt((double)b.d_k)), ctx->d_flag, trc_arg, skip));
+        count_launch();
+    }
 #ifdef CX_EXPERIMENTS
     if (tracing) {  // debugging only: per-tile phase times of CTA (0, 0), us since the staging ended
-        std::vector<unsigned long long> h(2048);
+        std::vector<unsigned long long> h(8192);
         CX_CUDA(cudaStreamSynchronize(s));
         CX_CUDA(cudaMemcpy(h.data(), trc, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost));
         const double t0 = (double)h[1000];
@@ -964,7 +994,19 @@ bool decode_tc_launch(cx_ctx* ctx, const cx_decode_batch& b, cudaStream_t s) {
             for (int k = 8; k < 15; ++k) fprintf(stderr, " %7.2f", h[ti * 16 + k] ? (h[ti * 16 + k] - t0) / 1e3 : -1.0);
             fprintf(stderr, "\n");
         }
-        CX_CUDA(cudaMemset(trc, 0, 2048 * sizeof(unsigned long long)));
+        {  // every CTA's start / end (us, from the first start)
+            const int nc = n_lh * per_lh;
+            unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+            double dur = 0;
+            for (int i = 0; i < nc; ++i) {
+                const unsigned long long a = h[2048 + 2 * i], b = h[2048 + 2 * i + 1];
+                s0 = std::min(s0, a); s1 = std::max(s1, a); e0 = std::min(e0, b); e1 = std::max(e1, b);
+                dur += (double)(b - a);
+            }
+            fprintf(stderr, "decode_tc CTAs: starts %.2f..%.2f us, ends %.2f..%.2f us, mean duration %.2f us\n", 0.0,
+                    (s1 - s0) / 1e3, (e0 - s0) / 1e3, (e1 - s0) / 1e3, dur / nc / 1e3);
+        }
+        CX_CUDA(cudaMemset(trc, 0, 8192 * sizeof(unsigned long long)));
     }
 #endif
     return true;

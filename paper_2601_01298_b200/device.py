@@ -187,11 +187,14 @@ def compress_grouped_host(keys: torch.Tensor, values: torch.Tensor, queries: tor
 
 def decode_step(syn_keys: torch.Tensor, syn_values: torch.Tensor, tail_keys: torch.Tensor,
                 tail_values: torch.Tensor, tail_len: torch.Tensor, q: torch.Tensor, out: torch.Tensor,
-                new_keys: torch.Tensor | None = None, new_values: torch.Tensor | None = None) -> torch.Tensor:
+                new_keys: torch.Tensor | None = None, new_values: torch.Tensor | None = None,
+                syn_unchanged: bool = False) -> torch.Tensor:
     """One decode step of N agents against the shared synapse (append + attend).
 
     syn_*: [n_layers, n_kv, k, d_k]; tail_*: [N, n_layers, n_kv, t_cap, d_k];
     tail_len: [N] int32; q/out: [N, n_layers, n_q, d_k]; new_*: [N, n_layers, n_kv, d_k].
+    syn_unchanged: the synapse was not written since the previous step on this stream
+    (CX_DECODE_SYN_UNCHANGED: its staging overlaps the previous step's tail).
     """
     n_layers, n_kv, k_syn, d_k = syn_keys.shape
     N, _, _, t_cap, _ = tail_keys.shape
@@ -210,6 +213,7 @@ def decode_step(syn_keys: torch.Tensor, syn_values: torch.Tensor, tail_keys: tor
     b.new_keys = new_keys.data_ptr() if new_keys is not None else None
     b.new_values = new_values.data_ptr() if new_values is not None else None
     b.q, b.out = q.data_ptr(), out.data_ptr()
+    b.flags = 1 if syn_unchanged else 0
     check(lib.cx_decode_step_dev(ctx(q.device.index), C.byref(b), _stream()), "decode_step")
     return out
 

@@ -18,7 +18,7 @@ for impl in impls:
       torch.cuda.synchronize()
       e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
       e0.record()
-      for _ in range(20): cxd.decode_step(sk, sv, tk, tv, tl, q, o, nk, nv)
+      for _ in range(20): cxd.decode_step(sk, sv, tk, tv, tl, q, o, nk, nv, syn_unchanged=os.environ.get('PDL') == '1')
       e1.record(); torch.cuda.synchronize()
       ms = e0.elapsed_time(e1) / 20
       B = 24*2*164*64*4*2 + N*(24576*33 + 172032)
