@@ -1,23 +1,64 @@
-// cortex/model.hpp -- B200 drop-in for the KvCache part of
-// proj/include/cortex/model.hpp:16,67-113.  Storage lives in HBM (cx_kvcache,
+// cortex/model.hpp -- B200 drop-in for proj/include/cortex/model.hpp (Origin,
+// LayerWeights, WeightStore, KvCache, StepResult, forward_step, generate_greedy,
+// the byte tokenizer).  KvCache storage lives in HBM (cx_kvcache,
 // [n_layers][capacity][d_model] fp32); key()/value()/layer_keys() return spans
 // over a host mirror that is kept in step with host-side appends and re-synced
-// from the device after device-side appends (inject_dev, decode appends).
-// WeightStore / forward_step (dense model compute) are out of scope
-// (SURVEY.md §8(f) "next").
+// from the device after device-side appends.  WeightStore keeps the reference's
+// host vectors (same seeded draw order) plus a device copy created on first use;
+// forward_step runs on the device (cx_forward_step_dev).
 #pragma once
 
 #include "cortex/config.hpp"
 
 #include <cstdint>
+#include <memory>
 #include <span>
+#include <string>
+#include <string_view>
 #include <vector>
 
 struct cx_kvcache;
+struct cx_weights;
 
 namespace cortex {
 
 enum class Origin : uint8_t { context, injected };
+
+struct LayerWeights {
+    std::vector<float> attn_norm;       // d_model
+    std::vector<float> wq, wk, wv, wo;  // d_model x d_model, row-major
+    std::vector<float> mlp_norm;        // d_model
+    std::vector<float> w_in;            // d_ff x d_model
+    std::vector<float> w_out;           // d_model x d_ff
+};
+
+class WeightStore {
+public:
+    static WeightStore init(const ModelConfig& cfg);
+
+    const ModelConfig& config() const { return cfg_; }
+    const LayerWeights& layer(int l) const { return layers_[static_cast<size_t>(l)]; }
+    std::span<const float> embedding_row(int token) const;
+    const std::vector<float>& final_norm() const { return final_norm_; }
+    const std::vector<float>& unembedding() const { return unembedding_; }
+
+    int64_t parameter_count() const { return parameter_count_; }
+    int64_t total_bytes() const { return parameter_count_ * 4; }
+
+    // ---- B200 extension: the device copy (created on first use, shared by copies)
+    cx_weights* device_handle() const;
+
+private:
+    WeightStore() = default;
+
+    ModelConfig cfg_;
+    std::vector<float> embedding_;
+    std::vector<LayerWeights> layers_;
+    std::vector<float> final_norm_;
+    std::vector<float> unembedding_;
+    int64_t parameter_count_ = 0;
+    mutable std::shared_ptr<cx_weights> dev_;
+};
 
 class KvCache {
 public:
@@ -25,8 +66,8 @@ public:
     ~KvCache();
     KvCache(KvCache&& o) noexcept;
     KvCache& operator=(KvCache&& o) noexcept;
-    KvCache(const KvCache&) = delete;
-    KvCache& operator=(const KvCache&) = delete;
+    KvCache(const KvCache& o);             // deep copy on the device (cx_kvcache_clone)
+    KvCache& operator=(const KvCache& o);
 
     const ModelConfig& config() const { return cfg_; }
     int64_t size() const;
@@ -65,5 +106,18 @@ private:
     mutable int64_t mirror_rows_ = 0;
     std::vector<int> layer_rows_;  // rows mirrored per layer while an entry is open
 };
+
+struct StepResult {
+    std::vector<float> logits;       // vocab_size
+    std::vector<float> hidden_last;  // d_model, after the final norm
+    std::vector<float> final_query;  // d_model, final-layer post-RoPE query
+};
+
+StepResult forward_step(const WeightStore& w, KvCache& cache, int token, int64_t position);
+
+std::vector<int> generate_greedy(const WeightStore& w, std::span<const int> prompt, int n_new);
+
+std::vector<int> tokenize_bytes(std::string_view text);
+std::string detokenize_bytes(std::span<const int> tokens);
 
 }  // namespace cortex

@@ -295,6 +295,8 @@ typedef struct cx_kvcache cx_kvcache;
 cx_status cx_kvcache_create(int n_layers, int n_heads, int d_model, int d_k,
                             int64_t max_positions, int64_t capacity, cx_kvcache** out);
 cx_status cx_kvcache_destroy(cx_kvcache* c);
+/* deep copy (the reference KvCache is a value type): rows, positions, origins, state */
+cx_status cx_kvcache_clone(const cx_kvcache* src, cx_kvcache** out);
 int64_t cx_kvcache_size(const cx_kvcache* c);
 int64_t cx_kvcache_context_count(const cx_kvcache* c);
 int64_t cx_kvcache_last_context_position(const cx_kvcache* c);
@@ -381,6 +383,46 @@ cx_status cx_synapse_buffer_wait_nonempty(cx_synapse_buffer* b, int64_t timeout_
                                           const cx_snapshot** out);
 cx_status cx_synapse_buffer_shutdown(cx_synapse_buffer* b);
 cx_status cx_snapshot_release(const cx_snapshot* s);
+
+/* Device memory helpers for C consumers of the *_dev entry points: allocate /
+ * free device bytes, and a synchronous read of device bytes ordered on `stream`. */
+cx_status cx_device_alloc(size_t bytes, void** out);
+cx_status cx_device_free(void* p);
+cx_status cx_device_read(void* host, const void* dev, size_t bytes, void* stream);
+
+/* ======================================================================
+ * The toy transformer on the device: WeightStore,
+ * forward_step batched across agents, and the kernels:: primitives it uses.
+ * ====================================================================== */
+typedef struct cx_weights cx_weights;
+/* floats of the flat weight array, in the reference's draw order (model.cpp:49-80):
+ * embedding [vocab][d], per layer {attn_norm [d], wq, wk, wv, wo [d][d], mlp_norm [d],
+ * w_in [4d][d], w_out [d][4d]}, final_norm [d], unembedding [vocab][d] */
+size_t cx_weights_flat_floats(int n_layers, int d_model, int vocab_size);
+cx_status cx_weights_create(int n_layers, int n_heads, int d_model, int d_k, int vocab_size,
+                            int64_t max_positions, double rope_base, const float* flat,
+                            cx_weights** out);
+cx_status cx_weights_destroy(cx_weights* w);
+
+/* forward_step (model.hpp:130-131, model.cpp:175-235) for n_agents agents at once:
+ * agent i feeds tokens[i] at positions[i] (host arrays) into caches[i] (distinct
+ * caches) and gets logits [i][vocab], hidden [i][d] (after the final norm) and
+ * final_query [i][d] (final layer, post RoPE) -- device outputs, any may be NULL.
+ * Every agent is checked (token range, open entry, position bounds, strictly
+ * increasing context positions) before any device work, with the reference's
+ * error categories.  Projections, RMSNorm, RoPE and attention accumulate in fp64
+ * (the reference's rounding points), so logits agree to ~1e-12 relative. */
+cx_status cx_forward_step_dev(cx_ctx* ctx, const cx_weights* w, int n_agents, cx_kvcache* const* caches,
+                              const int* tokens, const int64_t* positions, float* logits,
+                              float* hidden, float* final_query, void* stream);
+
+/* kernels.hpp:14-28 (host pointers, computed on the device, synchronous):
+ * matvec y = W x (fp64 accumulate), rmsnorm, add_inplace (op 0: x += y) and
+ * relu_inplace (op 1), apply_rope. */
+cx_status cx_matvec(const float* w, int n_out, int n_in, const float* x, float* y);
+cx_status cx_rmsnorm(const float* x, const float* gain, int64_t n, double eps, float* out);
+cx_status cx_elementwise(float* x, const float* y, int64_t n, int op);
+cx_status cx_apply_rope(float* v, int64_t n, int64_t position, double rope_base);
 
 /* ======================================================================
  * Multi-GPU (the reference has none -- SPEC.md:15).

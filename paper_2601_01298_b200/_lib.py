@@ -94,6 +94,18 @@ _SIGS = [
     ("cx_selection_gaps", C.c_int, [c_vp, C.c_int, c_vp, c_vp]),
     ("cx_ctx_set_option", C.c_int, [c_vp, C.c_int, C.c_int64]),
     ("cx_nccl_version", C.c_int, []),
+    ("cx_weights_flat_floats", C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    ("cx_weights_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_double, c_vp,
+                                     C.POINTER(c_vp)]),
+    ("cx_weights_destroy", C.c_int, [c_vp]),
+    ("cx_forward_step_dev", C.c_int, [c_vp, c_vp, C.c_int, C.POINTER(c_vp), c_i32p, c_i64p, c_vp, c_vp, c_vp, c_vp]),
+    ("cx_device_alloc", C.c_int, [C.c_size_t, C.POINTER(c_vp)]),
+    ("cx_device_free", C.c_int, [c_vp]),
+    ("cx_device_read", C.c_int, [c_vp, c_vp, C.c_size_t, c_vp]),
+    ("cx_matvec", C.c_int, [c_f32p, C.c_int, C.c_int, c_f32p, c_f32p]),
+    ("cx_rmsnorm", C.c_int, [c_f32p, c_f32p, C.c_int64, C.c_double, c_f32p]),
+    ("cx_elementwise", C.c_int, [c_f32p, c_f32p, C.c_int64, C.c_int]),
+    ("cx_apply_rope", C.c_int, [c_f32p, C.c_int64, C.c_int64, C.c_double]),
     ("cx_probe_fp64_rate", C.c_int, [c_vp, C.POINTER(C.c_double)]),
     ("cx_comm_unique_id", C.c_int, [c_vp]),
     ("cx_comm_init_rank", C.c_int, [C.c_int, c_vp, C.c_int, C.c_int, C.POINTER(c_vp)]),
@@ -118,6 +130,7 @@ _SIGS = [
     ("cx_decode_step_dev", C.c_int, [c_vp, C.POINTER(CxDecodeBatch), c_vp]),
     ("cx_kvcache_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.POINTER(c_vp)]),
     ("cx_kvcache_destroy", C.c_int, [c_vp]),
+    ("cx_kvcache_clone", C.c_int, [c_vp, C.POINTER(c_vp)]),
     ("cx_kvcache_size", C.c_int64, [c_vp]),
     ("cx_kvcache_context_count", C.c_int64, [c_vp]),
     ("cx_kvcache_last_context_position", C.c_int64, [c_vp]),

@@ -916,24 +916,8 @@ extern "C" cx_status cx_decode_step_dev(cx_ctx* c, const cx_decode_batch* b, voi
 // ============================================================================
 // device KvCache (model.hpp:67-113)
 // ============================================================================
-struct cx_kvcache {
-    int n_layers, n_heads, d_model, d_k;
-    int64_t max_positions;
-    int64_t capacity = 0;
-    float* keys = nullptr;    // [n_layers][capacity][d_model]
-    float* values = nullptr;
-    std::vector<int64_t> positions;
-    std::vector<uint8_t> origins;
-    int64_t last_context_position = -1;
-    int64_t context_count = 0;
-    bool entry_open = false;
-    int layers_written = 0;
-    cudaStream_t stream = nullptr;  // ordering for all of this cache's device work
-    cudaEvent_t ev = nullptr;       // cross-stream ordering with appends on caller streams
-};
 
-namespace {
-
+namespace cx {
 // Appends may run on a caller stream s.  Before: s waits for the cache's own pending work
 // (a regrow's copies).  After: the cache's stream waits for s, so a later regrow, read or
 // selection (all on c->stream) is ordered after the append.
@@ -972,6 +956,10 @@ void kv_grow(cx_kvcache* c, int64_t need) {
     c->values = nv;
     c->capacity = cap;
 }
+}  // namespace cx
+
+namespace {
+
 
 // model.cpp:124-140 (begin_entry) checks + host-side bookkeeping
 void kv_begin(cx_kvcache* c, int64_t position, cx_origin origin) {
@@ -1018,6 +1006,41 @@ extern "C" cx_status cx_kvcache_create(int n_layers, int n_heads, int d_model, i
             delete c;
             throw;
         }
+        *out = c;
+    });
+}
+
+// value semantics of the reference KvCache (model.hpp:67-113 is copyable): a deep copy
+extern "C" cx_status cx_kvcache_clone(const cx_kvcache* src, cx_kvcache** out) {
+    return guard([&] {
+        if (!src || !out) fail(CX_INVALID_ARGUMENT, "null cache/out");
+        cx_kvcache* c = nullptr;
+        const cx_status st = cx_kvcache_create(src->n_layers, src->n_heads, src->d_model, src->d_k, src->max_positions,
+                                               std::max<int64_t>(1, src->capacity), &c);
+        if (st != CX_OK) fail(st, cx_last_error());
+        try {
+            CX_CUDA(cudaStreamSynchronize(src->stream));  // the source's pending appends
+            const int64_t rows = (int64_t)src->positions.size() + (src->entry_open ? 1 : 0);
+            if (rows > 0)
+                for (int l = 0; l < src->n_layers; ++l) {
+                    const size_t o_src = (size_t)l * src->capacity * src->d_model;
+                    const size_t o_dst = (size_t)l * c->capacity * c->d_model;
+                    CX_CUDA(cudaMemcpyAsync(c->keys + o_dst, src->keys + o_src, sizeof(float) * rows * src->d_model,
+                                            cudaMemcpyDeviceToDevice, c->stream));
+                    CX_CUDA(cudaMemcpyAsync(c->values + o_dst, src->values + o_src,
+                                            sizeof(float) * rows * src->d_model, cudaMemcpyDeviceToDevice, c->stream));
+                }
+            CX_CUDA(cudaStreamSynchronize(c->stream));
+        } catch (...) {
+            cx_kvcache_destroy(c);
+            throw;
+        }
+        c->positions = src->positions;
+        c->origins = src->origins;
+        c->last_context_position = src->last_context_position;
+        c->context_count = src->context_count;
+        c->entry_open = src->entry_open;
+        c->layers_written = src->layers_written;
         *out = c;
     });
 }

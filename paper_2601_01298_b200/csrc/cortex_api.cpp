@@ -93,6 +93,19 @@ KvCache::KvCache(KvCache&& o) noexcept
     o.h_ = nullptr;
 }
 
+KvCache::KvCache(const KvCache& o)
+    : cfg_(o.cfg_), hk_(o.hk_), hv_(o.hv_), mirror_rows_(o.mirror_rows_), layer_rows_(o.layer_rows_) {
+    ck(cx_kvcache_clone(o.h_, &h_));
+}
+
+KvCache& KvCache::operator=(const KvCache& o) {
+    if (this != &o) {
+        KvCache tmp(o);
+        *this = std::move(tmp);
+    }
+    return *this;
+}
+
 KvCache& KvCache::operator=(KvCache&& o) noexcept {
     if (this != &o) {
         if (h_) cx_kvcache_destroy(h_);

@@ -136,7 +136,29 @@ struct cx_ctx {
     std::mutex mu;
 };
 
+// Device KvCache (model.hpp:67-113): storage in HBM, host-checked append protocol.
+struct cx_kvcache {
+    int n_layers, n_heads, d_model, d_k;
+    int64_t max_positions;
+    int64_t capacity = 0;
+    float* keys = nullptr;    // [n_layers][capacity][d_model]
+    float* values = nullptr;
+    std::vector<int64_t> positions;
+    std::vector<uint8_t> origins;
+    int64_t last_context_position = -1;
+    int64_t context_count = 0;
+    bool entry_open = false;
+    int layers_written = 0;
+    cudaStream_t stream = nullptr;  // ordering for all of this cache's device work
+    cudaEvent_t ev = nullptr;       // cross-stream ordering with appends on caller streams
+};
+
 namespace cx {
+
+// KvCache stream ordering and growth (capi.cu)
+void kv_before(cx_kvcache* c, cudaStream_t s);  // s waits for the cache's pending work
+void kv_after(cx_kvcache* c, cudaStream_t s);   // the cache's stream waits for s
+void kv_grow(cx_kvcache* c, int64_t need);      // capacity >= need rows (copies, synchronous)
 
 // Thread-local default context for the reference-shaped host calls.
 cx_ctx* default_ctx();
