@@ -212,6 +212,16 @@ cx_status cx_compress_grouped_dev(cx_ctx* ctx, const cx_groups* g, const float* 
                                   int64_t* out_rows, double* out_scores,
                                   float* syn_keys, float* syn_values, void* stream);
 
+/* cx_compress_grouped_dev with the synapse blocks syn_group_stride floats apart
+ * (0 = take * dim): e.g. a per-KV-head view of the river cache compressed
+ * straight into the decode layout [layer][kv head][k][d_k] (stride n_kv * k * d_k,
+ * base + head * k * d_k), with no copy. */
+cx_status cx_compress_grouped_strided_dev(cx_ctx* ctx, const cx_groups* g, const float* values,
+                                          int k, double lambda, unsigned flags,
+                                          int64_t* out_rows, double* out_scores,
+                                          float* syn_keys, float* syn_values,
+                                          int64_t syn_group_stride, void* stream);
+
 /* One synapse compression from HOST buffers (the end-to-end call): dense
  * keys/values [G][count][dim], queries [G][n_pass][d_k] (n_pass/d_k/col_step as
  * in cx_groups); outputs (host): rows/scores [G][take], syn_keys/syn_values
@@ -423,6 +433,76 @@ cx_status cx_matvec(const float* w, int n_out, int n_in, const float* x, float* 
 cx_status cx_rmsnorm(const float* x, const float* gain, int64_t n, double eps, float* out);
 cx_status cx_elementwise(float* x, const float* y, int64_t n, int op);
 cx_status cx_apply_rope(float* v, int64_t n, int64_t position, double rope_base);
+
+/* ======================================================================
+ * The River / Stream loop on the device (BASELINE
+ * configs[4]): Scheduler::run's device work, scheduler.cpp:63-165.
+ * River lane (greatest priority; the calling host thread): per river token the
+ * token's forward_step on the river cache; every inject_every tokens a thought
+ * (thought_tokens ids) is encoded at the next reserved virtual positions
+ * (encode_thought) and injected before the token; every push_every tokens (when
+ * the previous push has been published) a synapse push into the back buffer.
+ * Stream lane (medium priority; a second host thread): each agent step is every
+ * agent decoding one token against the front synapse (one CUDA-graph replay).
+ * A push is published (version + 1) at the first agent step after its completion
+ * event fired, and that step waits on it: agents never read a partly written
+ * synapse (SynapseBuffer::push / read_latest, synapse.hpp:115-135).
+ * ====================================================================== */
+typedef struct cx_cortex cx_cortex;
+#define CX_CORTEX_PUSH_SCHEDULER 0 /* Scheduler::push_synapse (scheduler.cpp:158-165): select_landmarks
+                                      over the last layer's context keys with the river's final query
+                                      (synapse.cpp:286-323), one row set for every layer and head */
+#define CX_CORTEX_PUSH_GROUPS 1    /* one selection per (layer, KV head) group with the fixed
+                                      river_queries (the BASELINE cfg2 decomposition, 48 groups) */
+typedef struct cx_cortex_config {
+    int n_agents;            /* stream agents */
+    int n_q;                 /* agent query heads per layer (GQA: n_q / n_kv per KV head) */
+    int t_cap;               /* agent private rows */
+    int k;                   /* landmarks (per group in CX_CORTEX_PUSH_GROUPS) */
+    double lambda;
+    int push_every;          /* river tokens between pushes (a push waits for the previous one) */
+    int inject_every;        /* river tokens between injections */
+    int thought_tokens;      /* tokens per injected thought */
+    int64_t virtual_base;    /* first reserved virtual position (RuntimeConfig::virtual_base) */
+    int64_t max_context;     /* context rows the push mirror holds (>= the prefill) */
+    int push_mode;           /* CX_CORTEX_PUSH_* */
+} cx_cortex_config;
+typedef struct cx_cortex_agents {  /* device tensors, the cx_decode_batch layouts */
+    float* tail_keys;
+    float* tail_values;
+    const int32_t* tail_len;
+    const float* new_keys;
+    const float* new_values;
+    const float* q;
+    float* out;
+    const float* river_queries;     /* CX_CORTEX_PUSH_GROUPS: [n_kv][n_layers][n_q / n_kv][d_k] */
+} cx_cortex_agents;
+typedef struct cx_cortex_stats {
+    double agent_ms, river_ms, push_ms_mean;  /* lane spans (device events) and mean push */
+    int pushes, injections;
+    uint64_t last_version;
+} cx_cortex_stats;
+/* river: the prefilled river cache (context rows only); it must outlive the runtime.
+ * The first synapse is pushed and published (version 1) before this returns
+ * (CX_CORTEX_PUSH_SCHEDULER: with the final query of the river's last forward_step
+ * through this runtime, zeros before the first one). */
+cx_status cx_cortex_create(cx_ctx* ctx, const cx_weights* w, cx_kvcache* river,
+                           const cx_cortex_config* cfg, const cx_cortex_agents* agents,
+                           cx_cortex** out);
+/* n_river_tokens river tokens (host ids) at the next river positions, concurrently
+ * with n_agent_steps agent steps.  thought_tokens: host ids, thought_tokens per
+ * injection, ceil(n_river_tokens / inject_every) thoughts.
+ * versions_used (host, optional): the synapse version each agent step read;
+ * river_logits (device, optional): [n_river_tokens][vocab].  Audit (device,
+ * optional): synapse_history [max_versions][K | V][n_layers][n_kv][k][d_k] gets
+ * every version as published (at its version index); out_history
+ * [n_agent_steps][agents' out]. */
+cx_status cx_cortex_run(cx_cortex* rt, int n_river_tokens, const int* river_tokens, const int* thought_tokens,
+                        int n_agent_steps, cx_cortex_stats* stats, uint64_t* versions_used,
+                        float* river_logits, float* synapse_history, int max_versions, float* out_history);
+/* the latest published synapse (keys / values [n_layers][n_kv][k][d_k], any memory) */
+cx_status cx_cortex_front_synapse(const cx_cortex* rt, float* keys, float* values, uint64_t* version);
+cx_status cx_cortex_destroy(cx_cortex* rt);
 
 /* ======================================================================
  * Multi-GPU (the reference has none -- SPEC.md:15).

@@ -17,7 +17,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libcortex_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["synapse_kernels.cu", "select64.cu", "select128.cu", "select_tc.cu", "attend_kernels.cu", "decode_tc.cu", "capi.cu", "comm.cu", "probe.cu", "forward.cu"]
+CU_SOURCES = ["synapse_kernels.cu", "select64.cu", "select128.cu", "select_tc.cu", "attend_kernels.cu", "decode_tc.cu", "capi.cu", "comm.cu", "probe.cu", "forward.cu", "cortex_runtime.cu"]
 CPP_SOURCES = ["cortex_api.cpp", "cortex_model.cpp"]
 
 NVCC_FLAGS = [

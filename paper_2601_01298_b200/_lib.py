@@ -61,6 +61,23 @@ class CxInjectionRecord(C.Structure):
     ]
 
 
+class CxCortexConfig(C.Structure):
+    _fields_ = [("n_agents", C.c_int), ("n_q", C.c_int), ("t_cap", C.c_int), ("k", C.c_int),
+                ("lambda_", C.c_double), ("push_every", C.c_int), ("inject_every", C.c_int),
+                ("thought_tokens", C.c_int), ("virtual_base", C.c_int64), ("max_context", C.c_int64),
+                ("push_mode", C.c_int)]
+
+
+class CxCortexAgents(C.Structure):
+    _fields_ = [("tail_keys", c_vp), ("tail_values", c_vp), ("tail_len", c_vp), ("new_keys", c_vp),
+                ("new_values", c_vp), ("q", c_vp), ("out", c_vp), ("river_queries", c_vp)]
+
+
+class CxCortexStats(C.Structure):
+    _fields_ = [("agent_ms", C.c_double), ("river_ms", C.c_double), ("push_ms_mean", C.c_double),
+                ("pushes", C.c_int), ("injections", C.c_int), ("last_version", C.c_uint64)]
+
+
 # (name, restype, argtypes); cx_status-returning calls use C.c_int.
 _SIGS = [
     ("cx_abi_version", C.c_int, []),
@@ -128,6 +145,8 @@ _SIGS = [
     ("cx_compress_grouped_dev", C.c_int,
      [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp, c_vp, c_vp]),
     ("cx_decode_step_dev", C.c_int, [c_vp, C.POINTER(CxDecodeBatch), c_vp]),
+    ("cx_compress_grouped_strided_dev", C.c_int,
+     [c_vp, C.POINTER(CxGroups), c_vp, C.c_int, C.c_double, C.c_uint, c_vp, c_vp, c_vp, c_vp, C.c_int64, c_vp]),
     ("cx_kvcache_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.POINTER(c_vp)]),
     ("cx_kvcache_destroy", C.c_int, [c_vp]),
     ("cx_kvcache_clone", C.c_int, [c_vp, C.POINTER(c_vp)]),
@@ -172,6 +191,13 @@ _SIGS = [
     ("cx_synapse_buffer_read_latest", C.c_int, [c_vp, C.POINTER(c_vp)]),
     ("cx_synapse_buffer_wait_nonempty", C.c_int, [c_vp, C.c_int64, C.POINTER(c_vp)]),
     ("cx_synapse_buffer_shutdown", C.c_int, [c_vp]),
+    ("cx_cortex_create", C.c_int,
+     [c_vp, c_vp, c_vp, C.POINTER(CxCortexConfig), C.POINTER(CxCortexAgents), C.POINTER(c_vp)]),
+    ("cx_cortex_run", C.c_int,
+     [c_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int, C.POINTER(CxCortexStats),
+      C.POINTER(C.c_uint64), c_vp, c_vp, C.c_int, c_vp]),
+    ("cx_cortex_front_synapse", C.c_int, [c_vp, c_vp, c_vp, C.POINTER(C.c_uint64)]),
+    ("cx_cortex_destroy", C.c_int, [c_vp]),
 ]
 
 EXPORTED_SYMBOLS = [s[0] for s in _SIGS]

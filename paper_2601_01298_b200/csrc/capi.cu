@@ -676,7 +676,8 @@ namespace {
 
 // attention || centroid, selection, landmark gather for the groups of `gr` (validated)
 void compress_impl(cx_ctx* c, const cx_groups* gr, const float* values, int k, double lambda, unsigned flags,
-                   int64_t* out_rows, double* out_scores, float* syn_keys, float* syn_values, void* stream) {
+                   int64_t* out_rows, double* out_scores, float* syn_keys, float* syn_values, void* stream,
+                   int64_t syn_gstride = 0) {
     {
         GroupView g = view_of(gr);
         const int take = (int)std::min<int64_t>(k, g.L);
@@ -701,8 +702,13 @@ void compress_impl(cx_ctx* c, const cx_groups* gr, const float* values, int k, d
         c->arena.used = mark;  // attention scratch is dead once `attn` is written (stream-ordered)
         CX_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
         select_grouped(c, g, attn, k, lambda, flags, out_rows, out_scores, s, cen);
-        if (syn_keys) gather_rows(g, g.X, out_rows, take, syn_keys, s);
-        if (syn_values && values) gather_rows(g, values, out_rows, take, syn_values, s);
+        const int64_t gs = syn_gstride > 0 ? syn_gstride : (int64_t)take * g.dim;
+        if (syn_keys && syn_values && values)  // keys and values in one launch
+            gather_rows2(g, g.X, values, out_rows, take, syn_keys, syn_values, gs, s);
+        else if (syn_keys)
+            gather_rows2(g, g.X, nullptr, out_rows, take, syn_keys, nullptr, gs, s);
+        else if (syn_values && values)
+            gather_rows2(g, values, nullptr, out_rows, take, syn_values, nullptr, gs, s);
     }
 }
 
@@ -718,6 +724,26 @@ extern "C" cx_status cx_compress_grouped_dev(cx_ctx* c, const cx_groups* gr, con
         validate_groups(gr, true);
         if (!out_rows || !out_scores) fail(CX_INVALID_ARGUMENT, "null outputs");
         compress_impl(c, gr, values, k, lambda, flags, out_rows, out_scores, syn_keys, syn_values, stream);
+    });
+}
+
+// the same with the synapse blocks syn_group_stride floats apart (0: take * dim), e.g. straight
+// into the decode layout [layer][kv head][k][d_k] from a per-head view of the river cache
+extern "C" cx_status cx_compress_grouped_strided_dev(cx_ctx* c, const cx_groups* gr, const float* values, int k,
+                                                     double lambda, unsigned flags, int64_t* out_rows,
+                                                     double* out_scores, float* syn_keys, float* syn_values,
+                                                     int64_t syn_group_stride, void* stream) {
+    return guard([&] {
+        if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
+        if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
+        if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
+        validate_groups(gr, true);
+        if (!out_rows || !out_scores) fail(CX_INVALID_ARGUMENT, "null outputs");
+        const int64_t take = std::min<int64_t>(k, gr->count);
+        if (syn_group_stride != 0 && syn_group_stride < take * gr->dim)
+            fail(CX_INVALID_ARGUMENT, "syn_group_stride smaller than a group's take * dim");
+        compress_impl(c, gr, values, k, lambda, flags, out_rows, out_scores, syn_keys, syn_values, stream,
+                      syn_group_stride);
     });
 }
 
@@ -934,7 +960,8 @@ void kv_after(cx_kvcache* c, cudaStream_t s) {
 
 void kv_grow(cx_kvcache* c, int64_t need) {
     if (need <= c->capacity) return;
-    int64_t cap = std::max<int64_t>(need, std::max<int64_t>(64, c->capacity * 2));
+    // the first allocation is exactly the requested capacity; growth doubles (at least 64 rows)
+    int64_t cap = c->capacity == 0 ? need : std::max<int64_t>(need, std::max<int64_t>(64, c->capacity * 2));
     const size_t per_layer_old = (size_t)c->capacity * c->d_model;
     const size_t per_layer_new = (size_t)cap * c->d_model;
     float *nk = nullptr, *nv = nullptr;

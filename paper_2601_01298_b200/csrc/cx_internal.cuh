@@ -153,6 +153,26 @@ struct cx_kvcache {
     cudaEvent_t ev = nullptr;       // cross-stream ordering with appends on caller streams
 };
 
+// Weights in the reference's draw order (model.cpp:49-80): embedding [vocab][d],
+// per layer {attn_norm [d], wq, wk, wv, wo [d][d], mlp_norm [d], w_in [dff][d],
+// w_out [d][dff]}, final_norm [d], unembedding [vocab][d].
+struct cx_weights {
+    int n_layers = 0, n_heads = 0, d_model = 0, d_k = 0, vocab = 0;
+    int64_t max_positions = 0;
+    double rope_base = 10000.0;
+    float* buf = nullptr;
+    size_t per_layer = 0;
+    size_t emb = 0, layers = 0, final_norm = 0, unemb = 0;  // offsets (floats)
+    size_t attn_norm(int l) const { return layers + (size_t)l * per_layer; }
+    size_t wq(int l) const { return attn_norm(l) + d_model; }
+    size_t wk(int l) const { return wq(l) + (size_t)d_model * d_model; }
+    size_t wv(int l) const { return wk(l) + (size_t)d_model * d_model; }
+    size_t wo(int l) const { return wv(l) + (size_t)d_model * d_model; }
+    size_t mlp_norm(int l) const { return wo(l) + (size_t)d_model * d_model; }
+    size_t w_in(int l) const { return mlp_norm(l) + d_model; }
+    size_t w_out(int l) const { return w_in(l) + (size_t)4 * d_model * d_model; }
+};
+
 namespace cx {
 
 // KvCache stream ordering and growth (capi.cu)
@@ -221,6 +241,9 @@ bool select64_launch(const GroupView& g, const Options& o, const double* attn, c
 // gather selected rows from a (values or keys) tensor with the group addressing.
 void gather_rows(const GroupView& g, const float* src, const int64_t* rows, int take, float* dst,
                  cudaStream_t s);
+// keys and values in one launch; destination group blocks dst_gstride floats apart
+void gather_rows2(const GroupView& g, const float* src0, const float* src1, const int64_t* rows, int take, float* dst0,
+                  float* dst1, int64_t dst_gstride, cudaStream_t s);
 
 // coverage_scores_points with a non-empty selection (one group).
 void coverage_selected(const GroupView& g, const int64_t* sel, int64_t n_sel, double* out,

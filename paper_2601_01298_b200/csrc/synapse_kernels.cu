@@ -589,13 +589,19 @@ __global__ void __launch_bounds__(512, 1) select_kernel(SelectParams p) {
 // ----------------------------------------------------------------------------
 // A5: landmark gather dst[g][s][:] = src[g][rows[g][s]][:]
 // ----------------------------------------------------------------------------
-__global__ void gather_rows_kernel(GroupView gv, const float* __restrict__ src, const int64_t* __restrict__ rows,
-                                   int take, float* __restrict__ dst) {
+// landmark gather (synapse.cpp:303-318 copy): dst[g][s] = src row rows[g][s] of group g, for
+// up to two sources (keys and values) in one launch (blockIdx.z); dst group blocks dst_gstride
+// floats apart (take * dim when dense; the decode layout [layer][kv head][k][d] otherwise)
+__global__ void gather_rows_kernel(GroupView gv, const float* __restrict__ src0, const float* __restrict__ src1,
+                                   const int64_t* __restrict__ rows, int take, float* __restrict__ dst0,
+                                   float* __restrict__ dst1, int64_t dst_gstride) {
     const int g = blockIdx.y;
     const int s = blockIdx.x;
+    const float* src = blockIdx.z ? src1 : src0;
+    float* dst = blockIdx.z ? dst1 : dst0;
     const int64_t r = rows[(int64_t)g * take + s];
     const float* in = src + g * gv.gstride + r * gv.rstride;
-    float* out = dst + ((int64_t)g * take + s) * gv.dim;
+    float* out = dst + (int64_t)g * dst_gstride + (int64_t)s * gv.dim;
     if ((gv.dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
         for (int c = threadIdx.x; c < gv.dim / 4; c += blockDim.x)
             reinterpret_cast<float4*>(out)[c] = __ldg(reinterpret_cast<const float4*>(in) + c);
@@ -907,8 +913,14 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
 
 void gather_rows(const GroupView& g, const float* src, const int64_t* rows, int take, float* dst,
                  cudaStream_t s) {
+    gather_rows2(g, src, nullptr, rows, take, dst, nullptr, (int64_t)take * g.dim, s);
+}
+
+void gather_rows2(const GroupView& g, const float* src0, const float* src1, const int64_t* rows, int take, float* dst0,
+                  float* dst1, int64_t dst_gstride, cudaStream_t s) {
     if (take <= 0 || g.G <= 0) return;
-    gather_rows_kernel<<<dim3((unsigned)take, (unsigned)g.G), 64, 0, s>>>(g, src, rows, take, dst);
+    gather_rows_kernel<<<dim3((unsigned)take, (unsigned)g.G, src1 ? 2u : 1u), 64, 0, s>>>(g, src0, src1, rows, take, dst0,
+                                                                                       dst1, dst_gstride);
     check_launch("gather_rows_kernel");
 }
 

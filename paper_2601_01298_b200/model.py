@@ -165,6 +165,15 @@ class KvCache:
     def values_dev(self) -> int:
         return int(lib.cx_kvcache_values_dev(self._h) or 0)
 
+    def clone(self) -> "KvCache":
+        """A deep copy (KvCache's copy constructor, model.hpp:67-113): rows, positions,
+        origins and the append protocol state."""
+        h = c_vp()
+        check(lib.cx_kvcache_clone(self._h, C.byref(h)), "KvCache clone")
+        c = KvCache.__new__(KvCache)
+        c._cfg, c._h = self._cfg, h.value
+        return c
+
     def capacity(self) -> int:
         return int(lib.cx_kvcache_capacity(self._h))
 
