@@ -502,115 +502,75 @@ def run_decode(args, dev, rank=0, world=1):
 
 def run_cfg5(args, dev, tokens=600, n_agents=100, inj_every=10, push_every=10, t_inj=16):
     """BASELINE configs[4]: River + 100 Stream agents, Referential Injection every
-    10 tokens, River and Stream work on priority CUDA streams.
+    10 tokens, River and Stream work on priority CUDA streams -- through the C-ABI
+    runtime (cx_cortex_*, csrc/cortex_runtime.cu; runtime.Cortex).
 
-    River lane (highest priority): every `inj_every` agent tokens, inject a
-    16-token thought block into the river's device KvCache (cx_inject_dev,
-    injector.cpp:70-94); every `push_every` tokens, if the previous push has
-    landed, re-compress the river's L=8192 context rows (48 (layer, KV-head)
-    groups, k=164) into the back synapse buffer -- the push (scheduler.cpp:
-    158-165).  Stream lane (medium priority): N agents x 24 layers decode one
-    token per step against the FRONT synapse (append + attend, decode_tc).  A
-    push is published to the agents when its CUDA event has completed (a
-    non-blocking query: SynapseBuffer::read_latest semantics, synapse.hpp:
-    115-135); the agent lane then waits on that event.  The host stays at most
-    `inj_every` tokens ahead of the agent lane, so "landed" is judged at device
-    time, not at launch time.
-    River forward_step / encode_thought (the projections) are out of scope
-    (SURVEY.md §8(f) row 1): the river work is its injections and pushes."""
+    River lane (highest priority, the calling host thread): per river token its
+    forward_step on the river KvCache (24 layers x d_model 128, random weights, L=8192
+    prefilled context rows); every 10 tokens a 16-token thought is encoded
+    (encode_thought: 16 forward_steps on a scratch cache at reserved virtual positions)
+    and injected; every 10 tokens, once the previous push is published, a push
+    compresses the context rows of all 48 (layer, KV head) groups (k=164) straight into
+    the back synapse buffer.  Stream lane (medium priority, a second host thread): each
+    agent step is 100 agents x 24 layers decoding one token against the front synapse,
+    one CUDA-graph replay.  Retention = the agents' rate while the river runs over
+    their rate alone (same runtime, no river tokens)."""
+    import numpy as np
     import torch
 
-    from paper_2601_01298_b200 import device as cxd
-    from paper_2601_01298_b200.injector import inject_dev
+    from paper_2601_01298_b200 import runtime as rt
     from paper_2601_01298_b200.model import KvCache, ModelConfig
-    river_lane, agent_lane = cxd.lane_stream("river"), cxd.lane_stream("stream")
-    dm = N_KV * D
-    n_inj = tokens // inj_every + 1
-    cfg = ModelConfig(n_layers=N_LAYERS, n_heads=N_KV, d_model=dm, d_k=D, max_positions=L + 4096 + n_inj * t_inj)
-    river = KvCache(cfg, capacity=L + n_inj * t_inj + 16)  # pre-sized: views stay valid
+    dm, qpg = N_KV * D, N_Q // N_KV
+    calib = 40
+    n_inj = -(-(tokens + calib) // inj_every)
+    vbase = L + tokens + calib + 64
+    cfg = ModelConfig(n_layers=N_LAYERS, n_heads=N_KV, d_model=dm, d_k=D, vocab_size=256,
+                      max_positions=vbase + (n_inj + 4) * t_inj)
+    w = rt.Weights(cfg, rt.random_flat_weights(cfg, 7))
+    river = KvCache(cfg, capacity=L + tokens + calib + (n_inj + 4) * t_inj)  # pre-sized: no growth mid-run
     gen = torch.Generator(device=dev).manual_seed(5)
-    qpg = N_Q // N_KV
-    with torch.cuda.stream(river_lane):
-        pre_k = torch.randn(N_LAYERS, L, dm, device=dev, generator=gen)
-        pre_v = torch.randn(N_LAYERS, L, dm, device=dev, generator=gen)
-        river.append_context_dev(pre_k.data_ptr(), pre_v.data_ptr(), 0, L, river_lane.cuda_stream)
-        th_k = torch.randn(N_LAYERS, t_inj, dm, device=dev, generator=gen)
-        th_v = torch.randn(N_LAYERS, t_inj, dm, device=dev, generator=gen)
-        rq = [torch.randn(N_LAYERS, qpg, D, device=dev, generator=gen) for _ in range(N_KV)]
-        heads = [(cxd.kvcache_head_view(river, h, L), cxd.kvcache_head_view(river, h, L, values=True))
-                 for h in range(N_KV)]
-        syn = torch.empty(2, 2, N_LAYERS, N_KV, K, D, device=dev)  # [buffer][K|V][layer][kv][k][d]
-        outs = [(torch.empty(N_LAYERS, K, dtype=torch.int64, device=dev),
-                 torch.empty(N_LAYERS, K, dtype=torch.float64, device=dev),
-                 torch.empty(N_LAYERS, K, D, device=dev), torch.empty(N_LAYERS, K, D, device=dev))
-                for _ in range(N_KV)]
-
-    def push(buf):  # river lane: one synapse compression of all 48 groups into syn[buf]
-        for h in range(N_KV):
-            kh, vh = heads[h]
-            cxd.compress_grouped(kh, vh, rq[h], K, LAM, out=outs[h])
-            syn[buf, 0, :, h].copy_(outs[h][2])
-            syn[buf, 1, :, h].copy_(outs[h][3])
-
-    with torch.cuda.stream(river_lane):
-        push(0)
+    pre_k = torch.randn(N_LAYERS, L, dm, device=dev, generator=gen)
+    pre_v = torch.randn(N_LAYERS, L, dm, device=dev, generator=gen)
     torch.cuda.synchronize()
-    gen2 = torch.Generator(device=dev).manual_seed(6)
-    tk = torch.randn(n_agents, N_LAYERS, N_KV, T_PRIV + 1, D, device=dev, generator=gen2)
-    tv = torch.randn_like(tk)
-    tl = torch.full((n_agents,), T_PRIV, dtype=torch.int32, device=dev)
-    nk = torch.randn(n_agents, N_LAYERS, N_KV, D, device=dev, generator=gen2)
-    nv = torch.randn_like(nk)
-    q = torch.randn(n_agents, N_LAYERS, N_Q, D, device=dev, generator=gen2)
-    o = torch.empty_like(q)
-    front, inflight, pushes, injections = 0, None, 0, 0
-    push_ms, vbase = [], L + 1024
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev0.record(agent_lane)
-    river_lane.wait_event(ev0)
-    tok_ev = []
-    for t in range(tokens):
-        if t >= inj_every:
-            tok_ev[t - inj_every].synchronize()
-        if inflight is not None and inflight[0].query():  # the push landed: publish it
-            agent_lane.wait_event(inflight[0])
-            front = inflight[1]
-            push_ms.append(inflight[2].elapsed_time(inflight[0]))
-            pushes += 1
-            inflight = None
-        if t % inj_every == 0:
-            with torch.cuda.stream(river_lane):
-                inject_dev(river, th_k.data_ptr(), th_v.data_ptr(), vbase + injections * t_inj, t_inj, N_LAYERS, dm,
-                           injections, t, river_lane.cuda_stream)
-            injections += 1
-        if t % push_every == 0 and inflight is None:
-            with torch.cuda.stream(river_lane):
-                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s0.record(river_lane)
-                push(1 - front)
-                s1.record(river_lane)
-            inflight = (s1, 1 - front, s0)
-        with torch.cuda.stream(agent_lane):
-            cxd.decode_step(syn[front, 0], syn[front, 1], tk, tv, tl, q, o, nk, nv)
-        ev = torch.cuda.Event()
-        ev.record(agent_lane)
-        tok_ev.append(ev)
-    e_ag, e_rv = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_ag.record(agent_lane)
-    e_rv.record(river_lane)
+    river.append_context_dev(pre_k.data_ptr(), pre_v.data_ptr(), 0, L)
     torch.cuda.synchronize()
-    if inflight is not None:
-        push_ms.append(inflight[2].elapsed_time(inflight[0]))
-        pushes += 1
-    ag_ms = ev0.elapsed_time(e_ag)
-    return {"workload": f"cfg5 (BASELINE configs[4]): river KvCache L={L} context rows, {n_agents} stream agents x "
-                        f"{tokens} tokens, injection of {t_inj} tokens every {inj_every}, synapse push every "
-                        f"{push_every} tokens when the previous one has landed",
-            "agent_steps_per_s": n_agents * tokens / (ag_ms * 1e-3), "agent_ms": ag_ms,
-            "river_ms": ev0.elapsed_time(e_rv), "pushes": pushes, "injections": injections,
-            "push_ms_mean": statistics.mean(push_ms) if push_ms else None,
-            "lanes": {"river_priority": river_lane.cx_priority, "stream_priority": agent_lane.cx_priority},
-            "river_entries": river.size(), "river_context_count": river.context_count()}
+    del pre_k, pre_v
+    ag = dict(tail_keys=torch.randn(n_agents, N_LAYERS, N_KV, T_PRIV + 1, D, device=dev, generator=gen),
+              tail_values=torch.randn(n_agents, N_LAYERS, N_KV, T_PRIV + 1, D, device=dev, generator=gen),
+              tail_len=torch.full((n_agents,), T_PRIV, dtype=torch.int32, device=dev),
+              new_keys=torch.randn(n_agents, N_LAYERS, N_KV, D, device=dev, generator=gen),
+              new_values=torch.randn(n_agents, N_LAYERS, N_KV, D, device=dev, generator=gen),
+              q=torch.randn(n_agents, N_LAYERS, N_Q, D, device=dev, generator=gen),
+              out=torch.empty(n_agents, N_LAYERS, N_Q, D, device=dev),
+              river_queries=torch.randn(N_KV, N_LAYERS, qpg, D, device=dev, generator=gen))
+    cx = rt.Cortex(w, river, k=K, lam=LAM, push_every=push_every, inject_every=inj_every, thought_tokens=t_inj,
+                   virtual_base=vbase, max_context=L + tokens + calib + 16, push_mode="groups", **ag)
+    rng = np.random.default_rng(9)
+    # agents alone (the stand-alone rate), the river alone (its token time), then both
+    alone, _ = cx.run([], [], 2000)
+    ag_alone_ms = alone["agent_ms"] / 2000
+    r_tok = rng.integers(0, 256, calib).tolist()
+    river_alone, _ = cx.run(r_tok, rng.integers(0, 256, -(-calib // inj_every) * t_inj).tolist(), 0)
+    river_tok_ms = river_alone["river_ms"] / calib
+    n_steps = max(200, int(tokens * river_tok_ms / ag_alone_ms))  # agents span the river's run
+    r_tok = rng.integers(0, 256, tokens).tolist()
+    th = rng.integers(0, 256, -(-tokens // inj_every) * t_inj).tolist()
+    st, vers = cx.run(r_tok, th, n_steps)
+    cx.close()
+    rate = n_agents * n_steps / (st["agent_ms"] * 1e-3)
+    rate_alone = n_agents / (ag_alone_ms * 1e-3)
+    return {"workload": f"cfg5 (BASELINE configs[4]): river model 24 layers x d_model {dm} (random weights), "
+                        f"L={L} prefilled context rows, {tokens} river tokens (forward_step each); a {t_inj}-token "
+                        f"thought encoded + injected every {inj_every} river tokens; a push of all {G} (layer, KV "
+                        f"head) groups (k={K}) every {push_every} tokens once the previous one is published; "
+                        f"concurrently {n_steps} agent steps of {n_agents} agents x {N_LAYERS} layers",
+            "api": "cx_cortex_create / cx_cortex_run (runtime.Cortex)",
+            "agent_steps_per_s": rate, "agent_steps_per_s_alone": rate_alone, "agent_rate_retention": rate / rate_alone,
+            "agent_ms": st["agent_ms"], "river_ms": st["river_ms"],
+            "river_tokens_per_s": tokens / (st["river_ms"] * 1e-3), "river_tokens_per_s_alone": 1000.0 / river_tok_ms,
+            "pushes": st["pushes"], "push_ms_mean": st["push_ms_mean"], "injections": st["injections"],
+            "versions_read": int(len(set(vers.tolist()))), "river_entries": river.size(),
+            "river_context_count": river.context_count()}
 
 
 def run_cfg4(args, dev, rank=0, world=1, comm=None, steps=3):

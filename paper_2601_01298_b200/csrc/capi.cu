@@ -185,6 +185,7 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
         cudaStreamSynchronize(c->stream);
         cudaStreamSynchronize(c->side);
         if (c->arena.base) cudaFree(c->arena.base);
+        if (c->fw_counters) cudaFree(c->fw_counters);
         if (c->d_flag) cudaFree(c->d_flag);
         if (c->gaps) cudaFree(c->gaps);
         cudaEventDestroy(c->ev_fork);

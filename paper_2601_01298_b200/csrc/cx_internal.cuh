@@ -132,6 +132,8 @@ struct cx_ctx {
     double* gaps = nullptr;         // decision-gap monitor: [gaps_n] of the last selection (device)
     int gaps_cap = 0, gaps_n = 0;
     int num_sms = 0;
+    unsigned* fw_counters = nullptr;  // forward_step attention: per (agent, head) chunk counters (kept zero)
+    int fw_counters_n = 0;
     cx::Options opt;                // cx_ctx_set_option
     std::mutex mu;
 };

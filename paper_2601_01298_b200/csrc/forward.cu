@@ -25,7 +25,12 @@
 namespace cx {
 namespace {
 
-constexpr int FW_CHUNK = 128;  // attention entries per CTA
+constexpr int FW_CHUNK = 128;      // attention entries per CTA
+#ifndef CX_FW_MAX_B
+#define CX_FW_MAX_B 32
+#endif
+constexpr int FW_MAX_B = CX_FW_MAX_B;  // agents per launch (kernel-parameter batch; larger batches are split)
+constexpr int FW_MAX_CHUNKS = 1024;  // attention chunks per (agent, head): 131072 rows
 
 // per agent: its cache arrays and the row the new entry goes to
 struct FwAgent {
@@ -36,6 +41,12 @@ struct FwAgent {
     int64_t position;
     int token;
 };
+// the batch travels as a kernel parameter: no host->device copy, so a forward step
+// never synchronizes its stream (a pageable cudaMemcpyAsync would)
+struct FwBatch {
+    int B;
+    FwAgent a[FW_MAX_B];
+};
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -43,10 +54,18 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-__global__ void fw_embed(const FwAgent* ag, int B, const float* emb, int d, float* x) {
+__global__ void fw_embed(const __grid_constant__ FwBatch P, const float* emb, int d, float* x) {
     const int b = blockIdx.x;
-    if (b >= B) return;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) x[(size_t)b * d + i] = emb[(size_t)ag[b].token * d + i];
+    if (b >= P.B) return;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) x[(size_t)b * d + i] = emb[(size_t)P.a[b].token * d + i];
+}
+
+// 1 / sqrt(mean(x^2) + eps) of one agent's row, by a full warp (kernels.cpp:28-38)
+__device__ __forceinline__ double warp_rms_inv(const float* xb, int d, double eps) {
+    double ssq = 0.0;
+    for (int i = threadIdx.x & 31; i < d; i += 32) ssq += (double)xb[i] * (double)xb[i];
+    ssq = warp_sum(ssq);
+    return 1.0 / sqrt(ssq / (double)d + eps);
 }
 
 // out[b] = x[b] * (1 / sqrt(mean(x^2) + eps)) * gain, fp64 (kernels.cpp:28-38); one warp per agent
@@ -54,32 +73,34 @@ __global__ void fw_rmsnorm(const float* x, const float* gain, int d, int B, floa
     const int b = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
     if (b >= B) return;
     const float* xb = x + (size_t)b * d;
-    double ssq = 0.0;
-    for (int i = lane; i < d; i += 32) ssq += (double)xb[i] * (double)xb[i];
-    ssq = warp_sum(ssq);
-    const double inv = 1.0 / sqrt(ssq / (double)d + eps);
+    const double inv = warp_rms_inv(xb, d, eps);
     for (int i = lane; i < d; i += 32) out[(size_t)b * d + i] = (float)((double)xb[i] * inv * (double)gain[i]);
 }
 
 // Y[b][r] (op) = sum_c W[r][c] x[b][c] in fp64, rounded once (kernels.cpp:12-26); a warp per
 // (b, r).  mode 0: store; 1: store relu; 2: Y += result (the residual add, fp32 like
-// kernels.cpp:40-43).  nmat matrices at W + m * mat_stride, outputs at Y + m * y_stride.
-__global__ void fw_matvec(const float* W, size_t mat_stride, int nmat, int n_out, int n_in, const float* X, int B,
-                          float* Y, size_t y_stride, int mode) {
+// kernels.cpp:40-43).  gain != NULL: x is rmsnorm(x) * gain first (fused; the normed value is
+// rounded to fp32 exactly as the separate rmsnorm's output).
+__global__ void fw_matvec(const float* W, int n_out, int n_in, const float* X, int B, float* Y, int mode,
+                          const float* gain, double eps) {
     const int wpb = blockDim.x / 32;
     const long long item = (long long)blockIdx.x * wpb + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
-    if (item >= (long long)nmat * n_out * B) return;
-    const int b = (int)(item % B);
-    const long long mr = item / B;
-    const int r = (int)(mr % n_out), m = (int)(mr / n_out);
-    const float* row = W + m * mat_stride + (size_t)r * n_in;
+    if (item >= (long long)n_out * B) return;
+    const int b = (int)(item % B), r = (int)(item / B);
+    const float* row = W + (size_t)r * n_in;
     const float* xb = X + (size_t)b * n_in;
     double acc = 0.0;
-    for (int c = lane; c < n_in; c += 32) acc += (double)row[c] * (double)xb[c];
+    if (gain) {
+        const double inv = warp_rms_inv(xb, n_in, eps);
+        for (int c = lane; c < n_in; c += 32)
+            acc += (double)row[c] * (double)(float)((double)xb[c] * inv * (double)gain[c]);
+    } else {
+        for (int c = lane; c < n_in; c += 32) acc += (double)row[c] * (double)xb[c];
+    }
     acc = warp_sum(acc);
     if (lane == 0) {
-        float* y = Y + m * y_stride + (size_t)b * n_out + r;
+        float* y = Y + (size_t)b * n_out + r;
         const float v = (float)acc;
         if (mode == 0) *y = v;
         else if (mode == 1) *y = fmaxf(v, 0.0f);
@@ -87,70 +108,107 @@ __global__ void fw_matvec(const float* W, size_t mat_stride, int nmat, int n_out
     }
 }
 
-// RoPE on q and k (each head's pairs (2j, 2j+1), kernels.cpp:49-62), then the new entry's
-// K / V rows into the agent's cache at layer l (model.cpp:142-152 write_layer)
-__global__ void fw_rope_append(FwAgent* ag, int B, int l, int n_heads, int d_k, double base, float* q, const float* k,
-                               const float* v, float* final_q) {
-    const int b = blockIdx.x;
-    if (b >= B) return;
+// q, k, v = W{q,k,v} rmsnorm(x) for one rotation pair (2e, 2e+1) per warp, then RoPE on q and
+// k (kernels.cpp:49-62) and the new entry's K / V into the agent's cache at layer l
+// (model.cpp:142-152 write_layer); q (rotated) -> qbuf, and final_q at the last layer.
+__global__ void fw_qkv_rope(const __grid_constant__ FwBatch P, int l, const float* Wq, int n_heads, int d_k,
+                            double base, const float* x, const float* gain, double eps, float* qbuf, float* final_q) {
     const int d = n_heads * d_k;
-    const FwAgent a = ag[b];
-    float* kdst = a.keys + ((size_t)l * a.cap + a.row) * d;
-    float* vdst = a.values + ((size_t)l * a.cap + a.row) * d;
-    for (int e = threadIdx.x; e < d / 2; e += blockDim.x) {
-        const int h = e / (d_k / 2), j = e % (d_k / 2);
-        const int i0 = h * d_k + 2 * j;
+    const int wpb = blockDim.x / 32, lane = threadIdx.x & 31;
+    const long long item = (long long)blockIdx.x * wpb + threadIdx.x / 32;
+    if (item >= (long long)(d / 2) * P.B) return;
+    const int b = (int)(item % P.B), e = (int)(item / P.B);
+    const int i0 = 2 * e;
+    const float* xb = x + (size_t)b * d;
+    const double inv = warp_rms_inv(xb, d, eps);
+    const size_t dd = (size_t)d * d;
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (int c = lane; c < d; c += 32) {
+        const double xn = (double)(float)((double)xb[c] * inv * (double)gain[c]);
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+            acc[2 * m] += (double)Wq[m * dd + (size_t)i0 * d + c] * xn;
+            acc[2 * m + 1] += (double)Wq[m * dd + (size_t)(i0 + 1) * d + c] * xn;
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 6; ++m) acc[m] = warp_sum(acc[m]);
+    if (lane == 0) {
+        const FwAgent& a = P.a[b];
+        const int j = e % (d_k / 2);
         const double freq = pow(base, -2.0 * j / (double)d_k);
         const double ang = (double)a.position * freq;
-        const double c = cos(ang), s = sin(ang);
+        const double cs = cos(ang), sn = sin(ang);
+        const double q0 = (float)acc[0], q1 = (float)acc[1], k0 = (float)acc[2], k1 = (float)acc[3];
+        const float rq0 = (float)(cs * q0 - sn * q1), rq1 = (float)(sn * q0 + cs * q1);
         const size_t o = (size_t)b * d + i0;
-        const double q0 = q[o], q1 = q[o + 1], k0 = k[o], k1 = k[o + 1];
-        const float rq0 = (float)(c * q0 - s * q1), rq1 = (float)(s * q0 + c * q1);
-        q[o] = rq0;
-        q[o + 1] = rq1;
-        kdst[i0] = (float)(c * k0 - s * k1);
-        kdst[i0 + 1] = (float)(s * k0 + c * k1);
+        qbuf[o] = rq0;
+        qbuf[o + 1] = rq1;
         if (final_q) {
             final_q[o] = rq0;
             final_q[o + 1] = rq1;
         }
+        float* kdst = a.keys + ((size_t)l * a.cap + a.row) * d;
+        float* vdst = a.values + ((size_t)l * a.cap + a.row) * d;
+        kdst[i0] = (float)(cs * k0 - sn * k1);
+        kdst[i0 + 1] = (float)(sn * k0 + cs * k1);
+        vdst[i0] = (float)acc[4];
+        vdst[i0 + 1] = (float)acc[5];
     }
-    for (int i = threadIdx.x; i < d; i += blockDim.x) vdst[i] = v[(size_t)b * d + i];
 }
 
-// attention partials: block (chunk, head, agent) over entries [chunk*128, +128) of rows
-// [0, row + 1): m = max score, l = sum exp(s - m), acc = sum exp(s - m) v  (fp64)
-__global__ void fw_attend_partial(const FwAgent* ag, int l, int n_heads, int d_k, const float* q, double* part,
-                                  int n_chunks) {
-    const int ch = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-    const FwAgent a = ag[b];
-    const int64_t n = a.row + 1;
-    const int64_t e0 = (int64_t)ch * FW_CHUNK;
-    const int d = n_heads * d_k;
-    double* out = part + (((size_t)b * n_heads + h) * n_chunks + ch) * (2 + d_k);
-    if (e0 >= n) {
-        if (threadIdx.x == 0) {
-            out[0] = -INFINITY;
-            out[1] = 0.0;
+// rows [e0, e0 + ne) x columns [0, d_k) of a head's K or V -> tile (coalesced; float4 when aligned)
+__device__ __forceinline__ void stage_tile(float (*tile)[65], const float* src, int64_t e0, int ne, int d, int d_k) {
+    if ((d_k & 3) == 0) {
+        const int q4 = d_k / 4;
+        for (int i = threadIdx.x; i < ne * q4; i += blockDim.x) {
+            const int r = i / q4, c = (i % q4) * 4;
+            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (size_t)(e0 + r) * d + c));
+            tile[r][c] = v.x;
+            tile[r][c + 1] = v.y;
+            tile[r][c + 2] = v.z;
+            tile[r][c + 3] = v.w;
         }
-        for (int c = threadIdx.x; c < d_k; c += blockDim.x) out[2 + c] = 0.0;
-        return;
+    } else {
+        for (int i = threadIdx.x; i < ne * d_k; i += blockDim.x) {
+            const int r = i / d_k, c = i % d_k;
+            tile[r][c] = __ldg(src + (size_t)(e0 + r) * d + c);
+        }
     }
-    __shared__ double w[FW_CHUNK];
-    __shared__ double red[FW_CHUNK / 32];
+}
+
+// attention (kernels.cpp:103-142) of one (chunk of 128 entries, head, agent) per CTA over rows
+// [0, row + 1): K / V tiles staged through shared memory with coalesced loads; the chunk's
+// partial (max m, sum l of e^{s-m}, sum e^{s-m} v, all fp64) goes to `part`, and the last CTA
+// of the (agent, head) to finish combines every chunk (no second launch).
+__global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch P, int l, int n_heads, int d_k,
+                                                 const float* q, double* part, unsigned* counters, int n_chunks,
+                                                 float* att) {
+    const int ch = blockIdx.x, h = blockIdx.y, b = blockIdx.z, t = threadIdx.x;
+    const FwAgent& a = P.a[b];
+    const int64_t n = a.row + 1;
+    const int my_chunks = (int)((n + FW_CHUNK - 1) / FW_CHUNK);
+    if (ch >= my_chunks) return;
+    const int d = n_heads * d_k;
+    const int64_t e0 = (int64_t)ch * FW_CHUNK;
+    const int ne = (int)min((int64_t)FW_CHUNK, n - e0);
+    __shared__ float tile[FW_CHUNK][65];
     __shared__ double qs[64];
+    __shared__ double w[FW_CHUNK];
+    __shared__ double red[8];
+    __shared__ double pacc[4][64];
+    __shared__ double sc[FW_MAX_CHUNKS];
+    __shared__ int last;
     const float* kb = a.keys + (size_t)l * a.cap * d + (size_t)h * d_k;
     const float* vb = a.values + (size_t)l * a.cap * d + (size_t)h * d_k;
-    for (int c = threadIdx.x; c < d_k; c += blockDim.x) qs[c] = (double)q[(size_t)b * d + h * d_k + c];
+    if (t < d_k) qs[t] = (double)q[(size_t)b * d + h * d_k + t];
+    stage_tile(tile, kb, e0, ne, d, d_k);
     __syncthreads();
-    const int t = threadIdx.x;
-    const int64_t e = e0 + t;
     const double inv = 1.0 / sqrt((double)d_k);
     double s = -INFINITY;
-    if (e < n) {
-        const float* kr = kb + (size_t)e * d;
-        double dot = 0.0;
-        for (int c = 0; c < d_k; ++c) dot += qs[c] * (double)kr[c];
+    if (t < ne) {
+        double dot = 0.0;  // the reference's order: c = 0 .. d_k - 1
+        for (int c = 0; c < d_k; ++c) dot += qs[c] * (double)tile[t][c];
         s = dot * inv;
     }
     double mx = s;
@@ -160,47 +218,72 @@ __global__ void fw_attend_partial(const FwAgent* ag, int l, int n_heads, int d_k
     __syncthreads();
     mx = red[0];
     for (int i = 1; i < FW_CHUNK / 32; ++i) mx = fmax(mx, red[i]);
-    const double p = e < n ? exp(s - mx) : 0.0;
-    w[t] = p;
+    const double p = t < ne ? exp(s - mx) : 0.0;
+    if (t < FW_CHUNK) w[t] = p;
+    __syncthreads();  // every thread has read red[] and the K tile
+    const double ps = warp_sum(p);
+    if ((t & 31) == 0) red[t >> 5] = ps;
+    stage_tile(tile, vb, e0, ne, d, d_k);
     __syncthreads();
-    double sum = warp_sum(p);
+    double* out = part + (((size_t)b * n_heads + h) * n_chunks + ch) * (2 + d_k);
+    {
+        const int c = t % 64, qtr = t / 64;  // 4 row quarters x 64 columns
+        if (c < d_k) {
+            double acc = 0.0;
+            const int r1 = min(ne, (qtr + 1) * (FW_CHUNK / 4));
+            for (int r = qtr * (FW_CHUNK / 4); r < r1; ++r) acc += w[r] * (double)tile[r][c];
+            pacc[qtr][c] = acc;
+        }
+    }
     __syncthreads();
-    if ((t & 31) == 0) red[t >> 5] = sum;
-    __syncthreads();
+    if (t < d_k) out[2 + t] = ((pacc[0][t] + pacc[1][t]) + pacc[2][t]) + pacc[3][t];
     if (t == 0) {
         double acc = 0.0;
         for (int i = 0; i < FW_CHUNK / 32; ++i) acc += red[i];
         out[0] = mx;
         out[1] = acc;
     }
-    const int64_t ne = min((int64_t)FW_CHUNK, n - e0);
-    for (int c = t; c < d_k; c += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t j = 0; j < ne; ++j) acc += w[j] * (double)vb[(size_t)(e0 + j) * d + c];
-        out[2 + c] = acc;
-    }
-}
-
-// out[b][h*d_k + c] = (sum_ch acc e^{m_ch - M}) / (sum_ch l e^{m_ch - M}), rounded to fp32
-__global__ void fw_attend_combine(int B, int n_heads, int d_k, const double* part, int n_chunks, float* att) {
-    const int b = blockIdx.x, h = blockIdx.y;
-    if (b >= B) return;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) last = atomicAdd(&counters[b * n_heads + h], 1u) == (unsigned)(my_chunks - 1);
+    __syncthreads();
+    if (!last) return;
+    // the combine: out = (sum_ch acc e^{m_ch - M}) / (sum_ch l e^{m_ch - M}), rounded to fp32
+    __threadfence();
     const double* pp = part + ((size_t)b * n_heads + h) * n_chunks * (2 + d_k);
     double M = -INFINITY;
-    for (int ch = 0; ch < n_chunks; ++ch) M = fmax(M, pp[(size_t)ch * (2 + d_k)]);
-    double L = 0.0;
-    for (int ch = 0; ch < n_chunks; ++ch) {
-        const double m = pp[(size_t)ch * (2 + d_k)];
-        if (m > -INFINITY) L += pp[(size_t)ch * (2 + d_k) + 1] * exp(m - M);
+    for (int i = t; i < my_chunks; i += blockDim.x) M = fmax(M, __ldcg(pp + (size_t)i * (2 + d_k)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+    __syncthreads();
+    if ((t & 31) == 0) red[t >> 5] = M;
+    __syncthreads();
+    M = red[0];
+    for (int i = 1; i < 8; ++i) M = fmax(M, red[i]);
+    double Ls = 0.0;
+    for (int i = t; i < my_chunks; i += blockDim.x) {
+        const double f = exp(__ldcg(pp + (size_t)i * (2 + d_k)) - M);
+        sc[i] = f;
+        Ls += __ldcg(pp + (size_t)i * (2 + d_k) + 1) * f;
     }
-    for (int c = threadIdx.x; c < d_k; c += blockDim.x) {
-        double acc = 0.0;
-        for (int ch = 0; ch < n_chunks; ++ch) {
-            const double m = pp[(size_t)ch * (2 + d_k)];
-            if (m > -INFINITY) acc += pp[(size_t)ch * (2 + d_k) + 2 + c] * exp(m - M);
+    Ls = warp_sum(Ls);
+    __syncthreads();
+    if ((t & 31) == 0) red[t >> 5] = Ls;
+    __syncthreads();
+    Ls = 0.0;
+    for (int i = 0; i < 8; ++i) Ls += red[i];
+    {
+        const int c = t % 64, qtr = t / 64;
+        if (c < d_k) {
+            double acc = 0.0;
+            for (int i = qtr; i < my_chunks; i += 4) acc += __ldcg(pp + (size_t)i * (2 + d_k) + 2 + c) * sc[i];
+            pacc[qtr][c] = acc;
         }
-        att[(size_t)b * n_heads * d_k + h * d_k + c] = (float)(acc / L);
     }
+    __syncthreads();
+    if (t < d_k)
+        att[(size_t)b * d + h * d_k + t] = (float)((((pacc[0][t] + pacc[1][t]) + pacc[2][t]) + pacc[3][t]) / Ls);
+    if (t == 0) counters[b * n_heads + h] = 0u;  // ready for the next launch
 }
 
 __global__ void fw_elementwise(float* x, const float* y, int64_t n, int op) {  // 0: x += y, 1: relu
@@ -219,12 +302,11 @@ __global__ void fw_rope_vec(float* v, int n, int64_t position, double base) {  /
     }
 }
 
-void matvec_launch(const float* W, size_t mat_stride, int nmat, int n_out, int n_in, const float* X, int B, float* Y,
-                   size_t y_stride, int mode, cudaStream_t s) {
-    const long long items = (long long)nmat * n_out * B;
+void matvec_launch(const float* W, int n_out, int n_in, const float* X, int B, float* Y, int mode, cudaStream_t s,
+                   const float* gain = nullptr, double eps = 1e-5) {
+    const long long items = (long long)n_out * B;
     const int wpb = 8;
-    fw_matvec<<<(unsigned)((items + wpb - 1) / wpb), 32 * wpb, 0, s>>>(W, mat_stride, nmat, n_out, n_in, X, B, Y,
-                                                                        y_stride, mode);
+    fw_matvec<<<(unsigned)((items + wpb - 1) / wpb), 32 * wpb, 0, s>>>(W, n_out, n_in, X, B, Y, mode, gain, eps);
     check_launch("fw_matvec");
 }
 
@@ -274,6 +356,84 @@ extern "C" cx_status cx_weights_destroy(cx_weights* w) {
     });
 }
 
+namespace cx {
+namespace {
+// one launch sequence for nb <= FW_MAX_B agents (checks already done)
+void forward_batch(cx_ctx* c, const cx_weights* w, int nb, cx_kvcache* const* caches, const int* tokens,
+                   const int64_t* positions, float* logits, float* hidden, float* final_query, cudaStream_t s) {
+    const int d = w->d_model, dff = 4 * d, L = w->n_layers;
+    FwBatch P{};
+    P.B = nb;
+    int64_t max_rows = 1;
+    for (int b = 0; b < nb; ++b) {
+        cx_kvcache* kc = caches[b];
+        const int64_t row = (int64_t)kc->positions.size();
+        kv_grow(kc, row + 1);
+        kv_before(kc, s);
+        P.a[b] = FwAgent{kc->keys, kc->values, kc->capacity, row, positions[b], tokens[b]};
+        max_rows = std::max(max_rows, row + 1);
+    }
+    const int n_chunks = (int)((max_rows + FW_CHUNK - 1) / FW_CHUNK);
+    if (n_chunks > FW_MAX_CHUNKS) fail(CX_CAPACITY_ERROR, "forward_step: cache beyond 131072 entries");
+    const int n_cnt = nb * w->n_heads;
+    if (c->fw_counters_n < n_cnt) {  // zeroed once; every attention launch leaves them zero
+        if (c->fw_counters) CX_CUDA(cudaFree(c->fw_counters));
+        c->fw_counters = nullptr;
+        c->fw_counters_n = 0;
+        CX_CUDA(cudaMalloc(&c->fw_counters, sizeof(unsigned) * FW_MAX_B * 64));
+        CX_CUDA(cudaMemset(c->fw_counters, 0, sizeof(unsigned) * FW_MAX_B * 64));
+        c->fw_counters_n = FW_MAX_B * 64;
+        if (n_cnt > c->fw_counters_n) fail(CX_CONFIG_ERROR, "forward_step: more than 64 heads");
+    }
+    ArenaPlan pl;
+    pl.take<float>((size_t)nb * d);          // x
+    pl.take<float>((size_t)nb * d);          // q (rotated)
+    pl.take<float>((size_t)nb * d);          // att
+    pl.take<float>((size_t)nb * d);          // hidden scratch
+    pl.take<float>((size_t)nb * dff);        // ff
+    pl.take<double>((size_t)nb * w->n_heads * n_chunks * (2 + w->d_k));
+    c->arena.reserve(pl.used);
+    c->arena.reset();
+    float* x = c->arena.take<float>((size_t)nb * d);
+    float* qb = c->arena.take<float>((size_t)nb * d);
+    float* att = c->arena.take<float>((size_t)nb * d);
+    float* hs = c->arena.take<float>((size_t)nb * d);
+    float* ff = c->arena.take<float>((size_t)nb * dff);
+    double* part = c->arena.take<double>((size_t)nb * w->n_heads * n_chunks * (2 + w->d_k));
+    const float* W = w->buf;
+    fw_embed<<<nb, 128, 0, s>>>(P, W + w->emb, d, x);
+    check_launch("fw_embed");
+    const long long pairs = (long long)(d / 2) * nb;
+    for (int l = 0; l < L; ++l) {
+        // rmsnorm + q/k/v + RoPE + the cache append, one launch
+        fw_qkv_rope<<<(unsigned)((pairs + 7) / 8), 256, 0, s>>>(P, l, W + w->wq(l), w->n_heads, w->d_k, w->rope_base,
+                                                                 x, W + w->attn_norm(l), 1e-5, qb,
+                                                                 l == L - 1 ? final_query : nullptr);
+        check_launch("fw_qkv_rope");
+        fw_attend<<<dim3((unsigned)n_chunks, (unsigned)w->n_heads, (unsigned)nb), 256, 0, s>>>(
+            P, l, w->n_heads, w->d_k, qb, part, c->fw_counters, n_chunks, att);
+        check_launch("fw_attend");
+        matvec_launch(W + w->wo(l), d, d, att, nb, x, 2, s);                           // x += Wo att
+        matvec_launch(W + w->w_in(l), dff, d, x, nb, ff, 1, s, W + w->mlp_norm(l));  // relu(W_in rmsnorm(x))
+        matvec_launch(W + w->w_out(l), d, dff, ff, nb, x, 2, s);                       // x += W_out ff
+    }
+    float* hid = hidden ? hidden : hs;
+    fw_rmsnorm<<<(unsigned)((nb + 7) / 8), 256, 0, s>>>(x, W + w->final_norm, d, nb, hid, 1e-5);
+    check_launch("fw_rmsnorm");
+    if (logits) matvec_launch(W + w->unemb, w->vocab, d, hid, nb, logits, 0, s);
+    // the entry is complete at every layer (end_entry)
+    for (int b = 0; b < nb; ++b) {
+        cx_kvcache* kc = caches[b];
+        kv_after(kc, s);
+        kc->positions.push_back(positions[b]);
+        kc->origins.push_back((uint8_t)CX_ORIGIN_CONTEXT);
+        kc->last_context_position = positions[b];
+        kc->context_count += 1;
+    }
+}
+}  // namespace
+}  // namespace cx
+
 // forward_step (model.cpp:175-235) for n_agents agents, agent i on caches[i].
 extern "C" cx_status cx_forward_step_dev(cx_ctx* c, const cx_weights* w, int n_agents, cx_kvcache* const* caches,
                                          const int* tokens, const int64_t* positions, float* logits, float* hidden,
@@ -303,72 +463,13 @@ extern "C" cx_status cx_forward_step_dev(cx_ctx* c, const cx_weights* w, int n_a
                 if (caches[b2] == kc) fail(CX_INVALID_ARGUMENT, "forward_step: a cache appears twice in the batch");
         }
         cudaStream_t s = (cudaStream_t)stream;
-        std::vector<FwAgent> ag((size_t)B);
-        int64_t max_rows = 1;
-        for (int b = 0; b < B; ++b) {
-            cx_kvcache* kc = caches[b];
-            const int64_t row = (int64_t)kc->positions.size();
-            kv_grow(kc, row + 1);
-            kv_before(kc, s);
-            ag[(size_t)b] = FwAgent{kc->keys, kc->values, kc->capacity, row, positions[b], tokens[b]};
-            max_rows = std::max(max_rows, row + 1);
+        for (int b0 = 0; b0 < B; b0 += FW_MAX_B) {
+            const int nb = std::min(FW_MAX_B, B - b0);
+            forward_batch(c, w, nb, caches + b0, tokens + b0, positions + b0,
+                          logits ? logits + (size_t)b0 * w->vocab : nullptr, hidden ? hidden + (size_t)b0 * d : nullptr,
+                          final_query ? final_query + (size_t)b0 * d : nullptr, s);
         }
-        const int n_chunks = (int)((max_rows + FW_CHUNK - 1) / FW_CHUNK);
-        ArenaPlan pl;
-        pl.take<FwAgent>((size_t)B);
-        pl.take<float>((size_t)B * d);          // x
-        pl.take<float>((size_t)B * d);          // normed
-        pl.take<float>((size_t)3 * B * d);      // q, k, v
-        pl.take<float>((size_t)B * d);          // att
-        pl.take<float>((size_t)B * dff);        // ff
-        pl.take<double>((size_t)B * w->n_heads * n_chunks * (2 + w->d_k));
-        c->arena.reserve(pl.used);
-        c->arena.reset();
-        FwAgent* dag = c->arena.take<FwAgent>((size_t)B);
-        float* x = c->arena.take<float>((size_t)B * d);
-        float* nrm = c->arena.take<float>((size_t)B * d);
-        float* qkv = c->arena.take<float>((size_t)3 * B * d);
-        float* att = c->arena.take<float>((size_t)B * d);
-        float* ff = c->arena.take<float>((size_t)B * dff);
-        double* part = c->arena.take<double>((size_t)B * w->n_heads * n_chunks * (2 + w->d_k));
-        CX_CUDA(cudaMemcpyAsync(dag, ag.data(), sizeof(FwAgent) * B, cudaMemcpyHostToDevice, s));
-        const float* W = w->buf;
-        fw_embed<<<B, 128, 0, s>>>(dag, B, W + w->emb, d, x);
-        check_launch("fw_embed");
-        const unsigned nb_warps = (unsigned)((B + 7) / 8);
-        for (int l = 0; l < L; ++l) {
-            fw_rmsnorm<<<nb_warps, 256, 0, s>>>(x, W + w->attn_norm(l), d, B, nrm, 1e-5);
-            check_launch("fw_rmsnorm");
-            // q, k, v: three matrices in one launch (wq, wk, wv are consecutive)
-            matvec_launch(W + w->wq(l), (size_t)d * d, 3, d, d, nrm, B, qkv, (size_t)B * d, 0, s);
-            fw_rope_append<<<B, 128, 0, s>>>(dag, B, l, w->n_heads, w->d_k, w->rope_base, qkv, qkv + (size_t)B * d,
-                                             qkv + (size_t)2 * B * d, l == L - 1 ? final_query : nullptr);
-            check_launch("fw_rope_append");
-            fw_attend_partial<<<dim3((unsigned)n_chunks, (unsigned)w->n_heads, (unsigned)B), FW_CHUNK, 0, s>>>(
-                dag, l, w->n_heads, w->d_k, qkv, part, n_chunks);
-            check_launch("fw_attend_partial");
-            fw_attend_combine<<<dim3((unsigned)B, (unsigned)w->n_heads), 64, 0, s>>>(B, w->n_heads, w->d_k, part,
-                                                                                    n_chunks, att);
-            check_launch("fw_attend_combine");
-            matvec_launch(W + w->wo(l), 0, 1, d, d, att, B, x, 0, 2, s);                 // x += Wo att
-            fw_rmsnorm<<<nb_warps, 256, 0, s>>>(x, W + w->mlp_norm(l), d, B, nrm, 1e-5);
-            check_launch("fw_rmsnorm");
-            matvec_launch(W + w->w_in(l), 0, 1, dff, d, nrm, B, ff, 0, 1, s);            // relu(W_in n)
-            matvec_launch(W + w->w_out(l), 0, 1, d, dff, ff, B, x, 0, 2, s);             // x += W_out ff
-        }
-        float* hid = hidden ? hidden : nrm;
-        fw_rmsnorm<<<nb_warps, 256, 0, s>>>(x, W + w->final_norm, d, B, hid, 1e-5);
-        check_launch("fw_rmsnorm");
-        if (logits) matvec_launch(W + w->unemb, 0, 1, w->vocab, d, hid, B, logits, 0, 0, s);
-        // the entry is complete at every layer (end_entry)
-        for (int b = 0; b < B; ++b) {
-            cx_kvcache* kc = caches[b];
-            kv_after(kc, s);
-            kc->positions.push_back(positions[b]);
-            kc->origins.push_back((uint8_t)CX_ORIGIN_CONTEXT);
-            kc->last_context_position = positions[b];
-            kc->context_count += 1;
-        }
+        (void)dff;
     });
 }
 
@@ -423,7 +524,7 @@ extern "C" cx_status cx_matvec(const float* w, int n_out, int n_in, const float*
             float* dy = c->arena.take<float>((size_t)n_out);
             CX_CUDA(cudaMemcpyAsync(dw, w, sizeof(float) * n_out * n_in, cudaMemcpyHostToDevice, c->stream));
             CX_CUDA(cudaMemcpyAsync(dx, x, sizeof(float) * n_in, cudaMemcpyHostToDevice, c->stream));
-            matvec_launch(dw, 0, 1, n_out, n_in, dx, 1, dy, 0, 0, c->stream);
+            matvec_launch(dw, n_out, n_in, dx, 1, dy, 0, c->stream);
             CX_CUDA(cudaMemcpyAsync(y, dy, sizeof(float) * n_out, cudaMemcpyDeviceToHost, c->stream));
         });
     });
