@@ -212,6 +212,66 @@ __global__ void __launch_bounds__(32) centroid_pipe_kernel(GroupView gv, double*
     if (c0 + lane < gv.dim) cen[(int64_t)g * gv.dim + c0 + lane] = __ddiv_rn(acc, (double)gv.L);
 }
 
+// The same sum with the rows streamed by TMA bulk copies: one CTA per group, one thread
+// per coordinate; a ring of stages of 32 contiguous rows (rstride == dim), ONE
+// cp.async.bulk per stage completing on the stage's mbarrier (per-row copies measured
+// 2.5x slower than the cp.async ring: small TMA requests are expensive).  ~128 KB of rows in flight per SM keeps the loads
+// ahead of the only serial cost, the fp64 add chain (L x ~8.4 cycles).
+constexpr int kTmaRows = 32;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(256) centroid_tma_kernel(GroupView gv, double* __restrict__ cen, int n_stages) {
+    extern __shared__ __align__(128) unsigned char csm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(csm);  // [n_stages]
+    float* ring = reinterpret_cast<float*>(csm + 128 * ((n_stages * 8 + 127) / 128));  // [n_stages][32][dim]
+    const int g = blockIdx.x, j = threadIdx.x, dim = gv.dim;
+    const float* base = gv.X + g * gv.gstride;
+    const int64_t nst = (gv.L + kTmaRows - 1) / kTmaRows;
+    const uint32_t row_bytes = (uint32_t)dim * 4u;
+    if (j == 0) {
+        for (int i = 0; i < n_stages; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + i)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int64_t st) {  // thread 0: the stage's rows are contiguous (rstride == dim)
+        const int slot = (int)(st % n_stages);
+        const int64_t r0 = st * kTmaRows;
+        const uint32_t bytes = row_bytes * (uint32_t)min((int64_t)kTmaRows, gv.L - r0);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + slot)), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(ring + (size_t)slot * kTmaRows * dim)),
+            "l"(base + r0 * dim), "r"(bytes), "r"(smem_u32(full + slot))
+            : "memory");
+    };
+    if (j == 0)
+        for (int64_t st = 0; st < min((int64_t)n_stages, nst); ++st) issue(st);
+    double acc = 0.0;
+    for (int64_t st = 0; st < nst; ++st) {
+        const int slot = (int)(st % n_stages);
+        const uint32_t par = (uint32_t)((st / n_stages) & 1);
+        uint32_t ok = 0;
+        do {
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(ok)
+                         : "r"(smem_u32(full + slot)), "r"(par)
+                         : "memory");
+        } while (!ok);
+        const float* buf = ring + (size_t)slot * kTmaRows * dim;
+        const int rows = (int)min((int64_t)kTmaRows, gv.L - st * kTmaRows);
+        if (rows == kTmaRows) {
+#pragma unroll
+            for (int r = 0; r < kTmaRows; ++r) acc = __dadd_rn(acc, (double)buf[r * dim + j]);
+        } else {
+            for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, (double)buf[r * dim + j]);
+        }
+        __syncthreads();  // every thread is done with the slot
+        if (j == 0 && st + n_stages < nst) issue(st + n_stages);
+    }
+    cen[(int64_t)g * dim + j] = __ddiv_rn(acc, (double)gv.L);
+}
+
 constexpr int kCenRows = 64;
 __global__ void __launch_bounds__(256) centroid_staged_kernel(GroupView gv, double* __restrict__ cen) {
     extern __shared__ __align__(16) float cbuf[];  // [2][kCenRows][dim]
@@ -827,7 +887,15 @@ void plan_select(ArenaPlan& p, const GroupView& g, int k) {
 
 void centroid_launch(const GroupView& g, double* cen, cudaStream_t s) {
     if (g.dim > 1024) fail(CX_DEVICE_ERROR, "select: dim > 1024 unsupported");
-    if (g.dim % 32 == 0 && (g.rstride & 3) == 0 && (g.gstride & 3) == 0 &&
+    if (g.dim % 4 == 0 && g.dim <= 256 && g.rstride == g.dim && (g.gstride & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(g.X) & 15) == 0) {
+        const size_t stage_bytes = (size_t)kTmaRows * g.dim * sizeof(float);
+        const int n_stages = (int)std::max<size_t>(2, std::min<size_t>(16, (160 * 1024) / stage_bytes));
+        const size_t smem = 128 * (((size_t)n_stages * 8 + 127) / 128) + (size_t)n_stages * stage_bytes;
+        kernel_smem(centroid_tma_kernel, smem);
+        centroid_tma_kernel<<<(unsigned)g.G, (unsigned)g.dim, smem, s>>>(g, cen, n_stages);
+        check_launch("centroid_tma_kernel");
+    } else if (g.dim % 32 == 0 && (g.rstride & 3) == 0 && (g.gstride & 3) == 0 &&
         (reinterpret_cast<uintptr_t>(g.X) & 15) == 0) {
         centroid_pipe_kernel<<<dim3((unsigned)(g.dim / 32), (unsigned)g.G), 32, 0, s>>>(g, cen);
         check_launch("centroid_pipe_kernel");
