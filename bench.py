@@ -222,7 +222,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    groups = min(G, max(threads, 8))
+    groups = G  # every step is one whole cfg2 compression (all 48 groups), as in the B200 arm
     vals = []
     for i in range(args.warmup + args.steps):
         v, kind, sample = cpu_compress_sample(threads, groups, seconds_target=0.0)
@@ -236,10 +236,10 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg2: 24 layers x 2 KV heads x d=64, L=8192 -> k=164, lambda=0.5, 14 q-heads; "
                                f"decode N={args.n_agents}, T={T_PRIV}",
-                   "sample_groups_per_step": groups},
+                   "groups_per_step": groups},
         "cpu_baseline": {"value": value, "unit": "compressions/s", "cores": threads, "kind": "reference",
                          "cpu_model": cpu_model(),
-                         "sample": f"{groups} of 48 groups per step on {threads} threads (x 48/{groups})"},
+                         "sample": f"one whole compression ({groups} groups) per step on {threads} threads"},
         "decode": {k: v for k, v in extra.items() if k.startswith("decode_")},
         "cfg4": extra["cfg4"],
         "e2e": {"value": value, "unit": "compressions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -358,17 +358,17 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
                    "groups": G, "parallelism": f"groups sharded over {world} GPU(s)" +
                    (" + one NCCL all-gather (cx_compress_sharded_dev)" if world > 1 else ""),
                    "l2": "flushed (256 MB write) between timed steps"},
-        "roofline": {"kernel": "select64_kernel (greedy max-min selection, thread-block clusters)", "bound": "hbm",
+        "roofline": {"kernel": "selx_kernel (greedy max-min selection, tcgen05 distance filter, one wave)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_source": peak_kind, "traffic": ncu_traffic("select64_kernel"),
-                     "traffic_unit": "bytes per step: all select64 launches of one compression (ncu --set full)",
+                     "peak_source": peak_kind, "traffic": ncu_traffic("selx_kernel"),
+                     "traffic_unit": "bytes per step: all selx launches of one compression (ncu --set full)",
                      "note": "selection is fp64-issue + per-round latency bound (SURVEY.md §8(d)); see roofline_fp64"},
-        "roofline_fp64": {"kernel": "select64_kernel", "bound": "fp64 add/mul issue",
+        "roofline_fp64": {"kernel": "selx_kernel", "bound": "fp64 add/mul issue",
                           "achieved": fp64_achieved / 1e12, "peak": fp64_rate / 1e12, "unit": "T fp64 op/s",
                           "frac": fp64_achieved / fp64_rate, "algorithmic_ops_per_step": fp64_ops,
                           "peak_source": "measured on this GPU (cx_probe_fp64_rate: unfused DADD/DMUL chains)",
                           "latency_model": {"rounds": K, "us_per_round": sel_ms * 1e3 / K,
-                                            "note": "k dependent rounds, each two cluster-wide exchanges"}},
+                                            "note": "k dependent rounds, each with two exchanges among the group's CTAs"}},
         "select_ms": sel_ms,
         "selection_min_decision_gap": min_gap,
         "gpu_launches": launches,
@@ -387,7 +387,7 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         try:
-            v, kind, sample = cpu_compress_sample(threads, min(G, max(threads, 8)), seconds_target=8.0)
+            v, kind, sample = cpu_compress_sample(threads, G, seconds_target=3.0)
             line["cpu_baseline"] = {"value": v, "unit": "compressions/s", "cores": threads, "kind": kind,
                                     "cpu_model": cpu_model(), "sample": sample}
         except Exception as e:  # noqa: BLE001
@@ -403,9 +403,11 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
 
 def ncu_traffic(kernel_substr):
     """dram__bytes_read.sum + dram__bytes_write.sum (bytes, one launch) of a kernel
-    from the committed `ncu --set full` summary (profiles/r1_ncu_full_summary.json,
+    from the newest committed `ncu --set full` summary (profiles/r<N>_ncu_full_summary.json,
     made by tools/ncu_summary.py from `ncu ... python tools/prof_step.py`), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_full_summary.json")
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    path = next((os.path.join(prof, f"{t}_ncu_full_summary.json") for t in ("r2", "r1")
+                 if os.path.exists(os.path.join(prof, f"{t}_ncu_full_summary.json"))), "")
     try:
         with open(path) as f:
             rows = json.load(f)

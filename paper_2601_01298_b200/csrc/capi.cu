@@ -166,7 +166,7 @@ extern "C" const char* cx_last_error(void) { return t_last_error.c_str(); }
 extern "C" uint64_t cx_kernel_launch_count(void) { return g_launches.load(); }
 
 extern "C" cx_status cx_ctx_create(int device, cx_ctx** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!out) fail(CX_INVALID_ARGUMENT, "null out");
         auto* c = new cx_ctx();
         try {
@@ -180,7 +180,7 @@ extern "C" cx_status cx_ctx_create(int device, cx_ctx** out) {
 }
 
 extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) return;
         cudaStreamSynchronize(c->stream);
         cudaStreamSynchronize(c->side);
@@ -207,7 +207,7 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
 }
 
 extern "C" cx_status cx_ctx_lane_stream(cx_ctx* c, int lane, void** stream, int* priority) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !stream) fail(CX_INVALID_ARGUMENT, "null pointer");
         if (lane != CX_LANE_RIVER && lane != CX_LANE_STREAM) fail(CX_INVALID_ARGUMENT, "unknown lane");
         *stream = (void*)c->lane[lane];
@@ -220,7 +220,7 @@ extern "C" cx_status cx_ctx_lane_stream(cx_ctx* c, int lane, void** stream, int*
 // ============================================================================
 extern "C" cx_status cx_attention_scores_points(const float* keys, int64_t count, int dim, const float* query,
                                                 int64_t query_len, int n_heads, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         // synapse.cpp:66-70, in order
         if (count == 0) fail(CX_PRECONDITION_ERROR, "attention_scores: empty candidate set");
         if (query_len != (int64_t)dim) fail(CX_PRECONDITION_ERROR, "attention_scores: query width mismatch");
@@ -255,7 +255,7 @@ extern "C" cx_status cx_attention_scores_points(const float* keys, int64_t count
 
 extern "C" cx_status cx_coverage_scores_points(const float* cloud, int64_t count, int dim, const int64_t* selected,
                                                int64_t n_selected, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (count == 0) return;  // synapse.cpp:105-106 (empty output)
         if (count < 0 || dim < 1 || !cloud || !out || (n_selected > 0 && !selected))
             fail(CX_INVALID_ARGUMENT, "null pointer / bad shape");
@@ -287,7 +287,7 @@ extern "C" cx_status cx_coverage_scores_points(const float* cloud, int64_t count
 extern "C" cx_status cx_select_landmarks_points(const float* cloud, int64_t count, int dim, const double* attention,
                                                 int64_t attention_len, int k, double lambda, int64_t* out_indices,
                                                 double* out_scores, int64_t* out_n) {
-    return guard([&] {
+    return guard(__func__, [&] {
         // synapse.cpp:219-223, in order
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
         if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
@@ -366,7 +366,7 @@ double mean_pairwise_impl(cx_ctx* c, const float* d_pts, int64_t count, int dim,
 
 extern "C" cx_status cx_hausdorff_distance(const float* cloud, int64_t count, int dim, const float* landmarks,
                                            int64_t m, int ldim, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (count == 0 || m == 0) fail(CX_PRECONDITION_ERROR, "hausdorff_distance: empty point set");
         if (dim != ldim) fail(CX_PRECONDITION_ERROR, "hausdorff_distance: dimension mismatch");
         if (!cloud || !landmarks || !out || count < 0 || m < 0) fail(CX_INVALID_ARGUMENT, "null pointer");
@@ -376,7 +376,7 @@ extern "C" cx_status cx_hausdorff_distance(const float* cloud, int64_t count, in
 
 extern "C" cx_status cx_hausdorff_to_subset(const float* cloud, int64_t count, int dim, const int64_t* rows,
                                             int64_t n_rows, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_rows == 0) fail(CX_PRECONDITION_ERROR, "hausdorff: empty landmark set");
         if (!out || !rows || n_rows < 0 || count < 0) fail(CX_INVALID_ARGUMENT, "null pointer");
         if (count == 0) { *out = 0.0; return; }
@@ -386,7 +386,7 @@ extern "C" cx_status cx_hausdorff_to_subset(const float* cloud, int64_t count, i
 
 extern "C" cx_status cx_mean_pairwise_reduction(const float* cloud, int64_t count, int dim, const float* landmarks,
                                                 int64_t m, int ldim, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (m < 2) fail(CX_PRECONDITION_ERROR, "mean_pairwise_reduction: need >= 2 landmarks");
         if (count < 2) fail(CX_PRECONDITION_ERROR, "mean_pairwise_reduction: need >= 2 cloud points");
         if (!cloud || !landmarks || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
@@ -413,7 +413,7 @@ extern "C" cx_status cx_mean_pairwise_reduction(const float* cloud, int64_t coun
 
 extern "C" cx_status cx_mean_pairwise_reduction_subset(const float* cloud, int64_t count, int dim, const int64_t* rows,
                                                        int64_t n_rows, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_rows < 2) fail(CX_PRECONDITION_ERROR, "mean_pairwise_reduction: need >= 2 landmarks");
         if (count < 2) fail(CX_PRECONDITION_ERROR, "mean_pairwise_reduction: need >= 2 cloud points");
         if (!cloud || !rows || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
@@ -440,7 +440,7 @@ extern "C" cx_status cx_mean_pairwise_reduction_subset(const float* cloud, int64
 
 extern "C" cx_status cx_attend(const float* q, const float* keys, const float* values, int64_t n_entries, int n_heads,
                                int d_k, float* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_heads < 1 || d_k < 1 || n_entries < 1) fail(CX_PRECONDITION_ERROR, "attend: bad shape");
         if (!q || !keys || !values || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
         const int64_t dm = (int64_t)n_heads * d_k;
@@ -470,7 +470,7 @@ extern "C" cx_status cx_attend(const float* q, const float* keys, const float* v
 
 // kernels::softmax (kernels.cpp:66-92): precondition_error on empty or non-finite input
 extern "C" cx_status cx_softmax(const double* scores, int64_t n, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n < 1) fail(CX_PRECONDITION_ERROR, "softmax: empty input");
         if (!scores || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
         cx_ctx* c = default_ctx();
@@ -492,7 +492,7 @@ extern "C" cx_status cx_softmax(const double* scores, int64_t n, double* out) {
 
 // the float overload widens first (kernels.cpp:89-92)
 extern "C" cx_status cx_softmax_f32(const float* scores, int64_t n, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n < 1) fail(CX_PRECONDITION_ERROR, "softmax: empty input");
         if (!scores || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
         std::vector<double> w(scores, scores + n);
@@ -503,7 +503,7 @@ extern "C" cx_status cx_softmax_f32(const float* scores, int64_t n, double* out)
 
 // kernels::argmax (kernels.cpp:94-101); the reference asserts a non-empty input
 extern "C" cx_status cx_argmax(const float* v, int64_t n, int* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n < 1) fail(CX_PRECONDITION_ERROR, "argmax: empty input");
         if (!v || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
         cx_ctx* c = default_ctx();
@@ -524,7 +524,7 @@ extern "C" cx_status cx_argmax(const float* v, int64_t n, int* out) {
 
 // gate.cpp:27-43 gate_score for one (h_main, t_side) pair, on the device
 extern "C" cx_status cx_gate_score(const float* h_main, const float* t_side, int64_t n, double* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n < 1) fail(CX_DEGENERATE_INPUT_ERROR, "gate_score: zero-norm input");  // empty: both norms 0
         if (!h_main || !t_side || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
         cx_ctx* c = default_ctx();
@@ -556,7 +556,7 @@ extern "C" cx_status cx_gate_score(const float* h_main, const float* t_side, int
 extern "C" cx_status cx_gate_decide_dev(cx_ctx* c, int64_t n_pairs, int dim, const float* h, int64_t h_stride,
                                         const float* t, int64_t t_stride, double theta, double* scores,
                                         uint8_t* accepted, uint8_t* degenerate, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (theta < -1.0 || theta > 1.0) fail(CX_PRECONDITION_ERROR, "decide: theta must be in [-1,1]");
         if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
         if (n_pairs < 0 || dim < 0) fail(CX_PRECONDITION_ERROR, "gate: bad shape");
@@ -570,7 +570,7 @@ extern "C" cx_status cx_gate_decide_dev(cx_ctx* c, int64_t n_pairs, int dim, con
 // grouped device path
 // ============================================================================
 extern "C" cx_status cx_attention_grouped_dev(cx_ctx* c, const cx_groups* gr, double* out, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !out) fail(CX_INVALID_ARGUMENT, "null ctx/out");
         validate_groups(gr, true);
         GroupView g = view_of(gr);
@@ -585,7 +585,7 @@ extern "C" cx_status cx_attention_grouped_dev(cx_ctx* c, const cx_groups* gr, do
 extern "C" cx_status cx_select_grouped_dev(cx_ctx* c, const cx_groups* gr, const double* attention, int k,
                                            double lambda, unsigned flags, int64_t* out_rows, double* out_scores,
                                            void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
         if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
         if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
@@ -602,7 +602,7 @@ extern "C" cx_status cx_select_grouped_dev(cx_ctx* c, const cx_groups* gr, const
 }
 
 extern "C" cx_status cx_ctx_set_option(cx_ctx* c, int option, int64_t value) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
         auto in = [&](int64_t lo, int64_t hi) {
             if (value < lo || value > hi) fail(CX_INVALID_ARGUMENT, "ctx_set_option: value out of range");
@@ -623,7 +623,7 @@ extern "C" cx_status cx_ctx_set_option(cx_ctx* c, int option, int64_t value) {
 }
 
 extern "C" cx_status cx_ctx_get_option(cx_ctx* c, int option, int64_t* value) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !value) fail(CX_INVALID_ARGUMENT, "null ctx/value");
         switch (option) {
             case CX_OPT_SELECT_CLUSTER: *value = c->opt.select_cluster; break;
@@ -639,7 +639,7 @@ extern "C" cx_status cx_ctx_get_option(cx_ctx* c, int option, int64_t* value) {
 }
 
 extern "C" cx_status cx_ctx_device_errors(cx_ctx* c, void* stream, unsigned* flags, int clear) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !flags) fail(CX_INVALID_ARGUMENT, "null ctx/flags");
         int f = 0;
         cudaStream_t s = (cudaStream_t)stream;
@@ -651,7 +651,7 @@ extern "C" cx_status cx_ctx_device_errors(cx_ctx* c, void* stream, unsigned* fla
 }
 
 extern "C" cx_status cx_selection_gaps(cx_ctx* c, int n_groups, double* out, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !out) fail(CX_INVALID_ARGUMENT, "null ctx/out");
         if (n_groups < 0 || n_groups > c->gaps_n)
             fail(CX_PRECONDITION_ERROR, "selection_gaps: more groups than the last selection launch");
@@ -663,7 +663,7 @@ extern "C" cx_status cx_selection_gaps(cx_ctx* c, int n_groups, double* out, voi
 
 extern "C" cx_status cx_gather_grouped_dev(cx_ctx* c, const cx_groups* gr, const float* src, const int64_t* rows,
                                            int take, float* dst, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
         validate_groups(gr, false);
         if (take < 0) fail(CX_INVALID_ARGUMENT, "negative take");
@@ -718,7 +718,7 @@ void compress_impl(cx_ctx* c, const cx_groups* gr, const float* values, int k, d
 extern "C" cx_status cx_compress_grouped_dev(cx_ctx* c, const cx_groups* gr, const float* values, int k, double lambda,
                                              unsigned flags, int64_t* out_rows, double* out_scores, float* syn_keys,
                                              float* syn_values, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
         if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
         if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
@@ -734,7 +734,7 @@ extern "C" cx_status cx_compress_grouped_strided_dev(cx_ctx* c, const cx_groups*
                                                      double lambda, unsigned flags, int64_t* out_rows,
                                                      double* out_scores, float* syn_keys, float* syn_values,
                                                      int64_t syn_group_stride, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
         if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
         if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
@@ -752,7 +752,7 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
                                               const float* values, const float* queries, int n_pass, int d_k,
                                               int col_step, int k, double lambda, unsigned flags, int64_t* out_rows,
                                               double* out_scores, float* syn_keys, float* syn_values) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
         if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
         if (!c) fail(CX_INVALID_ARGUMENT, "null ctx");
@@ -924,7 +924,7 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
 }
 
 extern "C" cx_status cx_decode_step_dev(cx_ctx* c, const cx_decode_batch* b, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !b) fail(CX_INVALID_ARGUMENT, "null ctx/batch");
         if (b->n_agents < 0 || b->n_layers < 1 || b->n_kv < 1 || b->n_q < b->n_kv || b->n_q % b->n_kv != 0 ||
             b->d_k < 1 || b->k_syn < 0 || b->t_cap < 1)
@@ -1012,7 +1012,7 @@ void kv_begin(cx_kvcache* c, int64_t position, cx_origin origin) {
 
 extern "C" cx_status cx_kvcache_create(int n_layers, int n_heads, int d_model, int d_k, int64_t max_positions,
                                        int64_t capacity, cx_kvcache** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         // ModelConfig::validate (model.cpp:12-21), the parts KvCache depends on
         if (n_layers < 1 || n_heads < 1 || d_model < 1 || d_k < 1) fail(CX_CONFIG_ERROR, "model dimensions must be positive");
         if (n_heads * d_k != d_model) fail(CX_CONFIG_ERROR, "d_model must equal n_heads * d_k exactly");
@@ -1040,7 +1040,7 @@ extern "C" cx_status cx_kvcache_create(int n_layers, int n_heads, int d_model, i
 
 // value semantics of the reference KvCache (model.hpp:67-113 is copyable): a deep copy
 extern "C" cx_status cx_kvcache_clone(const cx_kvcache* src, cx_kvcache** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!src || !out) fail(CX_INVALID_ARGUMENT, "null cache/out");
         cx_kvcache* c = nullptr;
         const cx_status st = cx_kvcache_create(src->n_layers, src->n_heads, src->d_model, src->d_k, src->max_positions,
@@ -1074,7 +1074,7 @@ extern "C" cx_status cx_kvcache_clone(const cx_kvcache* src, cx_kvcache** out) {
 }
 
 extern "C" cx_status cx_kvcache_destroy(cx_kvcache* c) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) return;
         cudaStreamSynchronize(c->stream);
         if (c->keys) cudaFree(c->keys);
@@ -1096,7 +1096,7 @@ extern "C" const int64_t* cx_kvcache_positions_host(const cx_kvcache* c) { retur
 extern "C" const uint8_t* cx_kvcache_origins_host(const cx_kvcache* c) { return c ? c->origins.data() : nullptr; }
 
 extern "C" cx_status cx_kvcache_begin_entry(cx_kvcache* c, int64_t position, cx_origin origin) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
         kv_begin(c, position, origin);
     });
@@ -1104,7 +1104,7 @@ extern "C" cx_status cx_kvcache_begin_entry(cx_kvcache* c, int64_t position, cx_
 
 extern "C" cx_status cx_kvcache_write_layer(cx_kvcache* c, int layer, const float* key, const float* value,
                                             int64_t width) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
         // model.cpp:144-147
         if (!c->entry_open) fail(CX_SEQUENCING_ERROR, "no open cache entry");
@@ -1120,7 +1120,7 @@ extern "C" cx_status cx_kvcache_write_layer(cx_kvcache* c, int layer, const floa
 }
 
 extern "C" cx_status cx_kvcache_end_entry(cx_kvcache* c) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
         // model.cpp:155-157
         if (!c->entry_open) fail(CX_SEQUENCING_ERROR, "no open cache entry");
@@ -1131,7 +1131,7 @@ extern "C" cx_status cx_kvcache_end_entry(cx_kvcache* c) {
 
 extern "C" cx_status cx_kvcache_append_entry(cx_kvcache* c, int64_t position, cx_origin origin, const float* keys,
                                              const float* values) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !keys || !values) fail(CX_INVALID_ARGUMENT, "null pointer");
         kv_begin(c, position, origin);  // model.cpp:161-173: begin, write every layer, end
         const int64_t row = (int64_t)c->positions.size() - 1;
@@ -1148,7 +1148,7 @@ extern "C" cx_status cx_kvcache_append_entry(cx_kvcache* c, int64_t position, cx
 
 extern "C" cx_status cx_kvcache_append_context_dev(cx_kvcache* c, const float* keys, const float* values,
                                                     int64_t base_position, int64_t count, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
         if (count < 0) fail(CX_INVALID_ARGUMENT, "negative count");
         if (count == 0) return;
@@ -1205,7 +1205,7 @@ extern "C" cx_status cx_kvcache_append_context_dev(cx_kvcache* c, const float* k
 
 extern "C" cx_status cx_kvcache_read(const cx_kvcache* c, int layer, int64_t first, int64_t n, float* keys_out,
                                      float* values_out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
         if (layer < 0 || layer >= c->n_layers || first < 0 || n < 0 || first + n > (int64_t)c->positions.size())
             fail(CX_PRECONDITION_ERROR, "kvcache_read: range outside the cache");
@@ -1268,7 +1268,7 @@ void inject_apply(cx_kvcache* c, const float* dk, const float* dv, int64_t block
 extern "C" cx_status cx_inject_host(cx_kvcache* c, const float* keys, const float* values, int64_t base_position,
                                     int64_t token_count, int n_layers, int d_model, int64_t thought_id,
                                     int64_t stream_position, cx_injection_record* rec) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
         cx_status err;
         std::string msg;
@@ -1300,7 +1300,7 @@ extern "C" cx_status cx_inject_host(cx_kvcache* c, const float* keys, const floa
 extern "C" cx_status cx_inject_dev(cx_kvcache* c, const float* keys, const float* values, int64_t base_position,
                                    int64_t token_count, int n_layers, int d_model, int64_t thought_id,
                                    int64_t stream_position, cx_injection_record* rec, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null cache");
         cx_status err;
         std::string msg;
@@ -1343,7 +1343,7 @@ struct cx_snapshot {
 
 extern "C" cx_status cx_select_landmarks(const cx_kvcache* kc, const float* query, int64_t query_len, int k,
                                          double lambda, cx_snapshot** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");  // synapse.cpp:288
         if (!kc || !out) fail(CX_INVALID_ARGUMENT, "null cache/out");
         auto snap = std::make_unique<cx_snapshot>();
@@ -1459,7 +1459,7 @@ extern "C" cx_status cx_select_landmarks(const cx_kvcache* kc, const float* quer
 extern "C" cx_status cx_snapshot_create(int64_t source_length, int k_configured, int n_layers, int d_model,
                                         int64_t count, const int64_t* positions, const double* scores,
                                         const float* keys, const float* values, cx_snapshot** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!out || count < 0 || n_layers < 0 || d_model < 0) fail(CX_INVALID_ARGUMENT, "bad snapshot arguments");
         if (count > 0 && (!positions || !scores || n_layers < 1 || d_model < 1))
             fail(CX_INVALID_ARGUMENT, "snapshot arrays missing");
@@ -1494,7 +1494,7 @@ extern "C" cx_status cx_snapshot_create(int64_t source_length, int k_configured,
 }
 
 extern "C" cx_status cx_snapshot_release(const cx_snapshot* s) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!s) return;
         auto* m = const_cast<cx_snapshot*>(s);
         if (m->refs.fetch_sub(1) == 1) delete m;
@@ -1512,7 +1512,7 @@ extern "C" const float* cx_snapshot_values_dev(const cx_snapshot* s) { return s 
 
 extern "C" cx_status cx_snapshot_read(const cx_snapshot* s, int64_t* positions, double* scores, float* keys,
                                       float* values) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!s) fail(CX_INVALID_ARGUMENT, "null snapshot");
         if (positions) std::copy(s->positions.begin(), s->positions.end(), positions);
         if (scores) std::copy(s->scores.begin(), s->scores.end(), scores);
@@ -1543,14 +1543,14 @@ struct cx_synapse_buffer {
 };
 
 extern "C" cx_status cx_synapse_buffer_create(cx_synapse_buffer** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!out) fail(CX_INVALID_ARGUMENT, "null out");
         *out = new cx_synapse_buffer();
     });
 }
 
 extern "C" cx_status cx_synapse_buffer_destroy(cx_synapse_buffer* b) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!b) return;
         if (b->latest) cx_snapshot_release(b->latest);
         delete b;
@@ -1558,7 +1558,7 @@ extern "C" cx_status cx_synapse_buffer_destroy(cx_synapse_buffer* b) {
 }
 
 extern "C" cx_status cx_synapse_buffer_push(cx_synapse_buffer* b, cx_snapshot* snap, uint64_t* version) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!b || !snap) fail(CX_INVALID_ARGUMENT, "null buffer/snapshot");
         cx_snapshot* old = nullptr;
         {
@@ -1574,7 +1574,7 @@ extern "C" cx_status cx_synapse_buffer_push(cx_synapse_buffer* b, cx_snapshot* s
 }
 
 extern "C" cx_status cx_synapse_buffer_read_latest(cx_synapse_buffer* b, const cx_snapshot** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!b || !out) fail(CX_INVALID_ARGUMENT, "null buffer/out");
         std::lock_guard<std::mutex> lk(b->mu);
         if (b->latest) b->latest->refs.fetch_add(1);
@@ -1583,7 +1583,7 @@ extern "C" cx_status cx_synapse_buffer_read_latest(cx_synapse_buffer* b, const c
 }
 
 extern "C" cx_status cx_synapse_buffer_wait_nonempty(cx_synapse_buffer* b, int64_t timeout_ms, const cx_snapshot** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!b || !out) fail(CX_INVALID_ARGUMENT, "null buffer/out");
         std::unique_lock<std::mutex> lk(b->mu);
         b->cv.wait_for(lk, std::chrono::milliseconds(timeout_ms), [&] { return b->latest != nullptr || b->shutdown; });
@@ -1593,7 +1593,7 @@ extern "C" cx_status cx_synapse_buffer_wait_nonempty(cx_synapse_buffer* b, int64
 }
 
 extern "C" cx_status cx_synapse_buffer_shutdown(cx_synapse_buffer* b) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!b) fail(CX_INVALID_ARGUMENT, "null buffer");
         std::lock_guard<std::mutex> lk(b->mu);
         b->shutdown = true;

@@ -174,7 +174,7 @@ extern "C" int cx_nccl_version(void) {
 }
 
 extern "C" cx_status cx_comm_unique_id(void* id) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!id) fail(CX_INVALID_ARGUMENT, "null id");
         ncclUniqueId u;
         CX_NCCL(nccl().getUniqueId(&u));
@@ -183,7 +183,7 @@ extern "C" cx_status cx_comm_unique_id(void* id) {
 }
 
 extern "C" cx_status cx_comm_init_rank(int nranks, const void* id, int rank, int device, cx_comm** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!id || !out) fail(CX_INVALID_ARGUMENT, "null id/out");
         if (nranks < 1 || rank < 0 || rank >= nranks) fail(CX_INVALID_ARGUMENT, "bad rank / nranks");
         ncclUniqueId u;
@@ -199,7 +199,7 @@ extern "C" cx_status cx_comm_init_rank(int nranks, const void* id, int rank, int
 }
 
 extern "C" cx_status cx_comm_init_all(int ndev, const int* devices, cx_comm** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (ndev < 1 || !devices || !out) fail(CX_INVALID_ARGUMENT, "bad device list");
         std::vector<ncclComm_t> comms((size_t)ndev);
         CX_NCCL(nccl().commInitAll(comms.data(), ndev, devices));
@@ -215,7 +215,7 @@ extern "C" cx_status cx_comm_init_all(int ndev, const int* devices, cx_comm** ou
 }
 
 extern "C" cx_status cx_comm_destroy(cx_comm* c) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) return;
         if (c->buf) cudaFree(c->buf);
         if (c->comm) nccl().commDestroy(c->comm);
@@ -224,7 +224,7 @@ extern "C" cx_status cx_comm_destroy(cx_comm* c) {
 }
 
 extern "C" cx_status cx_comm_info(const cx_comm* c, int* rank, int* nranks, int* device) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c) fail(CX_INVALID_ARGUMENT, "null comm");
         if (rank) *rank = c->rank;
         if (nranks) *nranks = c->nranks;
@@ -232,15 +232,15 @@ extern "C" cx_status cx_comm_info(const cx_comm* c, int* rank, int* nranks, int*
     });
 }
 
-extern "C" cx_status cx_comm_group_start(void) { return guard([&] { CX_NCCL(nccl().groupStart()); }); }
-extern "C" cx_status cx_comm_group_end(void) { return guard([&] { CX_NCCL(nccl().groupEnd()); }); }
+extern "C" cx_status cx_comm_group_start(void) { return guard(__func__, [&] { CX_NCCL(nccl().groupStart()); }); }
+extern "C" cx_status cx_comm_group_end(void) { return guard(__func__, [&] { CX_NCCL(nccl().groupEnd()); }); }
 
 extern "C" size_t cx_synapse_record_bytes(int take, int dim) { return record_bytes(take, dim); }
 
 extern "C" cx_status cx_synapse_pack_dev(const int64_t* rows, const double* scores, const float* syn_keys,
                                          const float* syn_values, int g_begin, int n_groups, int take, int dim,
                                          void* dst, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_groups < 0 || take < 0 || g_begin < 0) fail(CX_INVALID_ARGUMENT, "negative size");
         if (n_groups == 0 || take == 0) return;
         check_dim(dim);
@@ -252,7 +252,7 @@ extern "C" cx_status cx_synapse_pack_dev(const int64_t* rows, const double* scor
 extern "C" cx_status cx_synapse_unpack_dev(const void* src, int n_groups, int nranks, int take, int dim,
                                            int64_t* rows, double* scores, float* syn_keys, float* syn_values,
                                            void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_groups < 0 || take < 0 || nranks < 1) fail(CX_INVALID_ARGUMENT, "bad size");
         if (n_groups == 0 || take == 0) return;
         check_dim(dim);
@@ -267,7 +267,7 @@ extern "C" cx_status cx_synapse_unpack_dev(const void* src, int n_groups, int nr
 extern "C" cx_status cx_synapse_pack_host(const int64_t* rows, const double* scores, const float* syn_keys,
                                           const float* syn_values, int g_begin, int n_groups, int take, int dim,
                                           void* dst) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_groups < 0 || take < 0 || g_begin < 0) fail(CX_INVALID_ARGUMENT, "negative size");
         if (n_groups == 0 || take == 0) return;
         check_dim(dim);
@@ -287,7 +287,7 @@ extern "C" cx_status cx_synapse_pack_host(const int64_t* rows, const double* sco
 
 extern "C" cx_status cx_synapse_unpack_host(const void* src, int n_groups, int nranks, int take, int dim,
                                             int64_t* rows, double* scores, float* syn_keys, float* syn_values) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_groups < 0 || take < 0 || nranks < 1) fail(CX_INVALID_ARGUMENT, "bad size");
         if (n_groups == 0 || take == 0) return;
         check_dim(dim);
@@ -313,7 +313,7 @@ extern "C" cx_status cx_compress_sharded_dev(cx_ctx* ctx, cx_comm* comm, const c
                                              int n_groups_total, int k, double lambda, unsigned flags,
                                              int64_t* out_rows, double* out_scores, float* syn_keys,
                                              float* syn_values, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (k < 1) fail(CX_CONFIG_ERROR, "select_landmarks: k must be >= 1");
         if (lambda < 0.0 || lambda > 1.0) fail(CX_CONFIG_ERROR, "select_landmarks: lambda must be in [0,1]");
         if (!ctx || !comm || !local) fail(CX_INVALID_ARGUMENT, "null ctx/comm/groups");
@@ -360,7 +360,7 @@ extern "C" cx_status cx_compress_sharded_dev(cx_ctx* ctx, cx_comm* comm, const c
 // [n_layers][T][d_model] keys + values as one ncclSend / ncclRecv pair.
 extern "C" cx_status cx_thought_send_dev(cx_comm* comm, const float* keys, const float* values, int64_t token_count,
                                          int n_layers, int d_model, int river_rank, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!comm || !keys || !values) fail(CX_INVALID_ARGUMENT, "null comm/block");
         if (token_count < 1) fail(CX_PRECONDITION_ERROR, "inject: empty block");
         if (river_rank < 0 || river_rank >= comm->nranks || river_rank == comm->rank)
@@ -375,7 +375,7 @@ extern "C" cx_status cx_thought_send_dev(cx_comm* comm, const float* keys, const
 
 extern "C" cx_status cx_thought_recv_dev(cx_comm* comm, float* keys, float* values, int64_t token_count, int n_layers,
                                          int d_model, int src_rank, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!comm || !keys || !values) fail(CX_INVALID_ARGUMENT, "null comm/block");
         if (token_count < 1) fail(CX_PRECONDITION_ERROR, "inject: empty block");
         if (src_rank < 0 || src_rank >= comm->nranks || src_rank == comm->rank)

@@ -132,6 +132,7 @@ cx_decode_batch agent_batch(cx_cortex* r, int buf) {
 
 // push_synapse (scheduler.cpp:158-165) of the context rows so far -> syn[buf]
 void push(cx_cortex* r, int buf) {
+    cx::NvtxRange range("cortex push_synapse");
     const int64_t L = r->ctx_n;
     // the last agent step that read this buffer is done with it
     CX_CUDA(cudaStreamWaitEvent(r->rs, r->reader_done[buf], 0));
@@ -226,6 +227,7 @@ void mirror_row(cx_cortex* r, int64_t row) {
 
 // drain_injections: encode the thought at the next virtual positions, append it to the river
 void inject_thought(cx_cortex* r, const int* thought, int64_t thought_id, int64_t stream_position) {
+    cx::NvtxRange range("cortex drain_injections");
     const int T = r->cfg.thought_tokens;
     cx_kvcache* sc = r->scratch;
     // a fresh scratch cache per thought (encode_thought's KvCache scratch(cfg))
@@ -255,7 +257,7 @@ using namespace cx;
 
 extern "C" cx_status cx_cortex_create(cx_ctx* ctx, const cx_weights* w, cx_kvcache* river, const cx_cortex_config* cfg,
                                       const cx_cortex_agents* agents, cx_cortex** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!ctx || !w || !river || !cfg || !agents || !out) fail(CX_INVALID_ARGUMENT, "null argument");
         if (cfg->n_agents < 1 || cfg->k < 1 || cfg->push_every < 1 || cfg->inject_every < 1 || cfg->thought_tokens < 1 ||
             cfg->t_cap < 1 || cfg->n_q < river->n_heads || cfg->n_q % river->n_heads != 0)
@@ -356,6 +358,7 @@ void agent_lane(cx_cortex* r, int n_steps, uint64_t* versions_used, float* out_h
     CX_CUDA(cudaSetDevice(r->ctx->device));
     const size_t n_out = (size_t)r->cfg.n_agents * r->n_layers * r->cfg.n_q * r->d_k;
     for (int s = 0; s < n_steps; ++s) {
+        cx::NvtxRange range("cortex agent step");
         if (s >= kAhead) CX_CUDA(cudaEventSynchronize(r->aev[s % kAhead]));
         uint64_t ver = 0;
         {
@@ -377,6 +380,7 @@ void agent_lane(cx_cortex* r, int n_steps, uint64_t* versions_used, float* out_h
 void river_lane(cx_cortex* r, int n_tokens, const int* river_tokens, const int* thought_tokens, float* river_logits) {
     const int V = r->w->vocab, inj = r->cfg.inject_every;
     for (int t = 0; t < n_tokens; ++t) {
+        cx::NvtxRange range("cortex river token");
         if (t >= kAhead) CX_CUDA(cudaEventSynchronize(r->rev[t % kAhead]));
         if (r->position >= r->cfg.virtual_base)  // scheduler.cpp step_token
             fail(CX_CAPACITY_ERROR, "river stream reached the reserved virtual range");
@@ -416,7 +420,7 @@ void river_lane(cx_cortex* r, int n_tokens, const int* river_tokens, const int* 
 extern "C" cx_status cx_cortex_run(cx_cortex* r, int n_tokens, const int* river_tokens, const int* thought_tokens,
                                    int n_agent_steps, cx_cortex_stats* stats, uint64_t* versions_used,
                                    float* river_logits, float* synapse_history, int max_versions, float* out_history) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!r || (n_tokens > 0 && (!river_tokens || !thought_tokens))) fail(CX_INVALID_ARGUMENT, "null argument");
         if (n_tokens < 0 || n_agent_steps < 0) fail(CX_INVALID_ARGUMENT, "negative step count");
         for (int t = 0; t < n_tokens; ++t)
@@ -479,7 +483,7 @@ extern "C" cx_status cx_cortex_run(cx_cortex* r, int n_tokens, const int* river_
 
 // the synapse of the front buffer (the latest published version) -> device copies
 extern "C" cx_status cx_cortex_front_synapse(const cx_cortex* r, float* keys, float* values, uint64_t* version) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!r) fail(CX_INVALID_ARGUMENT, "null runtime");
         CX_CUDA(cudaStreamSynchronize(r->ss));
         if (keys)
@@ -493,7 +497,7 @@ extern "C" cx_status cx_cortex_front_synapse(const cx_cortex* r, float* keys, fl
 }
 
 extern "C" cx_status cx_cortex_destroy(cx_cortex* r) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!r) return;
         cudaStreamSynchronize(r->ss);
         cudaStreamSynchronize(r->rs);

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -61,9 +62,21 @@ struct Options {
     int host_upload_values = 0;  // CX_OPT_HOST_UPLOAD_VALUES: host path uploads all values even when pinned
 };
 
-// Runs f, mapping exceptions to cx_status (the C boundary).
+// One NVTX range per C-ABI call (named after the entry point) and per runtime phase: an
+// attached Nsight tool shows the boundary calls and the River / Stream work on the timeline;
+// without a tool the push / pop are a few-ns no-op (NVTX v3 is header-only, no link-time
+// dependency).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// Runs f inside an NVTX range named `name`, mapping exceptions to cx_status (the C boundary).
 template <class F>
-cx_status guard(F&& f) {
+cx_status guard(const char* name, F&& f) {
+    NvtxRange range(name);
     try {
         f();
         return CX_OK;

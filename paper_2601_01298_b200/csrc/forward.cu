@@ -322,7 +322,7 @@ extern "C" size_t cx_weights_flat_floats(int n_layers, int d_model, int vocab_si
 
 extern "C" cx_status cx_weights_create(int n_layers, int n_heads, int d_model, int d_k, int vocab_size,
                                        int64_t max_positions, double rope_base, const float* flat, cx_weights** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!flat || !out) fail(CX_INVALID_ARGUMENT, "null flat/out");
         if (n_layers < 1 || n_heads < 1 || d_k < 1 || n_heads * d_k != d_model || d_k % 2 != 0 || vocab_size < 1 ||
             d_k > 64)
@@ -349,7 +349,7 @@ extern "C" cx_status cx_weights_create(int n_layers, int n_heads, int d_model, i
 }
 
 extern "C" cx_status cx_weights_destroy(cx_weights* w) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!w) return;
         if (w->buf) cudaFree(w->buf);
         delete w;
@@ -438,7 +438,7 @@ void forward_batch(cx_ctx* c, const cx_weights* w, int nb, cx_kvcache* const* ca
 extern "C" cx_status cx_forward_step_dev(cx_ctx* c, const cx_weights* w, int n_agents, cx_kvcache* const* caches,
                                          const int* tokens, const int64_t* positions, float* logits, float* hidden,
                                          float* final_query, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !w) fail(CX_INVALID_ARGUMENT, "null ctx/weights");
         if (n_agents < 0) fail(CX_INVALID_ARGUMENT, "negative agent count");
         if (n_agents == 0) return;
@@ -474,7 +474,7 @@ extern "C" cx_status cx_forward_step_dev(cx_ctx* c, const cx_weights* w, int n_a
 }
 
 extern "C" cx_status cx_device_alloc(size_t bytes, void** out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!out) fail(CX_INVALID_ARGUMENT, "null out");
         *out = nullptr;
         if (bytes) CX_CUDA(cudaMalloc(out, bytes));
@@ -482,13 +482,13 @@ extern "C" cx_status cx_device_alloc(size_t bytes, void** out) {
 }
 
 extern "C" cx_status cx_device_free(void* p) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (p) CX_CUDA(cudaFree(p));
     });
 }
 
 extern "C" cx_status cx_device_read(void* host, const void* dev, size_t bytes, void* stream) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!bytes) return;
         if (!host || !dev) fail(CX_INVALID_ARGUMENT, "null pointer");
         CX_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
@@ -508,7 +508,7 @@ void on_default(F&& f) {
 }  // namespace
 
 extern "C" cx_status cx_matvec(const float* w, int n_out, int n_in, const float* x, float* y) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n_out < 0 || n_in < 0) fail(CX_PRECONDITION_ERROR, "matvec: bad shape");
         if (n_out == 0) return;
         if (!w || !x || !y) fail(CX_INVALID_ARGUMENT, "null pointer");
@@ -531,7 +531,7 @@ extern "C" cx_status cx_matvec(const float* w, int n_out, int n_in, const float*
 }
 
 extern "C" cx_status cx_rmsnorm(const float* x, const float* gain, int64_t n, double eps, float* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n < 1) fail(CX_PRECONDITION_ERROR, "rmsnorm: empty input");
         if (!x || !gain || !out) fail(CX_INVALID_ARGUMENT, "null pointer");
         on_default([&](cx_ctx* c) {
@@ -554,7 +554,7 @@ extern "C" cx_status cx_rmsnorm(const float* x, const float* gain, int64_t n, do
 }
 
 extern "C" cx_status cx_elementwise(float* x, const float* y, int64_t n, int op) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n < 0 || (op != 0 && op != 1)) fail(CX_INVALID_ARGUMENT, "elementwise: bad arguments");
         if (n == 0) return;
         if (!x || (op == 0 && !y)) fail(CX_INVALID_ARGUMENT, "null pointer");
@@ -576,7 +576,7 @@ extern "C" cx_status cx_elementwise(float* x, const float* y, int64_t n, int op)
 }
 
 extern "C" cx_status cx_apply_rope(float* v, int64_t n, int64_t position, double rope_base) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (n < 0 || n % 2 != 0) fail(CX_PRECONDITION_ERROR, "apply_rope: odd length");
         if (n == 0) return;
         if (!v) fail(CX_INVALID_ARGUMENT, "null pointer");

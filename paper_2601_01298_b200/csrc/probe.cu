@@ -33,7 +33,7 @@ using namespace cx;
 
 // fp64 add / mul operations per second (one op per DADD or DMUL), whole device.
 extern "C" cx_status cx_probe_fp64_rate(cx_ctx* c, double* ops_per_s) {
-    return guard([&] {
+    return guard(__func__, [&] {
         if (!c || !ops_per_s) fail(CX_INVALID_ARGUMENT, "null ctx/out");
         CX_CUDA(cudaSetDevice(c->device));
         const int blocks = c->num_sms * 8, threads = 256, n = 4096;

@@ -1,5 +1,7 @@
+# per-phase cycles of select_tc (experiments build: tools/build_variant.sh exp WORKTREE -DCX_EXPERIMENTS)
+# usage on the box: bash tools/_seltrace.sh "EXCHANGE C" ...   (exchange 1 = cluster, 2 = cooperative)
 cd $GRAFT_REPO_ROOT
-for cfg in "2 3" "1 4" "2 4"; do set -- $cfg; CX_SEL_TRACE=1 CX_PKG_ROOT=.variants/exp timeout 120 python -c "
+for cfg in "$@"; do set -- $cfg; CX_SEL_TRACE=1 CX_PKG_ROOT=.variants/exp timeout 120 python -c "
 import torch,sys
 sys.path.insert(0,'.variants/exp')
 from paper_2601_01298_b200 import device as cxd
