@@ -177,7 +177,9 @@ cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* a
 #define CX_SELECT_IMPL_TC 1         /* pinned: an error if the shape does not apply */
 #define CX_SELECT_IMPL_CUDA_CORE 2  /* the CUDA-core filter kernels (select64 / select128) */
 #define CX_OPT_SELECT_EXCHANGE 7    /* tensor-core selection: 0 cost model, 1 thread-block clusters
-                                       (DSMEM), 2 cooperative launch (global-memory exchanges) */
+                                       (DSMEM), 2 cooperative launch (global-memory exchanges),
+                                       3 split: co-resident clusters + a cooperative launch for the
+                                       remaining groups on the free SMs, side by side in one wave */
 #define CX_DECODE_AUTO 0            /* tcgen05, then v2, then the generic kernel */
 #define CX_DECODE_TC 1              /* pinned: an error if the shape does not apply */
 #define CX_DECODE_V2 2

@@ -615,7 +615,7 @@ extern "C" cx_status cx_ctx_set_option(cx_ctx* c, int option, int64_t value) {
             case CX_OPT_DECODE_CTAS_PER_LH: c->opt.decode_ctas_per_lh = in(0, 1 << 16); break;
             case CX_OPT_HOST_UPLOAD_VALUES: c->opt.host_upload_values = in(0, 1); break;
             case CX_OPT_SELECT_IMPL: c->opt.select_impl = in(CX_SELECT_IMPL_AUTO, CX_SELECT_IMPL_CUDA_CORE); break;
-            case CX_OPT_SELECT_EXCHANGE: c->opt.select_exchange = in(0, 2); break;
+            case CX_OPT_SELECT_EXCHANGE: c->opt.select_exchange = in(0, 3); break;
             default: fail(CX_INVALID_ARGUMENT, "ctx_set_option: unknown option");
         }
         if (c->aux) c->aux->opt = c->opt;  // the host path's prologue context follows

@@ -314,6 +314,8 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     unsigned long long* min_gap = &misc[5];
 
     const float* gX = p.X + g * p.gstride + r0 * p.rstride;
+    // a split plan's cooperative part may launch once every CTA of this grid is resident
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     // the CTA's fp32 rows -> L2 (the exact evaluations and the winners' coordinates read them
     // from global memory every round: an L2 hit instead of an HBM round trip)
@@ -879,6 +881,9 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     if (CL) cg::this_cluster().sync();  // no CTA exits while a peer may still push into it
     else __syncthreads();
     if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+    // launched as a programmatic dependent (a split plan's cooperative part): complete only
+    // after the cluster grid has (a no-op for a normally launched grid)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 using SelxKern = void (*)(SelxParams);
@@ -974,10 +979,24 @@ int selx_active(const SelxCfg& c) {
 
 // Cost model (us per round): a fixed part (exchanges, barriers, the exact queue) plus a
 // per-row part, x1.15 for the global-memory exchanges of the cooperative mode; times the
-// waves = ceil(G / co-resident groups).  cfg2 (48 groups of 8192 rows): a cluster of 3 CTAs
-// holds a group on chip (22 tiles) but only 45 clusters of 3 are co-resident (two waves);
-// the cooperative mode places the 144 CTAs anywhere: one wave.
-static bool selx_plan(int G, int64_t L, const Options& o, SelxCfg* out) {
+// waves = ceil(G / co-resident groups).
+//
+// A SPLIT plan runs two launches side by side in one wave: as many groups as are
+// co-resident as thread-block clusters (DSMEM exchanges), and the rest as a cooperative
+// launch on the SMs the clusters leave free (CTAs anywhere, global-memory exchanges).
+// cfg2 (48 groups of 8192 rows): a cluster of 3 CTAs holds a group on chip (22 tiles) and
+// 45 clusters of 3 are co-resident (GPC granularity), leaving 13 SMs: the other 3 groups run
+// as cooperative groups of 4 CTAs.  Measured per round: clusters of 3 17.5K cycles,
+// cooperative 3 CTAs 21.6K (the single-wave alternative), cooperative 4 CTAs ~ the same as
+// clusters of 3 (fewer rows per CTA offset the slower exchanges).
+struct SelxPlan {
+    SelxCfg a;           // groups [0, na): clusters (or the single plan)
+    SelxCfg b;           // groups [na, G): cooperative, concurrently (split plans only)
+    int na = 0;
+    bool split = false;
+};
+
+static bool selx_plan(int G, int64_t L, const Options& o, SelxPlan* out) {
     static int max_optin = -1;
     if (max_optin < 0) {
         int dev = 0;
@@ -986,27 +1005,57 @@ static bool selx_plan(int G, int64_t L, const Options& o, SelxCfg* out) {
             max_optin = 232448;
     }
     const size_t budget = (size_t)max_optin - 1024;
-    double best = 1e300;
-    bool found = false;
+    auto per_round = [](const SelxCfg& c) { return (4.0 + 0.0008 * c.S) * (c.cluster ? 1.0 : 1.15); };
+    // every (mode, C) that fits, with its co-residency
+    std::vector<SelxCfg> cand;
     for (int mode = 0; mode < 2; ++mode) {
         const bool cl = mode == 0;
-        if (o.select_exchange == 1 && !cl) continue;  // pinned: clusters
-        if (o.select_exchange == 2 && cl) continue;   // pinned: cooperative
         for (int c = 1; c <= MAXC; ++c) {
-            if (o.select_cluster > 0 && c != o.select_cluster) continue;
+            if (o.select_cluster > 0 && c != o.select_cluster && o.select_exchange != 3) continue;
             SelxCfg cfg;
             cfg.C = c;
             cfg.cluster = cl;
             if (!selx_shape((int)((L + c - 1) / c), budget, &cfg)) continue;
-            const int act = selx_active(cfg);
-            if (act <= 0) continue;
-            const double per = (4.0 + 0.0008 * cfg.S) * (cl ? 1.0 : 1.15);
-            const double cost = (double)((G + act - 1) / act) * per;
+            cfg.per_wave = selx_active(cfg);
+            if (cfg.per_wave > 0) cand.push_back(cfg);
+        }
+    }
+    double best = 1e300;
+    bool found = false;
+    if (o.select_exchange != 3) {
+        for (const SelxCfg& cfg : cand) {
+            if (o.select_exchange == 1 && !cfg.cluster) continue;  // pinned: clusters
+            if (o.select_exchange == 2 && cfg.cluster) continue;   // pinned: cooperative
+            const double cost = (double)((G + cfg.per_wave - 1) / cfg.per_wave) * per_round(cfg);
             if (cost < best * (1.0 - 1e-9)) {
                 best = cost;
-                cfg.per_wave = act;
-                *out = cfg;
+                out->a = cfg;
+                out->na = G;
+                out->split = false;
                 found = true;
+            }
+        }
+    }
+    // split plans: auto (no pinned exchange / cluster size) or pinned (select_exchange = 3)
+    if (o.select_exchange == 3 || (o.select_exchange == 0 && o.select_cluster == 0)) {
+        const int sms = sm_count();
+        for (const SelxCfg& ca : cand) {
+            // auto: only when the clusters alone would need a second wave; pinned (tests): any
+            // G >= 2 splits, at most G - 1 groups as clusters
+            if (!ca.cluster || G < 2 || (o.select_exchange != 3 && ca.per_wave >= G)) continue;
+            if (o.select_exchange == 3 && o.select_cluster > 0 && ca.C != o.select_cluster) continue;
+            const int na = std::min(ca.per_wave, G - 1), rest = G - na, free_sms = sms - na * ca.C;
+            for (const SelxCfg& cb : cand) {
+                if (cb.cluster || rest * cb.C > free_sms || cb.per_wave < rest) continue;
+                const double cost = std::max(per_round(ca), per_round(cb));
+                if (cost < best * (1.0 - 1e-9)) {
+                    best = cost;
+                    out->a = ca;
+                    out->b = cb;
+                    out->na = na;
+                    out->split = true;
+                    found = true;
+                }
             }
         }
     }
@@ -1025,8 +1074,8 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
     if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 || (reinterpret_cast<uintptr_t>(g.X) & 15) != 0 ||
         g.L < 1)
         return false;
-    SelxCfg cfg;
-    if (!selx_plan(g.G, g.L, o, &cfg)) return false;
+    SelxPlan plan;
+    if (!selx_plan(g.G, g.L, o, &plan)) return false;
     SelxParams prm;
     prm.X = g.X;
     prm.gstride = g.gstride;
@@ -1036,10 +1085,6 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
     prm.cen = cen;
     prm.take = take;
     prm.lambda = lambda;
-    prm.S = cfg.S;
-    prm.n_tiles = cfg.n_tiles;
-    prm.n_smem = cfg.n_smem;
-    prm.n_stage = cfg.n_stage;
     prm.filter = (flags & CX_SELECT_EXACT_ONLY) ? 0 : 1;
     prm.pick_rows = pick_rows;
     prm.pick_scores = pick_scores;
@@ -1047,7 +1092,6 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
     prm.out_scores = scores;
     prm.gaps = gaps;
     prm.trace = nullptr;
-    prm.C = cfg.C;
     prm.x1g = nullptr;
     prm.x2h = nullptr;
     prm.x2c = nullptr;
@@ -1056,53 +1100,93 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
 #endif
-    SelxKern kern = selx_kernel_for(cfg.rpt, cfg.cluster);
-    kernel_smem(kern, cfg.smem, cfg.cluster && cfg.C > 8);
-    // the groups in waves of per_wave (cooperative launches must fit on the GPU at once;
-    // cluster launches are a single grid, the hardware forms the waves)
-    const int wave = cfg.cluster ? g.G : cfg.per_wave;
-    for (int g0 = 0; g0 < g.G; g0 += wave) {
-        const int ng = std::min(wave, g.G - g0);
-        SelxParams pw = prm;
-        pw.X = g.X + (int64_t)g0 * g.gstride;
-        pw.attn = attn + (int64_t)g0 * g.L;
-        pw.cen = cen + (int64_t)g0 * D;
-        pw.pick_rows = pick_rows + (int64_t)g0 * take;
-        pw.pick_scores = pick_scores + (int64_t)g0 * take;
-        pw.out_rows = rows + (int64_t)g0 * take;
-        pw.out_scores = scores + (int64_t)g0 * take;
-        pw.gaps = gaps ? gaps + g0 : nullptr;
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3((unsigned)cfg.C, (unsigned)ng, 1);
-        lc.blockDim = dim3(NT, 1, 1);
-        lc.dynamicSmemBytes = cfg.smem;
-        lc.stream = s;
-        cudaLaunchAttribute attr[1];
-        if (cfg.cluster) {
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = (unsigned)cfg.C;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-        } else {
-            char* sc = reinterpret_cast<char*>(((uintptr_t)scratch + 255) & ~(uintptr_t)255);
-            const size_t slots = (size_t)ng * 2 * cfg.C * NW;
-            pw.x1g = reinterpret_cast<unsigned long long*>(sc);
-            sc += slots * 4 * sizeof(unsigned long long);
-            pw.x2h = reinterpret_cast<Hdr*>(sc);
-            sc += slots * sizeof(Hdr);
-            pw.x2c = reinterpret_cast<float*>(sc);
-            sc += slots * D * sizeof(float);
-            pw.cnt = reinterpret_cast<unsigned*>(sc);
-            CX_CUDA(cudaMemsetAsync(pw.cnt, 0, sizeof(unsigned) * 2 * ng, s));
-            attr[0].id = cudaLaunchAttributeCooperative;
-            attr[0].val.cooperative = 1;
+    // cooperative exchange buffers + counters for ng groups of C CTAs, carved from scr
+    auto coop_scratch = [](void* scr, int ng, int C, SelxParams* pw) {
+        char* sc = reinterpret_cast<char*>(((uintptr_t)scr + 255) & ~(uintptr_t)255);
+        const size_t slots = (size_t)ng * 2 * C * NW;
+        pw->x1g = reinterpret_cast<unsigned long long*>(sc);
+        sc += slots * 4 * sizeof(unsigned long long);
+        pw->x2h = reinterpret_cast<Hdr*>(sc);
+        sc += slots * sizeof(Hdr);
+        pw->x2c = reinterpret_cast<float*>(sc);
+        sc += slots * D * sizeof(float);
+        pw->cnt = reinterpret_cast<unsigned*>(sc);
+    };
+    // one part of the plan: groups [gb, ge) with configuration cfg on stream st
+    auto launch_part = [&](const SelxCfg& cfg, int gb, int ge, cudaStream_t st, void* scr, bool dependent) {
+        SelxParams pp = prm;
+        pp.S = cfg.S;
+        pp.n_tiles = cfg.n_tiles;
+        pp.n_smem = cfg.n_smem;
+        pp.n_stage = cfg.n_stage;
+        pp.C = cfg.C;
+        SelxKern kern = selx_kernel_for(cfg.rpt, cfg.cluster);
+        kernel_smem(kern, cfg.smem, cfg.cluster && cfg.C > 8);
+        // the groups in waves of per_wave (cooperative launches must fit on the GPU at once;
+        // cluster launches are a single grid, the hardware forms the waves)
+        const int wave = cfg.cluster ? ge - gb : cfg.per_wave;
+        for (int g0 = gb; g0 < ge; g0 += wave) {
+            const int ng = std::min(wave, ge - g0);
+            SelxParams pw = pp;
+            pw.X = g.X + (int64_t)g0 * g.gstride;
+            pw.attn = attn + (int64_t)g0 * g.L;
+            pw.cen = cen + (int64_t)g0 * D;
+            pw.pick_rows = pick_rows + (int64_t)g0 * take;
+            pw.pick_scores = pick_scores + (int64_t)g0 * take;
+            pw.out_rows = rows + (int64_t)g0 * take;
+            pw.out_scores = scores + (int64_t)g0 * take;
+            pw.gaps = gaps ? gaps + g0 : nullptr;
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)cfg.C, (unsigned)ng, 1);
+            lc.blockDim = dim3(NT, 1, 1);
+            lc.dynamicSmemBytes = cfg.smem;
+            lc.stream = st;
+            cudaLaunchAttribute attr[2];
+            if (cfg.cluster) {
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = (unsigned)cfg.C;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+            } else {
+                coop_scratch(scr, ng, cfg.C, &pw);
+                // (a dependent part's counters were cleared before its primary: a memset
+                // between the two launches would serialise them)
+                if (!dependent) CX_CUDA(cudaMemsetAsync(pw.cnt, 0, sizeof(unsigned) * 2 * ng, st));
+                // a dependent part is a plain grid: a cooperative launch ignores programmatic
+                // serialisation (measured: it ran after the cluster grid).  Its ng * C CTAs fit
+                // in the SMs the clusters leave free; were one not resident, its group would
+                // only wait for the cluster grid to retire (that grid never waits on them)
+                attr[0].id = cudaLaunchAttributeCooperative;
+                attr[0].val.cooperative = dependent ? 0 : 1;
+            }
+            int na = 1;
+            if (dependent) {
+                attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[na].val.programmaticStreamSerializationAllowed = 1;
+                ++na;
+            }
+            lc.attrs = attr;
+            lc.numAttrs = na;
+            CX_CUDA(cudaLaunchKernelEx(&lc, kern, pw));
+            count_launch();
         }
-        lc.attrs = attr;
-        lc.numAttrs = 1;
-        CX_CUDA(cudaLaunchKernelEx(&lc, kern, pw));
-        count_launch();
+    };
+    if (!plan.split) {
+        launch_part(plan.a, 0, g.G, s, scratch, false);
+    } else {
+        // both parts on s: the cooperative part is a programmatic dependent launch, released
+        // once EVERY cluster CTA is resident (each executes griddepcontrol.launch_dependents
+        // first), so the clusters take whole GPCs and the cooperative CTAs fill the SMs they
+        // leave; it waits for the cluster grid (griddepcontrol.wait) before it exits, so the
+        // next launch on s sees both parts complete
+        SelxParams pb = prm;
+        coop_scratch(scratch, g.G - plan.na, plan.b.C, &pb);
+        CX_CUDA(cudaMemsetAsync(pb.cnt, 0, sizeof(unsigned) * 2 * (g.G - plan.na), s));
+        launch_part(plan.a, 0, plan.na, s, scratch, false);
+        launch_part(plan.b, plan.na, g.G, s, scratch, true);
     }
 #ifdef CX_EXPERIMENTS
+    const SelxCfg& cfg = plan.a;  // (a split plan traces group 0 of both parts into one buffer)
     if (prm.trace) {  // average cycles per phase over rounds 2 .. take-2
         CX_CUDA(cudaStreamSynchronize(s));
         double acc[10] = {0};
@@ -1131,9 +1215,9 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
 }
 
 int select_tc_wave(int64_t L, int G) {
-    SelxCfg cfg;
+    SelxPlan plan;
     Options o;
-    return selx_plan(G, L, o, &cfg) ? cfg.per_wave : 0;
+    return selx_plan(G, L, o, &plan) ? (plan.split ? G : plan.a.per_wave) : 0;
 }
 
 }  // namespace cx

@@ -30,9 +30,11 @@ def _threads():
     return max(1, os.cpu_count() or 1)
 
 
-@pytest.mark.parametrize("seed,exchange", [(3, 0), (2026, 0), (11, 1)], ids=["auto", "auto2", "clusters"])
+@pytest.mark.parametrize("seed,exchange", [(3, 0), (2026, 0), (11, 1), (12, 2)], ids=["auto", "auto2", "clusters", "coop"])
 def test_cfg2_all_groups_vs_oracle(orc, cx_option, seed, exchange):
-    """exchange 0: the cost model (cfg2: the cooperative one-wave launch); 1: thread-block clusters."""
+    """exchange 0: the cost model (cfg2: the split one-wave plan -- 45 clusters of 3 beside a
+    cooperative launch of 3 groups x 4 CTAs); 1: thread-block clusters (two waves);
+    2: the cooperative launch alone (one wave of 48 x 3 CTAs)."""
     import torch
 
     from paper_2601_01298_b200 import device

@@ -79,7 +79,7 @@ def test_grouped_compress_random_sweep(dev, orc, seed):
             assert seed % 3 == 0 and gaps[gi] == 0.0, (seed, gi, float(gaps[gi]))
 
 
-@pytest.mark.parametrize("impl", ["cuda_core", "tc_cluster", "tc_coop"])
+@pytest.mark.parametrize("impl", ["cuda_core", "tc_cluster", "tc_coop", "tc_split"])
 @pytest.mark.parametrize("seed", list(range(12)))
 def test_grouped_compress_forced_row_modes(dev, orc, cx_option, seed, impl):
     """The same check with the cluster size forced small (CX_OPT_SELECT_CLUSTER): for the CUDA-core
@@ -91,7 +91,7 @@ def test_grouped_compress_forced_row_modes(dev, orc, cx_option, seed, impl):
         cx_option("select_impl", "cuda_core")
     else:
         cx_option("select_impl", "tc")
-        cx_option("select_exchange", 1 if impl == "tc_cluster" else 2)
+        cx_option("select_exchange", {"tc_cluster": 1, "tc_coop": 2, "tc_split": 3}[impl])
     rs = np.random.default_rng(500 + seed)
     d = int(rs.choice([64, 64, 128]))
     C = int(rs.integers(2, 7))
