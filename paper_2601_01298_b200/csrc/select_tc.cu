@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         // within GAP_WINDOW of its approximate maximum with the reference's exact divisions,
         // and takes its exact (score desc, row asc) argmax with shuffles.  X2 then carries
         // every warp's candidate to every CTA: no block-level barrier in H.
+        XSTAMP(10);
         const bool a_span = amax > amin, c_span = cmax > cmin;
         const double ar = __dsub_rn(amax, amin), cr = __dsub_rn(cmax, cmin);
         const double iar = a_span ? __drcp_rn(ar) : 0.0, icr = c_span ? __drcp_rn(cr) : 0.0;
@@ -700,6 +701,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             spec4 = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)spec_li * p.rstride) + lane);
         const bool approx_ok = (!a_span || ar >= 1e-290) && (!c_span || cr >= 1e-290);
         const double cut = approx_ok ? bitsd(wkey) - GAP_WINDOW : -INFINITY;
+        XSTAMP(11);
         // exact hybrid of the rows within the window; per lane: best (score desc, row asc)
         // and runner-up
         unsigned long long bkey = 0ull, rkey = 0ull;
@@ -721,6 +723,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                 has_r = true;
             }
         }
+        XSTAMP(12);
         // the warp's exact winner: max score, then the lowest row among equal scores
         const unsigned long long wbest = wmax64(has_b ? bkey : 0ull);
         const bool cand_b = has_b && bkey == wbest;
@@ -1189,7 +1192,7 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
     const SelxCfg& cfg = plan.a;  // (a split plan traces group 0 of both parts into one buffer)
     if (prm.trace) {  // average cycles per phase over rounds 2 .. take-2
         CX_CUDA(cudaStreamSynchronize(s));
-        double acc[10] = {0};
+        double acc[10] = {0}, hacc[3] = {0};
         int n = 0;
         for (int r = 2; r < std::min(take, 4096) - 1; ++r, ++n) {
             const long long* t = prm.trace + r * 16;
@@ -1202,12 +1205,18 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
             acc[6] += (double)(t[6] - t[5]);  // X2
             acc[7] += (double)(prm.trace[(r + 1) * 16] - t[0]);
             acc[8] += (double)t[8];
+            acc[9] += (double)(t[10] - t[4]);   // H: X1 values -> min/max
+            hacc[0] += (double)(t[11] - t[10]); // H: approximate ranking + winner-row prefetch issue
+            hacc[1] += (double)(t[12] - t[11]); // H: exact window
+            hacc[2] += (double)(t[5] - t[12]);  // H: warp winner / runner-up
         }
         if (n > 0)
             fprintf(stderr, "select_tc %s C=%d (co-resident %d) S=%d tiles=%d (smem %d) cycles/round: mma=%.0f bound+queue=%.0f exact=%.0f "
                             "X1loc=%.0f X1wait=%.0f H=%.0f X2=%.0f total=%.0f queued=%.1f\n",
                     cfg.cluster ? "cluster" : "cooperative", cfg.C, cfg.per_wave, cfg.S, cfg.n_tiles, cfg.n_smem, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n,
                     acc[5] / n, acc[6] / n, acc[7] / n, acc[8] / n);
+            fprintf(stderr, "  H split: minmax=%.0f rank=%.0f exact=%.0f winner=%.0f\n", acc[9] / n, hacc[0] / n,
+                    hacc[1] / n, hacc[2] / n);
         cudaFree(prm.trace);
     }
 #endif
