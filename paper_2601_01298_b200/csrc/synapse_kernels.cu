@@ -213,12 +213,12 @@ __global__ void __launch_bounds__(32) centroid_pipe_kernel(GroupView gv, double*
 }
 
 // The same sum with the rows streamed by TMA bulk copies: one CTA per group, one thread
-// per coordinate; a ring of stages of 32 contiguous rows (rstride == dim), ONE
+// per coordinate; a ring of stages of kTmaRows contiguous rows (rstride == dim), ONE
 // cp.async.bulk per stage completing on the stage's mbarrier (per-row copies measured
 // 2.5x slower than the cp.async ring: small TMA requests are expensive).  ~128 KB of rows in flight per SM keeps the loads
 // ahead of the only serial cost, the fp64 add chain (L x ~8.4 cycles).
-constexpr int kTmaRows = 32;
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int kTmaRows>
 __global__ void __launch_bounds__(256) centroid_tma_kernel(GroupView gv, double* __restrict__ cen, int n_stages) {
     extern __shared__ __align__(128) unsigned char csm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(csm);  // [n_stages]
@@ -233,8 +233,7 @@ __global__ void __launch_bounds__(256) centroid_tma_kernel(GroupView gv, double*
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto issue = [&](int64_t st) {  // thread 0: the stage's rows are contiguous (rstride == dim)
-        const int slot = (int)(st % n_stages);
+    auto issue = [&](int64_t st, int slot) {  // thread 0: the stage's rows are contiguous (rstride == dim)
         const int64_t r0 = st * kTmaRows;
         const uint32_t bytes = row_bytes * (uint32_t)min((int64_t)kTmaRows, gv.L - r0);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + slot)), "r"(bytes)
@@ -246,11 +245,13 @@ __global__ void __launch_bounds__(256) centroid_tma_kernel(GroupView gv, double*
             : "memory");
     };
     if (j == 0)
-        for (int64_t st = 0; st < min((int64_t)n_stages, nst); ++st) issue(st);
+        for (int64_t st = 0; st < min((int64_t)n_stages, nst); ++st) issue(st, (int)st);
     double acc = 0.0;
+    // slot and phase parity advance incrementally (a 64-bit % and / per stage cost more than
+    // the stage's 32 adds)
+    int slot = 0;
+    uint32_t par = 0;
     for (int64_t st = 0; st < nst; ++st) {
-        const int slot = (int)(st % n_stages);
-        const uint32_t par = (uint32_t)((st / n_stages) & 1);
         uint32_t ok = 0;
         do {
             asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
@@ -267,7 +268,11 @@ __global__ void __launch_bounds__(256) centroid_tma_kernel(GroupView gv, double*
             for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, (double)buf[r * dim + j]);
         }
         __syncthreads();  // every thread is done with the slot
-        if (j == 0 && st + n_stages < nst) issue(st + n_stages);
+        if (j == 0 && st + n_stages < nst) issue(st + n_stages, slot);
+        if (++slot == n_stages) {
+            slot = 0;
+            par ^= 1u;
+        }
     }
     cen[(int64_t)g * dim + j] = __ddiv_rn(acc, (double)gv.L);
 }
@@ -654,19 +659,24 @@ __global__ void __launch_bounds__(512, 1) select_kernel(SelectParams p) {
 // floats apart (take * dim when dense; the decode layout [layer][kv head][k][d] otherwise)
 __global__ void gather_rows_kernel(GroupView gv, const float* __restrict__ src0, const float* __restrict__ src1,
                                    const int64_t* __restrict__ rows, int take, float* __restrict__ dst0,
-                                   float* __restrict__ dst1, int64_t dst_gstride) {
+                                   float* __restrict__ dst1, int64_t dst_gstride, int rpb) {
     const int g = blockIdx.y;
-    const int s = blockIdx.x;
     const float* src = blockIdx.z ? src1 : src0;
     float* dst = blockIdx.z ? dst1 : dst0;
+    // rpb rows per block, tpr = blockDim.x / rpb threads per row (one 16-B chunk each when
+    // dim % 4 == 0): every row of a group's selection is in flight at once (one thread-block
+    // per row left 3/4 of each block idle and took ~3 waves of blocks: 11 us for cfg2)
+    const int tpr = (int)blockDim.x / rpb;
+    const int s = (int)blockIdx.x * rpb + (int)threadIdx.x / tpr, t = (int)threadIdx.x % tpr;
+    if (s >= take) return;
     const int64_t r = rows[(int64_t)g * take + s];
     const float* in = src + g * gv.gstride + r * gv.rstride;
     float* out = dst + (int64_t)g * dst_gstride + (int64_t)s * gv.dim;
     if ((gv.dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
-        for (int c = threadIdx.x; c < gv.dim / 4; c += blockDim.x)
+        for (int c = t; c < gv.dim / 4; c += tpr)
             reinterpret_cast<float4*>(out)[c] = __ldg(reinterpret_cast<const float4*>(in) + c);
     } else {
-        for (int c = threadIdx.x; c < gv.dim; c += blockDim.x) out[c] = __ldg(in + c);
+        for (int c = t; c < gv.dim; c += tpr) out[c] = __ldg(in + c);
     }
 }
 
@@ -889,11 +899,21 @@ void centroid_launch(const GroupView& g, double* cen, cudaStream_t s) {
     if (g.dim > 1024) fail(CX_DEVICE_ERROR, "select: dim > 1024 unsupported");
     if (g.dim % 4 == 0 && g.dim <= 256 && g.rstride == g.dim && (g.gstride & 3) == 0 &&
         (reinterpret_cast<uintptr_t>(g.X) & 15) == 0) {
-        const size_t stage_bytes = (size_t)kTmaRows * g.dim * sizeof(float);
+        // 128-row stages when rows are <= 256 B: every stage boundary costs ~200 cycles (mbarrier
+        // wait, refilling the load -> widen pipeline, the block barrier, the refill issue), so
+        // longer stages amortise it (32-row stages: 142 -> 110 us after removing a 64-bit % and
+        // / per stage; see tools/cen_micro.cu)
+        const int rows = g.dim <= 64 ? 128 : 32;
+        const size_t stage_bytes = (size_t)rows * g.dim * sizeof(float);
         const int n_stages = (int)std::max<size_t>(2, std::min<size_t>(16, (160 * 1024) / stage_bytes));
         const size_t smem = 128 * (((size_t)n_stages * 8 + 127) / 128) + (size_t)n_stages * stage_bytes;
-        kernel_smem(centroid_tma_kernel, smem);
-        centroid_tma_kernel<<<(unsigned)g.G, (unsigned)g.dim, smem, s>>>(g, cen, n_stages);
+        if (rows == 128) {
+            kernel_smem(centroid_tma_kernel<128>, smem);
+            centroid_tma_kernel<128><<<(unsigned)g.G, (unsigned)g.dim, smem, s>>>(g, cen, n_stages);
+        } else {
+            kernel_smem(centroid_tma_kernel<32>, smem);
+            centroid_tma_kernel<32><<<(unsigned)g.G, (unsigned)g.dim, smem, s>>>(g, cen, n_stages);
+        }
         check_launch("centroid_tma_kernel");
     } else if (g.dim % 32 == 0 && (g.rstride & 3) == 0 && (g.gstride & 3) == 0 &&
         (reinterpret_cast<uintptr_t>(g.X) & 15) == 0) {
@@ -987,8 +1007,12 @@ void gather_rows(const GroupView& g, const float* src, const int64_t* rows, int 
 void gather_rows2(const GroupView& g, const float* src0, const float* src1, const int64_t* rows, int take, float* dst0,
                   float* dst1, int64_t dst_gstride, cudaStream_t s) {
     if (take <= 0 || g.G <= 0) return;
-    gather_rows_kernel<<<dim3((unsigned)take, (unsigned)g.G, src1 ? 2u : 1u), 64, 0, s>>>(g, src0, src1, rows, take, dst0,
-                                                                                       dst1, dst_gstride);
+    // several rows per 256-thread block when a row is <= 64 chunks of 16 B (dim <= 256, % 4)
+    const bool multi = (g.dim & 3) == 0 && g.dim <= 256 && take > 1;
+    const int rpb = multi ? 256 / (g.dim / 4) : 1;
+    const unsigned gx = multi ? (unsigned)((take + rpb - 1) / rpb) : (unsigned)take;
+    gather_rows_kernel<<<dim3(gx, (unsigned)g.G, src1 ? 2u : 1u), multi ? 256 : 64, 0, s>>>(g, src0, src1, rows, take,
+                                                                                          dst0, dst1, dst_gstride, rpb);
     check_launch("gather_rows_kernel");
 }
 
