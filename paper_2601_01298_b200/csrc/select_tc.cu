@@ -536,6 +536,15 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                         const int li = (quad + 4 * k) * TILE + 32 * sub + lane;
                         qrow[sl] = li;
                         need &= ~(1u << k);
+#ifndef CX_SEL_NO_QPREFETCH
+                        // the evaluator thread reads this row after the block barrier: start
+                        // its two 128-B lines towards L1 now (the L2 / HBM latency overlaps
+                        // the rest of the bound pass and the barrier)
+                        {
+                            const float* rp = gX + (int64_t)li * p.rstride;
+                            asm volatile("prefetch.global.L1 [%0];\n\tprefetch.global.L1 [%1];" ::"l"(rp), "l"(rp + 32));
+                        }
+#endif
                         if (sl < p.n_stage) {  // the row starts moving now (TMA), not after the barrier
                             mbar_expect_tx(&mbar[4], D * sizeof(float));
                             bulk_g2s(stage + sl * D, gX + (int64_t)li * p.rstride, D * sizeof(float), &mbar[4]);
