@@ -44,14 +44,26 @@ constexpr int NT = 512;
 constexpr int NW = NT / 32;
 constexpr int TILE = 128;         // rows per MMA (M)
 constexpr int MAXT = 22;          // tiles per CTA: 2816 rows
-constexpr int DC = 8;             // TMEM columns of one tile's D (N = 8)
+constexpr int DC = 8;             // TMEM columns of one D block (N = 8)
+// D packing: the 4 tiles of a block share one 8-column D block; tile q of the block multiplies
+// B operand q = [0 ... b_hi b_lo (columns 2q, 2q+1) ... 0], so its two dots land in columns
+// 2q, 2q+1 and the other tiles add exact zeros there.  One warp issues a block's 4 tiles in
+// order (the first MMA overwrites, the rest accumulate).  D then takes 8 columns per 4 tiles
+// instead of per tile, and TMEM holds 14 row tiles instead of 10 at 22 tiles (fewer A reads
+// from shared memory: an SS MMA moves 4 KB through shared memory, a TS one none)
+#ifndef CX_SEL_NO_DPACK
+constexpr int DPACK = 4;
+#else
+constexpr int DPACK = 1;
+#endif
 constexpr int MAXC = 16;
 constexpr int TILE_BYTES = TILE * D * 2;  // one fp16 A tile: 16 KB
 constexpr double GAP_WINDOW = 1e-10;      // as select64.cu (gap monitor + exact window)
 static_assert(MAXC == kGapRecStride, "gap-monitor record stride");
-static_assert(MAXT * DC <= 512 - 32 * 10, "D and 10 row tiles fill TMEM at 22 tiles");
-// first TMEM column of the row tiles: after the tiles' D columns (8 per tile)
-__host__ __device__ inline int tm_rows_col(int n_tiles) { return (DC * n_tiles + 31) / 32 * 32; }
+static_assert((MAXT + DPACK - 1) / DPACK * DC <= 512 - 32 * 10, "D and 10 row tiles fill TMEM at 22 tiles");
+// first TMEM column of the row tiles: after the D blocks (8 columns per DPACK tiles)
+__host__ __device__ inline int tm_rows_col(int n_tiles) { return (DC * ((n_tiles + DPACK - 1) / DPACK) + 31) / 32 * 32; }
+__host__ __device__ inline int n_dblocks(int n_tiles) { return (n_tiles + DPACK - 1) / DPACK; }
 
 __device__ __forceinline__ double dmin_std(double a, double b) { return (b < a) ? b : a; }
 // Every value reduced below is a non-negative double (attention mass, distances, hybrid
@@ -271,7 +283,7 @@ __host__ __device__ inline SelxLayout selx_layout(int n_smem, int C, int n_stage
     l.misc = o;  o = al(o + sizeof(unsigned long long) * 8);
     l.qrow = o;  o = al(o + sizeof(int) * NT);         // exact-evaluation queue: local row
     l.qres = o;  o = al(o + sizeof(double) * 2 * NT);  // ... and its (d^2, d)
-    l.bop = o;   o = al(o + 8 * D * 2, 1024);  // B operand: 8 rows (b_hi, b_lo, 0...) x 64 fp16
+    l.bop = o;   o = al(o + DPACK * 8 * D * 2, 1024);  // DPACK B operands: 8 rows (b_hi, b_lo at 2q, 2q+1; 0...) x 64 fp16
     l.stage = o; o = al(o + (size_t)n_stage * D * sizeof(float), 1024);  // exact rows (fp32)
     l.tiles = o; o = al(o + (size_t)n_smem * TILE_BYTES, 1024);
     l.total = o;
@@ -330,7 +342,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tbase_s)), "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    for (int e = tid; e < 8 * D * 2 / 16; e += NT) reinterpret_cast<uint4*>(bop)[e] = make_uint4(0, 0, 0, 0);
+    for (int e = tid; e < DPACK * 8 * D * 2 / 16; e += NT) reinterpret_cast<uint4*>(bop)[e] = make_uint4(0, 0, 0, 0);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     if (tid == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
-        mbar_init(&mbar[2], (uint32_t)min(p.n_tiles, NW));  // one commit per MMA-issuing warp
+        mbar_init(&mbar[2], (uint32_t)min(n_dblocks(p.n_tiles), NW));  // one commit per MMA-issuing warp
         mbar_init(&mbar[4], 1);  // the exact rows' bulk copies (tx bytes) + one arrival
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         *qn = 0;
@@ -453,9 +465,8 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
     const uint32_t idesc = idesc_f16_f32(TILE, 8);
     // MMA operands that never change: B descriptors per k-step, the A descriptor of shared tile 0,
     // the first TMEM column of the row tiles
-    uint64_t bdesc[D / 16];
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) bdesc[kk] = sdesc(su32(bop) + kk * 2 * 128, 128, 128);
+    // B descriptor of operand q, k-step kk: bdesc0 + ((q * 1024 + kk * 256) >> 4) (address field)
+    const uint64_t bdesc0 = sdesc(su32(bop), 128, 128);
     const uint64_t adesc0 = sdesc(su32(tiles), (TILE / 8) * 128, 128);
     const uint32_t tm_col = (uint32_t)tm_rows_col(p.n_tiles);
 
@@ -472,29 +483,39 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                     const float bcv = bw[tid];
                     const __half hi = __float2half_rn(bcv);
                     const __half lo = __float2half_rn(bcv - __half2float(hi));
-                    *reinterpret_cast<__half*>(bop + cm_off(0, tid, 8)) = hi;
-                    *reinterpret_cast<__half*>(bop + cm_off(1, tid, 8)) = lo;
+#pragma unroll
+                    for (int q = 0; q < DPACK; ++q) {
+                        *reinterpret_cast<__half*>(bop + q * 8 * D * 2 + cm_off(2 * q % 8, tid, 8)) = hi;
+                        *reinterpret_cast<__half*>(bop + q * 8 * D * 2 + cm_off((2 * q + 1) % 8, tid, 8)) = lo;
+                    }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
                 __syncthreads();  // the B operand is written
-                // The filter GEMV.  A tcgen05.mma costs its issuing thread ~200 cycles at this
-                // size (descriptors to uniform registers), so lane 0 of EVERY warp issues the
-                // MMAs of tiles w, w + 16 (k-step major), and commits: the mbarrier counts one
-                // arrival per issuing warp.
-                if (wid < p.n_tiles) {  // warp-uniform: tiles wid, wid + NW, k-step major per tile
+                // The filter GEMV: lane 0 of warp w issues D block w's tiles 4w .. 4w + 3 in order
+                // (k-step major per tile; the block's first MMA overwrites, the rest accumulate)
+                // and commits: the mbarrier counts one arrival per issuing warp.
+                if (wid < n_dblocks(p.n_tiles)) {  // warp-uniform: blocks wid, wid + NW, ...
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    for (int j = wid; j < p.n_tiles; j += NW) {
-                        const uint32_t dt = tbase + (uint32_t)(DC * j);
+                    for (int blk = wid; blk < n_dblocks(p.n_tiles); blk += NW) {
+                    const uint32_t dt = tbase + (uint32_t)(DC * blk);
+#pragma unroll
+                    for (int q = 0; q < DPACK; ++q) {
+                        const int j = DPACK * blk + q;
+                        if (j >= p.n_tiles) break;
+                        const uint64_t bq = bdesc0 + (uint64_t)((q * 8 * D * 2) >> 4);
                         if (j >= p.n_smem) {
                             const uint32_t at = tbase + (uint32_t)(tm_col + 32 * (j - p.n_smem));
 #pragma unroll
-                            for (int kk = 0; kk < D / 16; ++kk) mma_ts_elect(dt, at + 8 * kk, bdesc[kk], idesc, kk);
+                            for (int kk = 0; kk < D / 16; ++kk)
+                                mma_ts_elect(dt, at + 8 * kk, bq + (uint64_t)((kk * 2 * 128) >> 4), idesc, q | kk);
                         } else {
                             const uint64_t ad = adesc0 + (uint64_t)((j * TILE_BYTES) >> 4);
 #pragma unroll
                             for (int kk = 0; kk < D / 16; ++kk)
-                                mma_ss_elect(dt, ad + (uint64_t)((kk * 2 * (TILE / 8) * 128) >> 4), bdesc[kk], idesc, kk);
+                                mma_ss_elect(dt, ad + (uint64_t)((kk * 2 * (TILE / 8) * 128) >> 4),
+                                             bq + (uint64_t)((kk * 2 * 128) >> 4), idesc, q | kk);
                         }
+                    }
                     }
                     mma_commit_elect(&mbar[2]);
                 }
@@ -510,7 +531,9 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                 for (int k = 0; k < RPT; ++k) {
                     const int j = quad + 4 * k;
                     dh[k] = dl[k] = 0u;
-                    if (j < p.n_tiles) tmem_ld2(tbase + ((uint32_t)(32 * sub) << 16) + (uint32_t)(DC * j), dh[k], dl[k]);
+                    if (j < p.n_tiles)
+                        tmem_ld2(tbase + ((uint32_t)(32 * sub) << 16) + (uint32_t)(DC * (j / DPACK) + 2 * (j % DPACK)), dh[k],
+                                 dl[k]);
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
