@@ -424,11 +424,47 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         mbar_arrive_expect(&mbar[0], tx1);
         mbar_arrive_expect(&mbar[1], tx2);
     }
-    // Cooperative mode.  Every warp writes its slot, then bumps the group's counter with a
-    // release add; one poller per CTA (thread 0) acquires the count, then ONE TMA bulk copy
-    // brings the whole exchange into shared memory, completing on the same mbarrier the
-    // cluster pushes would.  (Polling self-stamped words instead measured slower: ~4K vs ~3K
-    // cycles per exchange, cross-die L2 round trips.)
+    // Cooperative mode (CX_SEL_COOP_COUNTER: the previous protocol, kept for A/B).  Warp 0
+    // writes the CTA's slot, then bumps the group's counter with a release add; one poller per
+    // CTA (thread 0) acquires the count, then ONE TMA bulk copy brings the whole exchange into
+    // shared memory, completing on the same mbarrier the cluster pushes would.  The default
+    // stamped protocol below needs one L2 round trip instead of three: cooperative round
+    // 19.1K -> 16.0K cycles (4 CTAs), cfg2 compression 1.81 -> 1.70 ms.
+#ifndef CX_SEL_COOP_COUNTER
+    // Stamped exchange (the default).  Every 64-bit word of a slot carries the round's stamp in
+    // bit 63 (all payload words are non-negative double bit patterns or row indices, so the bit
+    // is free): stamp = 1 - ((round >> 1) & 1), the slots are zeroed per launch, and each slot
+    // buffer (round parity) is rewritten only two rounds later, after every CTA has read it.
+    // A writer stores its words relaxed -- no fence, no counter -- and warp 0 of every CTA
+    // polls the C slots' words until all carry this round's stamp: one L2 round trip after the
+    // last writer, instead of fence + counter add + counter poll + bulk copy.
+    constexpr unsigned long long TOPB = 1ull << 63;
+    constexpr unsigned long long SENT = 0x7FF8000000000001ull;  // encodes -1.0 (no candidate)
+    auto stamp_of = [](int round_) { return (unsigned long long)(1 - ((round_ >> 1) & 1)) << 63; };
+    auto st_word = [](unsigned long long* a, unsigned long long v) {
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+    };
+    auto ld_word = [](const unsigned long long* a) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+        return v;
+    };
+    // warp 0: the C slots' 4 C words of this round -> out[0 .. 4C) with the stamps removed
+    auto poll_slots = [&](const unsigned long long* slots, int round_, unsigned long long* out) {
+        const unsigned long long want = stamp_of(round_);
+        const int nwd = 4 * (int)C;
+        unsigned long long v0, v1;
+        bool ok;
+        do {
+            v0 = lane < nwd ? ld_word(slots + lane) : want;
+            v1 = lane + 32 < nwd ? ld_word(slots + lane + 32) : want;
+            ok = (v0 & TOPB) == want && (v1 & TOPB) == want;
+        } while (!__all_sync(0xffffffffu, ok));
+        if (lane < nwd) out[lane] = v0 & ~TOPB;
+        if (lane + 32 < nwd) out[lane + 32] = v1 & ~TOPB;
+    };
+#endif
+#ifdef CX_SEL_COOP_COUNTER
     auto bump = [&](int which) {  // after warp 0's slot writes
         __syncwarp();
         if (lane == 0) {
@@ -454,6 +490,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             bulk_g2s(bc, p.x2c + (size_t)(2 * g + par) * C * D, C * D * (uint32_t)sizeof(float), &mbar[1]);
         }
     };
+#endif
 
     const double lam = p.lambda;
     const double one_m_lam = __dsub_rn(1.0, lam);
@@ -670,6 +707,16 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                     const unsigned long long c1 = wmax64(lane < NW ? loc1[4 * lane + 1] : 0ull);
                     const unsigned long long c2 = wmin64(lane < NW ? loc1[4 * lane + 2] : BITS_INF);
                     const unsigned long long c3 = wmax64(lane < NW ? loc1[4 * lane + 3] : 0ull);
+#ifndef CX_SEL_COOP_COUNTER
+                    unsigned long long* sl = p.x1g + (size_t)(2 * g + (round & 1)) * C * 4;
+                    if (lane < 4) {
+                        const unsigned long long v = lane == 0 ? c0 : lane == 1 ? c1 : lane == 2 ? c2 : c3;
+                        st_word(sl + rank * 4 + lane, v | stamp_of(round));
+                    }
+                    poll_slots(sl, round, reinterpret_cast<unsigned long long*>(mm));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&mbar[0]);  // mm is written: the other warps may read it
+#else
                     if (lane == 0) {
                         unsigned long long* d = p.x1g + ((size_t)(2 * g + (round & 1)) * C + rank) * 4;
                         reinterpret_cast<ulonglong2*>(d)[0] = make_ulonglong2(c0, c1);
@@ -677,6 +724,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                     }
                     bump(0);
                     gather(0, round, C * 32u);
+#endif
                 }
             }
             XSTAMP(9);
@@ -821,6 +869,43 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                            : 0ull;
                     const unsigned long long r2b = wmax64(rb);
                     const bool any2 = __ballot_sync(0xffffffffu, hr) != 0u;
+#ifndef CX_SEL_COOP_COUNTER
+                    // header words: score / runner-up (>= 0, or SENT for -1), row, |b|^2; the
+                    // coordinates are not exchanged: every CTA reads the C candidates' rows from
+                    // the cloud itself (read-only, L2) once the headers are in
+                    unsigned long long* sl = reinterpret_cast<unsigned long long*>(p.x2h + (size_t)(2 * g + (round & 1)) * C);
+                    if (lane < 4) {
+                        const double hs = any ? locH[wsl].score : -1.0;
+                        const double h2 = any2 ? bitsd(r2b) : -1.0;
+                        unsigned long long v;
+                        if (lane == 0) v = hs < 0.0 ? SENT : dbits(hs);
+                        else if (lane == 1) v = (unsigned long long)(any ? locH[wsl].row : LLONG_MAX);
+                        else if (lane == 2) v = dbits(locH[wsl].nb);
+                        else v = h2 < 0.0 ? SENT : dbits(h2);
+                        st_word(sl + rank * 4 + lane, v | stamp_of(round));
+                    }
+                    unsigned long long* hw = reinterpret_cast<unsigned long long*>(hdr);
+                    poll_slots(sl, round, hw);
+                    __syncwarp();
+                    if (lane < (int)C) {  // decode the sentinels
+                        if (hw[4 * lane] == SENT) hdr[lane].score = -1.0;
+                        if (hw[4 * lane + 3] == SENT) hdr[lane].second = -1.0;
+                    }
+                    __syncwarp();
+                    // the candidates' coordinates: this CTA's own from locC, the others' rows from
+                    // the cloud (C x 16 float4, two per lane up to C = 4)
+                    for (int e4 = lane; e4 < (int)C * (D / 4); e4 += 32) {
+                        const int e = e4 / (D / 4), c4 = e4 % (D / 4);
+                        const long long rw = hdr[e].row;
+                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (e == (int)rank) v = reinterpret_cast<const float4*>(locC + wsl * D)[c4];
+                        else if (rw != LLONG_MAX)
+                            v = __ldg(reinterpret_cast<const float4*>(p.X + g * p.gstride + rw * p.rstride) + c4);
+                        reinterpret_cast<float4*>(bc + e * D)[c4] = v;
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&mbar[1]);
+#else
                     const size_t base = (size_t)(2 * g + (round & 1)) * C + rank;
                     if (lane == 0) {
                         Hdr h;
@@ -834,6 +919,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                         reinterpret_cast<float4*>(p.x2c + base * D)[lane] = reinterpret_cast<const float4*>(locC + wsl * D)[lane];
                     bump(1);
                     gather(1, round, C * (uint32_t)(sizeof(Hdr) + D * sizeof(float)));
+#endif
                 }
             }
         }
@@ -1147,6 +1233,13 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
         sc += slots * D * sizeof(float);
         pw->cnt = reinterpret_cast<unsigned*>(sc);
     };
+    // per launch: the exchange counters (counter protocol) or the stamped slots (zero = no
+    // round's stamp yet) of ng groups of C CTAs
+    auto coop_clear = [](const SelxParams& pw, int ng, int C, cudaStream_t st) {
+        CX_CUDA(cudaMemsetAsync(pw.cnt, 0, sizeof(unsigned) * 2 * ng, st));
+        CX_CUDA(cudaMemsetAsync(pw.x1g, 0, sizeof(unsigned long long) * 4 * 2 * (size_t)ng * C, st));
+        CX_CUDA(cudaMemsetAsync(pw.x2h, 0, sizeof(Hdr) * 2 * (size_t)ng * C, st));
+    };
     // one part of the plan: groups [gb, ge) with configuration cfg on stream st
     auto launch_part = [&](const SelxCfg& cfg, int gb, int ge, cudaStream_t st, void* scr, bool dependent) {
         SelxParams pp = prm;
@@ -1186,7 +1279,7 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
                 coop_scratch(scr, ng, cfg.C, &pw);
                 // (a dependent part's counters were cleared before its primary: a memset
                 // between the two launches would serialise them)
-                if (!dependent) CX_CUDA(cudaMemsetAsync(pw.cnt, 0, sizeof(unsigned) * 2 * ng, st));
+                if (!dependent) coop_clear(pw, ng, cfg.C, st);
                 // a dependent part is a plain grid: a cooperative launch ignores programmatic
                 // serialisation (measured: it ran after the cluster grid).  Its ng * C CTAs fit
                 // in the SMs the clusters leave free; were one not resident, its group would
@@ -1216,7 +1309,7 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
         // next launch on s sees both parts complete
         SelxParams pb = prm;
         coop_scratch(scratch, g.G - plan.na, plan.b.C, &pb);
-        CX_CUDA(cudaMemsetAsync(pb.cnt, 0, sizeof(unsigned) * 2 * (g.G - plan.na), s));
+        coop_clear(pb, g.G - plan.na, plan.b.C, s);
         launch_part(plan.a, 0, plan.na, s, scratch, false);
         launch_part(plan.b, plan.na, g.G, s, scratch, true);
     }
