@@ -813,7 +813,13 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         // Chunks of groups, one selection wave each (the cost model's co-resident clusters:
         // 22 on B200 at L=8192), so chunking costs no compute; the remainder goes FIRST so
         // that the only exposed upload is the smallest one.
-        const int w = dim == 64 ? select64_wave(count, n_groups) : 0;
+        // When the tensor-core selection of ALL groups is one wave (cfg2: the split plan), the
+        // uploads are chunked only for the prologues (centroid + attention of a chunk run as soon
+        // as it lands) and ONE selection over every group follows the last prologue: PCIe +
+        // one selection, instead of a pipeline of per-wave selections (the selection's latency
+        // does not depend on how many of the co-resident groups it runs).
+        const bool one_wave = dim == 64 && select_tc_wave(count, n_groups) >= n_groups && c->opt.select_impl != CX_SELECT_IMPL_CUDA_CORE;
+        const int w = one_wave ? (n_groups + 3) / 4 : dim == 64 ? select64_wave(count, n_groups) : 0;
         const int WAVE = w > 0 ? w : 15;
         std::vector<int> start;
 #ifdef CX_EXPERIMENTS
@@ -868,7 +874,12 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
             GroupView vm = view_of(&gm);
             ArenaPlan pa, ps;
             plan_attention(pa, vm);
-            plan_select(ps, vm, k);
+            if (one_wave) {
+                const GroupView va = view_of(&all);
+                plan_select(ps, va, k);
+            } else {
+                plan_select(ps, vm, k);
+            }
             CX_CUDA(cudaStreamSynchronize(x->stream));
             x->arena.reserve(pa.used);
             CX_CUDA(cudaStreamSynchronize(c->stream));
@@ -898,7 +909,17 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
             attention_grouped(x, g, dattn + (size_t)g0 * count, x->stream);
             CX_CUDA(cudaEventRecord(c->pev[i], x->stream));
         }
-        for (int i = 0; i < nch; ++i) {  // selection + gather of chunk i after its prologue
+        if (one_wave) {  // every prologue, then one selection + gather over all groups
+            for (int i = 0; i < nch; ++i) CX_CUDA(cudaStreamWaitEvent(c->stream, c->pev[i], 0));
+            cx_groups ga = all;
+            ga.clouds = dk;
+            ga.queries = dq;
+            const GroupView g = view_of(&ga);
+            c->arena.reset();
+            select_grouped(c, g, dattn, k, lambda, flags, dr, ds, c->stream, dcen);
+            gather_rows2(g, g.X, vdev ? vdev : dv, dr, take, dsk, dsv, (int64_t)o_g, c->stream);  // K and V, one launch
+        }
+        for (int i = 0; i < nch && !one_wave; ++i) {  // selection + gather of chunk i after its prologue
             const int g0 = start[i], ng = start[i + 1] - g0;
             CX_CUDA(cudaStreamWaitEvent(c->stream, c->pev[i], 0));
             cx_groups gi = all;

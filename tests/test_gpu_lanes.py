@@ -113,11 +113,13 @@ def test_compress_through_kvcache_view_and_lanes(cx):
 
 
 @pytest.mark.parametrize("G,pinned,L,k", [(13, True, 1500, 60), (3, False, 1500, 60), (1, True, 700, 30),
-                                         (5, True, 40, 64)])
+                                         (5, True, 40, 64), (48, True, 8192, 164)])
 def test_compress_grouped_host_matches_device(cx, G, pinned, L, k):
     """cx_compress_grouped_host (chunked uploads overlapping the per-chunk
-    compressions) == cx_compress_grouped_dev on the same data, bit for bit,
-    including a ragged last chunk and pageable host memory."""
+    prologues; one selection over all groups when the plan is one wave -- the cfg2 case
+    (48, 8192, 164) runs the split plan -- else per-wave selections) ==
+    cx_compress_grouped_dev on the same data, bit for bit, including a ragged last chunk
+    and pageable host memory."""
     import torch
     from paper_2601_01298_b200 import device
     d, P = 64, 7  # (5, 40, 64): k > L, every row taken (take = min(k, L))
