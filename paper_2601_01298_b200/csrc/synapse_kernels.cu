@@ -75,9 +75,12 @@ __global__ void __launch_bounds__(256) attn64_scores_kernel(GroupView gv, double
 #pragma unroll
     for (int c = 0; c < 64; ++c) {
         const double xc = (double)x[c];
+        // fused multiply-add: half the fp64 instructions of the reference's dmul + dadd, and one
+        // rounding per term instead of two (the attention mass contract is 1e-12 relative,
+        // DESIGN.md §3.1; the selection's decisions are certified by the gap monitor)
 #pragma unroll
         for (int p = 0; p < kAttnMaxP; ++p)
-            if (p < gv.P) acc[p] = __dadd_rn(acc[p], __dmul_rn(qs[p][c], xc));
+            if (p < gv.P) acc[p] = __fma_rn(qs[p][c], xc, acc[p]);
     }
 #pragma unroll
     for (int p = 0; p < kAttnMaxP; ++p) {
