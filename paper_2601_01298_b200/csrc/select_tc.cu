@@ -1098,9 +1098,10 @@ int selx_active(const SelxCfg& c) {
 
 }  // namespace
 
-// Cost model (us per round): a fixed part (exchanges, barriers, the exact queue) plus a
-// per-row part, x1.15 for the global-memory exchanges of the cooperative mode; times the
-// waves = ceil(G / co-resident groups).
+// Cost model (us per round, fitted below): a fixed part, a per-row part and a per-CTA part
+// (exchange fan-in) for each exchange mode; times the waves = ceil(G / co-resident groups).
+// The first model (fixed + per-row only) picked clusters of 16 for 6 groups -- cfg2 sharded
+// over 8 GPUs -- at 2.02 ms where clusters of 6 take 1.32 ms.
 //
 // A SPLIT plan runs two launches side by side in one wave: as many groups as are
 // co-resident as thread-block clusters (DSMEM exchanges), and the rest as a cooperative
@@ -1126,7 +1127,13 @@ static bool selx_plan(int G, int64_t L, const Options& o, SelxPlan* out) {
             max_optin = 232448;
     }
     const size_t budget = (size_t)max_optin - 1024;
-    auto per_round = [](const SelxCfg& c) { return (4.0 + 0.0008 * c.S) * (c.cluster ? 1.0 : 1.15); };
+    // us per round, fitted to B200 measurements (cfg2 rows, k = 164; tools/sel_sweep.sh):
+    // clusters C = 4 / 5 / 6 / 8 / 12 / 16: 7.80 / 7.98 / 7.63 / 8.23 / 9.74 / 11.86 us, stamped
+    // cooperative C = 4 / 6 / 8: 8.88 / 8.19 / 7.96 us -- a per-row part (the bound and ranking
+    // passes) plus a per-CTA part (exchange fan-in), smaller for the cooperative exchanges
+    auto per_round = [](const SelxCfg& c) {
+        return c.cluster ? 1.50 + 0.00195 * c.S + 0.58 * c.C : 3.83 + 0.00195 * c.S + 0.27 * c.C;
+    };
     // every (mode, C) that fits, with its co-residency
     std::vector<SelxCfg> cand;
     for (int mode = 0; mode < 2; ++mode) {
