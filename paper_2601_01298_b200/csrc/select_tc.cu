@@ -673,15 +673,18 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         // ======== X1: cluster-wide min/max over remaining rows ========
         double amin, amax, cmin, cmax;
         {
-            unsigned long long b0 = BITS_INF, b1 = 0ull, b2_ = BITS_INF, b3 = 0ull;
+            // per-thread min / max in fp64 (one DMNMX each; the values are finite and >= 0, so the
+            // fp64 order is the order of their bit patterns the warp reductions use)
+            double f0 = INFINITY, f1 = 0.0, f2 = INFINITY, f3 = 0.0;
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
-                if (!(remm >> k & 1u)) continue;
-                b0 = min(b0, dbits(a[k]));
-                b1 = max(b1, dbits(a[k]));
-                b2_ = min(b2_, dbits(m[k]));
-                b3 = max(b3, dbits(m[k]));
+                const bool r = remm >> k & 1u;
+                f0 = fmin(f0, r ? a[k] : INFINITY);
+                f1 = fmax(f1, r ? a[k] : 0.0);
+                f2 = fmin(f2, r ? m[k] : INFINITY);
+                f3 = fmax(f3, r ? m[k] : 0.0);
             }
+            unsigned long long b0 = dbits(f0), b1 = dbits(f1), b2_ = dbits(f2), b3 = dbits(f3);
             b0 = wmin64(b0);
             b1 = wmax64(b1);
             b2_ = wmin64(b2_);
@@ -732,14 +735,16 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             ph1 ^= 1u;
             XSTAMP(4);
             if (CL && tid == 0 && round + 1 < p.take) mbar_arrive_expect(&mbar[0], tx1);
-            const unsigned long long* mb64 = reinterpret_cast<const unsigned long long*>(mm);
-            b0 = BITS_INF; b1 = 0ull; b2_ = BITS_INF; b3 = 0ull;
+            f0 = INFINITY; f1 = 0.0; f2 = INFINITY; f3 = 0.0;
             for (int e = lane; e < (int)C * (CL ? NW : 1); e += 32) {
-                b0 = min(b0, mb64[e * 4 + 0]);
-                b1 = max(b1, mb64[e * 4 + 1]);
-                b2_ = min(b2_, mb64[e * 4 + 2]);
-                b3 = max(b3, mb64[e * 4 + 3]);
+                const double2 lo = reinterpret_cast<const double2*>(mm)[2 * e];
+                const double2 hi = reinterpret_cast<const double2*>(mm)[2 * e + 1];
+                f0 = fmin(f0, lo.x);
+                f1 = fmax(f1, lo.y);
+                f2 = fmin(f2, hi.x);
+                f3 = fmax(f3, hi.y);
             }
+            b0 = dbits(f0); b1 = dbits(f1); b2_ = dbits(f2); b3 = dbits(f3);
             // a warp with no remaining rows pushed (inf, 0, inf, 0): neutral
             amin = bitsd(wmin64(b0));
             amax = bitsd(wmax64(b1));
