@@ -468,6 +468,10 @@ typedef struct cx_cortex_config {
     int64_t virtual_base;    /* first reserved virtual position (RuntimeConfig::virtual_base) */
     int64_t max_context;     /* context rows the push mirror holds (>= the prefill) */
     int push_mode;           /* CX_CORTEX_PUSH_* */
+    int gate;                /* 1: gate each thought before its injection (scheduler.cpp:272-286 decide:
+                                cosine of the river's latest hidden state and the thought's last hidden
+                                state >= theta; a rejected thought is not injected); 0: inject all */
+    double theta;            /* gate threshold, [-1, 1] (gate.cpp:47-48) */
 } cx_cortex_config;
 typedef struct cx_cortex_agents {  /* device tensors, the cx_decode_batch layouts */
     float* tail_keys;
@@ -483,6 +487,7 @@ typedef struct cx_cortex_stats {
     double agent_ms, river_ms, push_ms_mean;  /* lane spans (device events) and mean push */
     int pushes, injections;
     uint64_t last_version;
+    int thoughts_accepted, thoughts_rejected;  /* gate decisions of the run (gate = 1) */
 } cx_cortex_stats;
 /* river: the prefilled river cache (context rows only); it must outlive the runtime.
  * The first synapse is pushed and published (version 1) before this returns
@@ -504,6 +509,11 @@ cx_status cx_cortex_run(cx_cortex* rt, int n_river_tokens, const int* river_toke
                         float* river_logits, float* synapse_history, int max_versions, float* out_history);
 /* the latest published synapse (keys / values [n_layers][n_kv][k][d_k], any memory) */
 cx_status cx_cortex_front_synapse(const cx_cortex* rt, float* keys, float* values, uint64_t* version);
+/* The gate decisions of the last cx_cortex_run (GateDecision rows, gate.hpp:14-22): up to
+ * max entries of (thought_id, score (NaN when degenerate), accepted, degenerate); *n = the
+ * run's decision count.  Empty when the runtime does not gate. */
+cx_status cx_cortex_gate_log(const cx_cortex* rt, int64_t max, int64_t* thought_ids, double* scores,
+                             uint8_t* accepted, uint8_t* degenerate, int64_t* n);
 cx_status cx_cortex_destroy(cx_cortex* rt);
 
 /* ======================================================================

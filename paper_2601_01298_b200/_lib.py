@@ -65,7 +65,7 @@ class CxCortexConfig(C.Structure):
     _fields_ = [("n_agents", C.c_int), ("n_q", C.c_int), ("t_cap", C.c_int), ("k", C.c_int),
                 ("lambda_", C.c_double), ("push_every", C.c_int), ("inject_every", C.c_int),
                 ("thought_tokens", C.c_int), ("virtual_base", C.c_int64), ("max_context", C.c_int64),
-                ("push_mode", C.c_int)]
+                ("push_mode", C.c_int), ("gate", C.c_int), ("theta", C.c_double)]
 
 
 class CxCortexAgents(C.Structure):
@@ -75,7 +75,8 @@ class CxCortexAgents(C.Structure):
 
 class CxCortexStats(C.Structure):
     _fields_ = [("agent_ms", C.c_double), ("river_ms", C.c_double), ("push_ms_mean", C.c_double),
-                ("pushes", C.c_int), ("injections", C.c_int), ("last_version", C.c_uint64)]
+                ("pushes", C.c_int), ("injections", C.c_int), ("last_version", C.c_uint64),
+                ("thoughts_accepted", C.c_int), ("thoughts_rejected", C.c_int)]
 
 
 # (name, restype, argtypes); cx_status-returning calls use C.c_int.
@@ -197,6 +198,8 @@ _SIGS = [
      [c_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int, C.POINTER(CxCortexStats),
       C.POINTER(C.c_uint64), c_vp, c_vp, C.c_int, c_vp]),
     ("cx_cortex_front_synapse", C.c_int, [c_vp, c_vp, c_vp, C.POINTER(C.c_uint64)]),
+    ("cx_cortex_gate_log", C.c_int, [c_vp, C.c_int64, c_i64p, c_f64p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint8),
+                                     c_i64p]),
     ("cx_cortex_destroy", C.c_int, [c_vp]),
 ]
 

@@ -70,6 +70,18 @@ struct cx_cortex {
     double* attn = nullptr;   // push attention [ctx_cap]
     std::mutex mu;            // front / version / inflight, shared by the two host threads
     cudaEvent_t rev[8] = {}, aev[8] = {};  // per-lane step completion rings (host throttle)
+    // the thought gate (cfg.gate): the river's latest hidden state and the thought's last one
+    // [2][d_model], the device decision, its pinned host copy, the run's log
+    float* hid = nullptr;
+    double* g_score = nullptr;      // device: score, then accepted / degenerate bytes
+    double* g_host = nullptr;       // pinned: score, flags
+    struct GateRec {
+        int64_t id;
+        double score;
+        uint8_t accepted, degenerate;
+    };
+    std::vector<GateRec> gate_log;
+    int accepted = 0, rejected = 0;
 };
 
 namespace cx {
@@ -237,11 +249,31 @@ void inject_thought(cx_cortex* r, const int* thought, int64_t thought_id, int64_
     sc->context_count = 0;
     for (int t = 0; t < T; ++t) {
         const int64_t pos = r->virtual_next + t;
-        const cx_status st = cx_forward_step_dev(r->ctx, r->w, 1, &sc, thought + t, &pos, nullptr, nullptr, nullptr, r->rs);
+        // the last token's hidden state is the thought's t_side (encode_thought's last_hidden)
+        float* h = (r->cfg.gate && t == T - 1) ? r->hid + r->d_model : nullptr;
+        const cx_status st = cx_forward_step_dev(r->ctx, r->w, 1, &sc, thought + t, &pos, nullptr, h, nullptr, r->rs);
         if (st != CX_OK) fail(st, cx_last_error());
     }
     // the scratch cache holds exactly T rows per layer ([layer][T][d] when its capacity is T)
     if (sc->capacity != T) fail(CX_DEVICE_ERROR, "cortex: the scratch cache must hold exactly the thought's rows");
+    if (r->cfg.gate) {
+        // decide(river hidden, thought hidden, theta) (gate.cpp:45-61) on the device; the host
+        // needs the verdict (a rejected thought leaves the river cache unchanged), so the river
+        // lane is synchronised once per thought
+        uint8_t* flags = reinterpret_cast<uint8_t*>(r->g_score + 1);
+        const cx_status gs = cx_gate_decide_dev(r->ctx, 1, r->d_model, r->hid, r->d_model, r->hid + r->d_model,
+                                                r->d_model, r->cfg.theta, r->g_score, flags, flags + 1, r->rs);
+        if (gs != CX_OK) fail(gs, cx_last_error());
+        CX_CUDA(cudaMemcpyAsync(r->g_host, r->g_score, 2 * sizeof(double), cudaMemcpyDeviceToHost, r->rs));
+        CX_CUDA(cudaStreamSynchronize(r->rs));
+        const uint8_t* hf = reinterpret_cast<const uint8_t*>(r->g_host + 1);
+        r->gate_log.push_back({thought_id, r->g_host[0], hf[0], hf[1]});
+        if (!hf[0]) {  // rejected (scheduler.cpp:299-302): not injected, the virtual range is reused
+            r->rejected += 1;
+            return;
+        }
+        r->accepted += 1;
+    }
     cx_injection_record rec{};
     const cx_status st = cx_inject_dev(r->river, sc->keys, sc->values, r->virtual_next, T, r->n_layers, r->d_model,
                                        thought_id, stream_position, &rec, r->rs);
@@ -273,6 +305,8 @@ extern "C" cx_status cx_cortex_create(cx_ctx* ctx, const cx_weights* w, cx_kvcac
         if (river->context_count != (int64_t)river->positions.size())
             fail(CX_PRECONDITION_ERROR, "cortex: the river cache must hold only context rows at creation");
         if (river->context_count < cfg->k) fail(CX_PRECONDITION_ERROR, "cortex: fewer context rows than k");
+        if (cfg->gate && (cfg->theta < -1.0 || cfg->theta > 1.0))
+            fail(CX_PRECONDITION_ERROR, "decide: theta must be in [-1,1]");
         auto r = std::make_unique<cx_cortex>();
         r->ctx = ctx;
         r->w = w;
@@ -297,6 +331,12 @@ extern "C" cx_status cx_cortex_create(cx_ctx* ctx, const cx_weights* w, cx_kvcac
         CX_CUDA(cudaMalloc(&r->dev_out, sizeof(float) * std::max(4096, w->vocab)));
         CX_CUDA(cudaMalloc(&r->fq, sizeof(float) * r->d_model));
         CX_CUDA(cudaMemset(r->fq, 0, sizeof(float) * r->d_model));
+        // gate buffers; the river hidden starts at zero (no river token yet: a degenerate,
+        // rejected decision, as decide() gives a zero-norm input)
+        CX_CUDA(cudaMalloc(&r->hid, sizeof(float) * 2 * r->d_model));
+        CX_CUDA(cudaMemset(r->hid, 0, sizeof(float) * 2 * r->d_model));
+        CX_CUDA(cudaMalloc(&r->g_score, 2 * sizeof(double)));
+        CX_CUDA(cudaMallocHost(&r->g_host, 2 * sizeof(double)));
         // the context mirror (the river holds only context rows, checked above)
         r->ctx_cap = std::max<int64_t>(cfg->max_context, river->context_count);
         CX_CUDA(cudaMalloc(&r->ctx_k, sizeof(float) * r->n_layers * r->ctx_cap * r->d_model));
@@ -390,7 +430,8 @@ void river_lane(cx_cortex* r, int n_tokens, const int* river_tokens, const int* 
         cx_kvcache* kc = r->river;
         const int64_t pos = r->position;
         const cx_status st =
-            cx_forward_step_dev(r->ctx, r->w, 1, &kc, river_tokens + t, &pos, r->dev_out, nullptr, r->fq, r->rs);
+            cx_forward_step_dev(r->ctx, r->w, 1, &kc, river_tokens + t, &pos, r->dev_out, r->cfg.gate ? r->hid : nullptr,
+                                r->fq, r->rs);
         if (st != CX_OK) fail(st, cx_last_error());
         r->position += 1;
         mirror_row(r, (int64_t)kc->positions.size() - 1);  // the new context row
@@ -433,6 +474,8 @@ extern "C" cx_status cx_cortex_run(cx_cortex* r, int n_tokens, const int* river_
         r->push_ms_sum = 0.0;
         r->pushes = 0;
         r->injections = 0;
+        r->accepted = r->rejected = 0;
+        r->gate_log.clear();
         if (synapse_history && (int64_t)r->front_version < max_versions)  // the version published before the run
             CX_CUDA(cudaMemcpyAsync(synapse_history + (size_t)r->front_version * 2 * r->syn_floats,
                                     r->syn + (size_t)(2 * r->front) * r->syn_floats, sizeof(float) * 2 * r->syn_floats,
@@ -477,6 +520,8 @@ extern "C" cx_status cx_cortex_run(cx_cortex* r, int n_tokens, const int* river_
             stats->injections = r->injections;
             stats->push_ms_mean = r->pushes ? r->push_ms_sum / r->pushes : 0.0;
             stats->last_version = r->version;
+            stats->thoughts_accepted = r->accepted;
+            stats->thoughts_rejected = r->rejected;
         }
     });
 }
@@ -493,6 +538,21 @@ extern "C" cx_status cx_cortex_front_synapse(const cx_cortex* r, float* keys, fl
             CX_CUDA(cudaMemcpy(values, r->syn + (size_t)(2 * r->front + 1) * r->syn_floats, sizeof(float) * r->syn_floats,
                                cudaMemcpyDefault));
         if (version) *version = r->front_version;
+    });
+}
+
+extern "C" cx_status cx_cortex_gate_log(const cx_cortex* r, int64_t max, int64_t* thought_ids, double* scores,
+                                        uint8_t* accepted, uint8_t* degenerate, int64_t* n) {
+    return guard(__func__, [&] {
+        if (!r || !n) fail(CX_INVALID_ARGUMENT, "null argument");
+        const int64_t m = std::min<int64_t>(max, (int64_t)r->gate_log.size());
+        for (int64_t i = 0; i < m; ++i) {
+            if (thought_ids) thought_ids[i] = r->gate_log[i].id;
+            if (scores) scores[i] = r->gate_log[i].score;
+            if (accepted) accepted[i] = r->gate_log[i].accepted;
+            if (degenerate) degenerate[i] = r->gate_log[i].degenerate;
+        }
+        *n = (int64_t)r->gate_log.size();
     });
 }
 
@@ -519,6 +579,9 @@ extern "C" cx_status cx_cortex_destroy(cx_cortex* r) {
         cudaFree(r->ctx_v);
         cudaFree(r->fq);
         cudaFree(r->attn);
+        cudaFree(r->hid);
+        cudaFree(r->g_score);
+        if (r->g_host) cudaFreeHost(r->g_host);
         delete r;
     });
 }

@@ -96,7 +96,8 @@ class Cortex:
 
     def __init__(self, weights: Weights, river: KvCache, *, k: int, lam: float, push_every: int, inject_every: int,
                  thought_tokens: int, virtual_base: int, max_context: int, tail_keys, tail_values, tail_len,
-                 new_keys, new_values, q, out, river_queries=None, push_mode: str = "scheduler"):
+                 new_keys, new_values, q, out, river_queries=None, push_mode: str = "scheduler",
+                 gate: bool = False, theta: float = 0.0):
         self._keep = (weights, river, tail_keys, tail_values, tail_len, new_keys, new_values, q, out, river_queries)
         for t in (tail_keys, tail_values, new_keys, new_values, q, out) + ((river_queries,) if river_queries is not None
                                                                           else ()):
@@ -106,7 +107,8 @@ class Cortex:
             raise TypeError("tail_len must be int32")
         n, n_layers, n_q, d_k = q.shape
         c = CxCortexConfig(n, n_q, tail_keys.shape[3], int(k), float(lam), int(push_every), int(inject_every),
-                           int(thought_tokens), int(virtual_base), int(max_context), self.PUSH_MODES[push_mode])
+                           int(thought_tokens), int(virtual_base), int(max_context), self.PUSH_MODES[push_mode],
+                           1 if gate else 0, float(theta))
         a = CxCortexAgents(tail_keys.data_ptr(), tail_values.data_ptr(), tail_len.data_ptr(), new_keys.data_ptr(),
                            new_values.data_ptr(), q.data_ptr(), out.data_ptr(),
                            river_queries.data_ptr() if river_queries is not None else None)
@@ -143,8 +145,20 @@ class Cortex:
                                 int(synapse_history.shape[0]) if synapse_history is not None else 0,
                                 dp(out_history)), "cortex_run")
         stats = {"agent_ms": st.agent_ms, "river_ms": st.river_ms, "push_ms_mean": st.push_ms_mean,
-                 "pushes": st.pushes, "injections": st.injections, "last_version": int(st.last_version)}
+                 "pushes": st.pushes, "injections": st.injections, "last_version": int(st.last_version),
+                 "thoughts_accepted": st.thoughts_accepted, "thoughts_rejected": st.thoughts_rejected}
         return stats, np.array(vers[:agent_steps], dtype=np.uint64)
+
+    def gate_log(self):
+        """The last run's gate decisions (gate=True): [(thought_id, score, accepted, degenerate)],
+        GateDecision's fields (gate.hpp:14-22; score NaN when degenerate)."""
+        n = C.c_int64()
+        check(lib.cx_cortex_gate_log(self._h, 0, None, None, None, None, C.byref(n)), "cortex_gate_log")
+        m = int(n.value)
+        ids, sc = (C.c_int64 * max(m, 1))(), (C.c_double * max(m, 1))()
+        acc, deg = (C.c_uint8 * max(m, 1))(), (C.c_uint8 * max(m, 1))()
+        check(lib.cx_cortex_gate_log(self._h, m, ids, sc, acc, deg, C.byref(n)), "cortex_gate_log")
+        return [(int(ids[i]), float(sc[i]), bool(acc[i]), bool(deg[i])) for i in range(m)]
 
     def front_synapse(self):
         """(keys, values, version) of the latest published synapse."""

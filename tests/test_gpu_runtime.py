@@ -185,3 +185,83 @@ def test_cortex_create_preconditions():
     with pytest.raises(errors.precondition_error):
         rt.Cortex(w, river, k=8, lam=0.5, push_every=2, inject_every=2, thought_tokens=2, virtual_base=3072,
                   max_context=128, **ag)
+
+
+def _gate_score_ref(h, t):
+    """gate.cpp:27-42 in plain Python floats (fp64, sequential, no FMA)."""
+    dot = na = nb = 0.0
+    for a, b in zip(h.tolist(), t.tolist()):
+        dot += a * b
+        na += a * a
+        nb += b * b
+    if na == 0.0 or nb == 0.0:
+        return None  # degenerate_input_error -> decide(): NaN score, rejected
+    import math
+    return min(1.0, max(-1.0, dot / (math.sqrt(na) * math.sqrt(nb))))
+
+
+@pytest.mark.parametrize("theta", [-1.0, "median"])
+def test_cortex_gate_decides_before_injection(theta):
+    """The runtime with the thought gate (cfg.gate): every thought is decided
+    (gate.cpp:45-61: cosine of the river's latest hidden state and the thought's last
+    hidden state >= theta) before drain_injections; a rejected thought leaves the river
+    cache alone and its virtual range is reused.  Checked against a host-driven replay
+    (forward_step / encode / decide in Python floats / inject one call at a time): the
+    gate log (scores bitwise, verdicts) and the river's logits at every token."""
+    from paper_2601_01298_b200 import runtime as rt
+    from paper_2601_01298_b200.injector import inject_dev
+    from paper_2601_01298_b200.model import KvCache
+    L0, T, k, lam, n_tok, vbase, inj = 600, 4, 40, 0.5, 24, 3072, 3
+    cfg, w, river, ag = _setup(L0=L0)
+    rs = np.random.default_rng(17)
+    river_tokens = rs.integers(0, cfg.vocab_size, n_tok).tolist()
+    thoughts = rs.integers(0, cfg.vocab_size, (n_tok // inj + 1) * T).tolist()
+
+    def replay(cache, th):
+        """-> (logits [n][vocab], gate log, injections)"""
+        logits = torch.empty(n_tok, cfg.vocab_size, device="cuda")
+        hid = torch.zeros(cfg.d_model, device="cuda")
+        log, vnext, n_inj = [], vbase, 0
+        for t, tok in enumerate(river_tokens):
+            if t % inj == 0:
+                i = t // inj
+                scratch = KvCache(cfg, capacity=T)
+                th_hid = torch.empty(cfg.d_model, device="cuda")
+                for j in range(T):
+                    rt.forward_step_dev(w, [scratch], [thoughts[i * T + j]], [vnext + j],
+                                        hidden=th_hid if j == T - 1 else None)
+                torch.cuda.synchronize()
+                s = _gate_score_ref(hid.double().cpu().numpy(), th_hid.double().cpu().numpy())
+                acc = s is not None and s >= th
+                log.append((i, s, acc, s is None))
+                if acc:
+                    inject_dev(cache, scratch.keys_dev(), scratch.values_dev(), vnext, T, cfg.n_layers, cfg.d_model, i,
+                               L0 + t - 1, torch.cuda.current_stream().cuda_stream)
+                    torch.cuda.synchronize()
+                    vnext += T
+                    n_inj += 1
+                del scratch
+            rt.forward_step_dev(w, [cache], [tok], [L0 + t], logits=logits[t], hidden=hid)
+        torch.cuda.synchronize()
+        return logits, log, n_inj
+
+    if theta == "median":  # a threshold that splits this river's thoughts
+        _, log0, _ = replay(river.clone(), -1.0)
+        theta = float(np.median([s for _, s, _, d in log0 if not d]))
+    ref_logits, ref_log, ref_inj = replay(river.clone(), theta)
+    cx = rt.Cortex(w, river, k=k, lam=lam, push_every=5, inject_every=inj, thought_tokens=T, virtual_base=vbase,
+                   max_context=1024, gate=True, theta=theta, **ag)
+    logits = torch.empty(n_tok, cfg.vocab_size, device="cuda")
+    stats, _ = cx.run(river_tokens, thoughts, 50, river_logits=logits)
+    log = cx.gate_log()
+    assert len(log) == len(ref_log)
+    for (i, s, a, d), (ri, rsc, ra, rd) in zip(log, ref_log):
+        assert (i, a, d) == (ri, ra, rd)
+        assert (np.isnan(s) and rsc is None) or s == rsc, (i, s, rsc)
+    assert stats["injections"] == ref_inj == stats["thoughts_accepted"]
+    assert stats["thoughts_rejected"] == len(ref_log) - ref_inj
+    assert log[0][3], "the first thought meets a river without a hidden state: degenerate, rejected"
+    if theta > -1.0:
+        assert 0 < ref_inj < len(ref_log) - 1, "the median threshold should split the thoughts"
+    assert torch.equal(logits, ref_logits), "river logits differ from the gated replay"
+    cx.close()
