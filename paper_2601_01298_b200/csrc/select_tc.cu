@@ -21,8 +21,9 @@
 // the reference.
 //
 // Rows: thread (warp w, lane l) owns rows tile*128 + 32 (w % 4) + l of the tiles
-// j = w / 4 + 4 k, k = 0..RPT-1 (tcgen05.ld: a warp reads the TMEM lanes of its
-// sub-partition w % 4).  Tiles [0, n_smem) are in shared memory, [n_smem, n_tiles)
+// j = w / 4 + (NW / 4) k, k = 0..RPT-1 (tcgen05.ld: a warp reads the TMEM lanes of its
+// sub-partition w % 4).  NT = 512 threads (CX_SEL_NT=1024 builds a 3-rows-per-thread variant:
+// 1.3-2.5 KB of spills at 64 registers, cfg2 selection 2.27 ms against 1.66 ms; not used).  Tiles [0, n_smem) are in shared memory, [n_smem, n_tiles)
 // in TMEM columns [tm_rows_col + 32 (j - n_smem), +32).
 #include <cooperative_groups.h>
 #include <cuda_fp16.h>
@@ -40,7 +41,10 @@ namespace cx {
 namespace {
 
 constexpr int D = 64;
-constexpr int NT = 512;
+#ifndef CX_SEL_NT
+#define CX_SEL_NT 512
+#endif
+constexpr int NT = CX_SEL_NT;  // threads per CTA (1024: 3 rows per thread at 22 tiles, 64 registers)
 constexpr int NW = NT / 32;
 constexpr int TILE = 128;         // rows per MMA (M)
 constexpr int MAXT = 22;          // tiles per CTA: 2816 rows
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
             m[k] = 0.0; a[k] = 0.0; th[k] = INFINITY; nx[k] = 0.f;
-            const int j = quad + 4 * k;
+            const int j = quad + (NW / 4) * k;
             if (j >= p.n_tiles) continue;
             const int li = j * TILE + 32 * sub + lane;
             const bool valid = li < nrows;
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                 uint32_t dh[RPT], dl[RPT];
 #pragma unroll
                 for (int k = 0; k < RPT; ++k) {
-                    const int j = quad + 4 * k;
+                    const int j = quad + (NW / 4) * k;
                     dh[k] = dl[k] = 0u;
                     if (j < p.n_tiles)
                         tmem_ld2(tbase + ((uint32_t)(32 * sub) << 16) + (uint32_t)(DC * (j / DPACK) + 2 * (j % DPACK)), dh[k],
@@ -593,7 +597,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
                     const int sl = atomicAdd(qn, 1);
                     if (sl < NT) {
                         slot[k] = sl;
-                        const int li = (quad + 4 * k) * TILE + 32 * sub + lane;
+                        const int li = (quad + (NW / 4) * k) * TILE + 32 * sub + lane;
                         qrow[sl] = li;
                         need &= ~(1u << k);
 #ifndef CX_SEL_NO_QPREFETCH
@@ -614,7 +618,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             }
             while (__any_sync(0xffffffffu, need != 0)) {  // round 1, or a queue overflow
                 const int k = need ? __ffs(need) - 1 : 0;
-                const int li = (quad + 4 * k) * TILE + 32 * sub + lane;
+                const int li = (quad + (NW / 4) * k) * TILE + 32 * sub + lane;
                 const float4* src = reinterpret_cast<const float4*>(gX + (int64_t)li * p.rstride);
                 float4 x4[D / 4];
 #pragma unroll
@@ -780,7 +784,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         const uint32_t atmax = __ballot_sync(0xffffffffu, kmax >= 0 && hkey == wkey);
         const int wl = atmax ? __ffs(atmax) - 1 : 0;
         const int spec_k = __shfl_sync(0xffffffffu, kmax, wl);
-        const int spec_li = atmax ? (quad + 4 * spec_k) * TILE + 32 * sub + wl : -1;
+        const int spec_li = atmax ? (quad + (NW / 4) * spec_k) * TILE + 32 * sub + wl : -1;
         float4 spec4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (atmax && lane < D / 4)
             spec4 = __ldg(reinterpret_cast<const float4*>(gX + (int64_t)spec_li * p.rstride) + lane);
@@ -799,7 +803,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             const double na = a_span ? __ddiv_rn(__dsub_rn(a[k], amin), ar) : 0.0;
             const double nc = c_span ? __ddiv_rn(__dsub_rn(m[k], cmin), cr) : 0.0;
             const unsigned long long hk = dbits(__dadd_rn(__dmul_rn(lam, nc), __dmul_rn(one_m_lam, na)));
-            const int li = (quad + 4 * k) * TILE + 32 * sub + lane;
+            const int li = (quad + (NW / 4) * k) * TILE + 32 * sub + lane;
             if (!has_b || hk > bkey) {  // rows ascend with k: on a tie the earlier (lower) row stays
                 if (has_b) { rkey = max(rkey, bkey); has_r = true; }
                 bkey = hk; brow = li; bnx = nx[k]; has_b = true;
@@ -980,7 +984,7 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
         if (br >= r0 && br < r0 + nrows) {
             const int li = (int)(br - r0);
             const int j = li / TILE, r = li % TILE;
-            if (wid == ((j & 3) << 2) + (r >> 5) && lane == (r & 31)) remm &= ~(1u << (j >> 2));
+            if (wid == ((j % (NW / 4)) << 2) + (r >> 5) && lane == (r & 31)) remm &= ~(1u << (j / (NW / 4)));
         }
         if (tid == 0 && rank == 0) {
             pick_rows[round] = br;
@@ -1046,7 +1050,7 @@ bool selx_shape(int s, size_t budget, SelxCfg* c) {
     c->S = s;
     c->n_tiles = nt;
     c->n_smem = ns;
-    c->rpt = (nt + 3) / 4;
+    c->rpt = (nt + NW / 4 - 1) / (NW / 4);
     c->n_stage = 0;  // (TMA staging of the exact rows measured slower than direct loads)
     // at least ~116 KB so that one CTA owns an SM (and its 512 TMEM columns)
     c->smem = std::max(selx_layout(ns, c->C, c->n_stage).total, (size_t)116 * 1024);
