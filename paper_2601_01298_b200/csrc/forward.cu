@@ -54,6 +54,14 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Programmatic dependent launch inside forward_step: every launch after the first one may
+// start while its predecessor drains; it waits for the predecessor's results here (a no-op
+// for a normally launched grid) and lets its own successor launch right away.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void fw_embed(const __grid_constant__ FwBatch P, const float* emb, int d, float* x) {
     const int b = blockIdx.x;
     if (b >= P.B) return;
@@ -70,6 +78,7 @@ __device__ __forceinline__ double warp_rms_inv(const float* xb, int d, double ep
 
 // out[b] = x[b] * (1 / sqrt(mean(x^2) + eps)) * gain, fp64 (kernels.cpp:28-38); one warp per agent
 __global__ void fw_rmsnorm(const float* x, const float* gain, int d, int B, float* out, double eps) {
+    pdl_enter();
     const int b = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
     if (b >= B) return;
     const float* xb = x + (size_t)b * d;
@@ -83,6 +92,7 @@ __global__ void fw_rmsnorm(const float* x, const float* gain, int d, int B, floa
 // rounded to fp32 exactly as the separate rmsnorm's output).
 __global__ void fw_matvec(const float* W, int n_out, int n_in, const float* X, int B, float* Y, int mode,
                           const float* gain, double eps) {
+    pdl_enter();
     const int wpb = blockDim.x / 32;
     const long long item = (long long)blockIdx.x * wpb + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -113,6 +123,7 @@ __global__ void fw_matvec(const float* W, int n_out, int n_in, const float* X, i
 // (model.cpp:142-152 write_layer); q (rotated) -> qbuf, and final_q at the last layer.
 __global__ void fw_qkv_rope(const __grid_constant__ FwBatch P, int l, const float* Wq, int n_heads, int d_k,
                             double base, const float* x, const float* gain, double eps, float* qbuf, float* final_q) {
+    pdl_enter();
     const int d = n_heads * d_k;
     const int wpb = blockDim.x / 32, lane = threadIdx.x & 31;
     const long long item = (long long)blockIdx.x * wpb + threadIdx.x / 32;
@@ -184,6 +195,7 @@ __device__ __forceinline__ void stage_tile(float (*tile)[65], const float* src, 
 __global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch P, int l, int n_heads, int d_k,
                                                  const float* q, double* part, unsigned* counters, int n_chunks,
                                                  float* att) {
+    pdl_enter();
     const int ch = blockIdx.x, h = blockIdx.y, b = blockIdx.z, t = threadIdx.x;
     const FwAgent& a = P.a[b];
     const int64_t n = a.row + 1;
@@ -302,10 +314,31 @@ __global__ void fw_rope_vec(float* v, int n, int64_t position, double base) {  /
     }
 }
 
+// a launch that may overlap its stream predecessor's tail (the kernel calls pdl_enter first)
+template <class... KArgs, class... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, bool pdl, Args&&... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    CX_CUDA(cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...));
+    count_launch();
+}
+
 void matvec_launch(const float* W, int n_out, int n_in, const float* X, int B, float* Y, int mode, cudaStream_t s,
-                   const float* gain = nullptr, double eps = 1e-5) {
+                   const float* gain = nullptr, double eps = 1e-5, bool pdl = false) {
     const long long items = (long long)n_out * B;
     const int wpb = 8;
+    if (pdl) {
+        launch_pdl(fw_matvec, dim3((unsigned)((items + wpb - 1) / wpb)), dim3(32 * wpb), s, true, W, n_out, n_in, X, B,
+                   Y, mode, gain, eps);
+        return;
+    }
     fw_matvec<<<(unsigned)((items + wpb - 1) / wpb), 32 * wpb, 0, s>>>(W, n_out, n_in, X, B, Y, mode, gain, eps);
     check_launch("fw_matvec");
 }
@@ -406,21 +439,20 @@ void forward_batch(cx_ctx* c, const cx_weights* w, int nb, cx_kvcache* const* ca
     const long long pairs = (long long)(d / 2) * nb;
     for (int l = 0; l < L; ++l) {
         // rmsnorm + q/k/v + RoPE + the cache append, one launch
-        fw_qkv_rope<<<(unsigned)((pairs + 7) / 8), 256, 0, s>>>(P, l, W + w->wq(l), w->n_heads, w->d_k, w->rope_base,
-                                                                 x, W + w->attn_norm(l), 1e-5, qb,
-                                                                 l == L - 1 ? final_query : nullptr);
-        check_launch("fw_qkv_rope");
-        fw_attend<<<dim3((unsigned)n_chunks, (unsigned)w->n_heads, (unsigned)nb), 256, 0, s>>>(
-            P, l, w->n_heads, w->d_k, qb, part, c->fw_counters, n_chunks, att);
-        check_launch("fw_attend");
-        matvec_launch(W + w->wo(l), d, d, att, nb, x, 2, s);                           // x += Wo att
-        matvec_launch(W + w->w_in(l), dff, d, x, nb, ff, 1, s, W + w->mlp_norm(l));  // relu(W_in rmsnorm(x))
-        matvec_launch(W + w->w_out(l), d, dff, ff, nb, x, 2, s);                       // x += W_out ff
+        // every launch after fw_embed is a programmatic dependent of the previous one
+        launch_pdl(fw_qkv_rope, dim3((unsigned)((pairs + 7) / 8)), dim3(256), s, true, P, l, W + w->wq(l), w->n_heads,
+                   w->d_k, w->rope_base, (const float*)x, W + w->attn_norm(l), 1e-5, qb,
+                   l == L - 1 ? final_query : nullptr);
+        launch_pdl(fw_attend, dim3((unsigned)n_chunks, (unsigned)w->n_heads, (unsigned)nb), dim3(256), s, true, P, l,
+                   w->n_heads, w->d_k, (const float*)qb, part, c->fw_counters, n_chunks, att);
+        matvec_launch(W + w->wo(l), d, d, att, nb, x, 2, s, nullptr, 1e-5, true);                // x += Wo att
+        matvec_launch(W + w->w_in(l), dff, d, x, nb, ff, 1, s, W + w->mlp_norm(l), 1e-5, true);  // relu(W_in rmsnorm(x))
+        matvec_launch(W + w->w_out(l), d, dff, ff, nb, x, 2, s, nullptr, 1e-5, true);            // x += W_out ff
     }
     float* hid = hidden ? hidden : hs;
-    fw_rmsnorm<<<(unsigned)((nb + 7) / 8), 256, 0, s>>>(x, W + w->final_norm, d, nb, hid, 1e-5);
-    check_launch("fw_rmsnorm");
-    if (logits) matvec_launch(W + w->unemb, w->vocab, d, hid, nb, logits, 0, s);
+    launch_pdl(fw_rmsnorm, dim3((unsigned)((nb + 7) / 8)), dim3(256), s, true, (const float*)x, W + w->final_norm, d,
+               nb, hid, 1e-5);
+    if (logits) matvec_launch(W + w->unemb, w->vocab, d, hid, nb, logits, 0, s, nullptr, 1e-5, true);
     // the entry is complete at every layer (end_entry)
     for (int b = 0; b < nb; ++b) {
         cx_kvcache* kc = caches[b];
