@@ -214,7 +214,31 @@ __global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch
     const float* kb = a.keys + (size_t)l * a.cap * d + (size_t)h * d_k;
     const float* vb = a.values + (size_t)l * a.cap * d + (size_t)h * d_k;
     if (t < d_k) qs[t] = (double)q[(size_t)b * d + h * d_k + t];
-    stage_tile(tile, kb, e0, ne, d, d_k);
+    // full chunks at d_k = 64: every K and V load of the chunk is issued up front (8 + 8 float4
+    // per thread); V waits in registers until the K tile has been consumed (a load -> store
+    // loop per tile was one DRAM round trip per iteration)
+    const bool fast = ne == FW_CHUNK && d_k == 64 && blockDim.x == 256;
+    constexpr int FV = FW_CHUNK * 16 / 256;
+    float4 vreg[FV];
+    if (fast) {
+        float4 kreg[FV];
+#pragma unroll
+        for (int i = 0; i < FV; ++i) {
+            const int idx = t + 256 * i, r = idx >> 4, c = (idx & 15) * 4;
+            kreg[i] = __ldg(reinterpret_cast<const float4*>(kb + (size_t)(e0 + r) * d + c));
+            vreg[i] = __ldg(reinterpret_cast<const float4*>(vb + (size_t)(e0 + r) * d + c));
+        }
+#pragma unroll
+        for (int i = 0; i < FV; ++i) {
+            const int idx = t + 256 * i, r = idx >> 4, c = (idx & 15) * 4;
+            tile[r][c] = kreg[i].x;
+            tile[r][c + 1] = kreg[i].y;
+            tile[r][c + 2] = kreg[i].z;
+            tile[r][c + 3] = kreg[i].w;
+        }
+    } else {
+        stage_tile(tile, kb, e0, ne, d, d_k);
+    }
     __syncthreads();
     const double inv = 1.0 / sqrt((double)d_k);
     double s = -INFINITY;
@@ -235,7 +259,18 @@ __global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch
     __syncthreads();  // every thread has read red[] and the K tile
     const double ps = warp_sum(p);
     if ((t & 31) == 0) red[t >> 5] = ps;
-    stage_tile(tile, vb, e0, ne, d, d_k);
+    if (fast) {
+#pragma unroll
+        for (int i = 0; i < FV; ++i) {
+            const int idx = t + 256 * i, r = idx >> 4, c = (idx & 15) * 4;
+            tile[r][c] = vreg[i].x;
+            tile[r][c + 1] = vreg[i].y;
+            tile[r][c + 2] = vreg[i].z;
+            tile[r][c + 3] = vreg[i].w;
+        }
+    } else {
+        stage_tile(tile, vb, e0, ne, d, d_k);
+    }
     __syncthreads();
     double* out = part + (((size_t)b * n_heads + h) * n_chunks + ch) * (2 + d_k);
     {
@@ -287,8 +322,19 @@ __global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch
     {
         const int c = t % 64, qtr = t / 64;
         if (c < d_k) {
+            // the chunks' partial P.V in order, 8 L2 loads in flight per batch
             double acc = 0.0;
-            for (int i = qtr; i < my_chunks; i += 4) acc += __ldcg(pp + (size_t)i * (2 + d_k) + 2 + c) * sc[i];
+            for (int i0 = qtr; i0 < my_chunks; i0 += 32) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + 4 * u;
+                    v[u] = i < my_chunks ? __ldcg(pp + (size_t)i * (2 + d_k) + 2 + c) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (i0 + 4 * u < my_chunks) acc += v[u] * sc[i0 + 4 * u];
+            }
             pacc[qtr][c] = acc;
         }
     }
