@@ -71,6 +71,7 @@ __global__ void fw_embed(const __grid_constant__ FwBatch P, const float* emb, in
 // 1 / sqrt(mean(x^2) + eps) of one agent's row, by a full warp (kernels.cpp:28-38)
 __device__ __forceinline__ double warp_rms_inv(const float* xb, int d, double eps) {
     double ssq = 0.0;
+#pragma unroll 4
     for (int i = threadIdx.x & 31; i < d; i += 32) ssq += (double)xb[i] * (double)xb[i];
     ssq = warp_sum(ssq);
     return 1.0 / sqrt(ssq / (double)d + eps);
@@ -103,9 +104,11 @@ __global__ void fw_matvec(const float* W, int n_out, int n_in, const float* X, i
     double acc = 0.0;
     if (gain) {
         const double inv = warp_rms_inv(xb, n_in, eps);
+#pragma unroll 4
         for (int c = lane; c < n_in; c += 32)
             acc += (double)row[c] * (double)(float)((double)xb[c] * inv * (double)gain[c]);
     } else {
+#pragma unroll 4
         for (int c = lane; c < n_in; c += 32) acc += (double)row[c] * (double)xb[c];
     }
     acc = warp_sum(acc);
@@ -134,6 +137,9 @@ __global__ void fw_qkv_rope(const __grid_constant__ FwBatch P, int l, const floa
     const double inv = warp_rms_inv(xb, d, eps);
     const size_t dd = (size_t)d * d;
     double acc[6] = {0, 0, 0, 0, 0, 0};
+    // unrolled: the 6 weight rows' loads of several column steps are in flight together
+    // (a rolled loop waited one memory round trip per step); the per-lane order is unchanged
+#pragma unroll 4
     for (int c = lane; c < d; c += 32) {
         const double xn = (double)(float)((double)xb[c] * inv * (double)gain[c]);
 #pragma unroll
