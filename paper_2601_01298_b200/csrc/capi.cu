@@ -702,8 +702,10 @@ void compress_impl(cx_ctx* c, const cx_groups* gr, const float* values, int k, d
         attention_grouped(c, g, attn, s);
         c->arena.used = mark;  // attention scratch is dead once `attn` is written (stream-ordered)
         CX_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
-        select_grouped(c, g, attn, k, lambda, flags, out_rows, out_scores, s, cen);
         const int64_t gs = syn_gstride > 0 ? syn_gstride : (int64_t)take * g.dim;
+        const SynGather gat{values, syn_keys, values ? syn_values : nullptr, gs};
+        if (select_grouped(c, g, attn, k, lambda, flags, out_rows, out_scores, s, cen, &gat))
+            return;  // the selection kernel gathered the landmark rows itself
         if (syn_keys && syn_values && values)  // keys and values in one launch
             gather_rows2(g, g.X, values, out_rows, take, syn_keys, syn_values, gs, s);
         else if (syn_keys)
@@ -916,8 +918,9 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
             ga.queries = dq;
             const GroupView g = view_of(&ga);
             c->arena.reset();
-            select_grouped(c, g, dattn, k, lambda, flags, dr, ds, c->stream, dcen);
-            gather_rows2(g, g.X, vdev ? vdev : dv, dr, take, dsk, dsv, (int64_t)o_g, c->stream);  // K and V, one launch
+            const SynGather gat{vdev ? vdev : dv, dsk, dsv, (int64_t)o_g};
+            if (!select_grouped(c, g, dattn, k, lambda, flags, dr, ds, c->stream, dcen, &gat))
+                gather_rows2(g, g.X, vdev ? vdev : dv, dr, take, dsk, dsv, (int64_t)o_g, c->stream);  // K and V, one launch
         }
         for (int i = 0; i < nch && !one_wave; ++i) {  // selection + gather of chunk i after its prologue
             const int g0 = start[i], ng = start[i + 1] - g0;

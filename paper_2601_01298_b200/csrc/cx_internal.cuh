@@ -223,10 +223,21 @@ void plan_attention(ArenaPlan& p, const GroupView& g);
 
 // selection-monitor scratch per (group, round): one candidate per cluster CTA (<= 16)
 constexpr int kGapRecStride = 16;
-// greedy selection for all groups.  rows/scores out [G][take] ascending.
-void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
+// the landmark K/V gather (A5) a selection may do itself once its picks are sorted:
+// syn_k[g][s] = keys row rows[g][s], syn_v[g][s] = values row (values in the keys' group
+// layout); blocks syn_gs floats apart.  Either output may be null.
+struct SynGather {
+    const float* values;
+    float* syn_k;
+    float* syn_v;
+    int64_t syn_gs;
+};
+// greedy selection for all groups.  rows/scores out [G][take] ascending.  Returns true when
+// the selection also did the gather `gat` (the tensor-core path); otherwise the caller gathers.
+bool select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
                     unsigned flags, int64_t* rows, double* scores, cudaStream_t s,
-                    const double* centroids = nullptr /* [G][dim], computed here when null */);
+                    const double* centroids = nullptr /* [G][dim], computed here when null */,
+                    const SynGather* gat = nullptr);
 // d = 128 instantiation (select128.cu): the reference-mode cloud of a 2-head MHA cache
 bool select128_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
                       double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows, double* scores,
@@ -245,7 +256,8 @@ void plan_select(ArenaPlan& p, const GroupView& g, int k);
 // does not apply
 bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
                       double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows,
-                      double* scores, double* gaps, void* scratch, cudaStream_t s);
+                      double* scores, double* gaps, void* scratch, cudaStream_t s,
+                      const SynGather* gat = nullptr, bool* gathered = nullptr);
 int select_tc_wave(int64_t L, int G);
 size_t select_tc_scratch(int G);  // bytes of scratch select_tc_launch may use
 // dim-64 fast path (select64.cu); false when it does not apply

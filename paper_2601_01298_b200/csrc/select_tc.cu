@@ -256,6 +256,12 @@ struct SelxParams {
     float* x2c;               // [G][2][C * NW][D]: the candidates' coordinates
     unsigned* cnt;            // [G][2]: monotonic arrival counters (zeroed per launch)
     int C;                    // CTAs per group  // CX_EXPERIMENTS builds: per-round phase clocks of group 0, rank 0
+    // the fused landmark gather (A5, synapse.cpp:303-318): rank 0 copies the sorted picks'
+    // key rows (from X) and value rows (from V, the keys' group layout) into syn_k / syn_v
+    const float* V;
+    float* syn_k;
+    float* syn_v;
+    int64_t syn_gs;
 };
 
 #ifdef CX_EXPERIMENTS
@@ -1006,6 +1012,30 @@ __global__ void __launch_bounds__(NT, 1) selx_kernel(SelxParams p) {
             out_rows[pos] = r;
             out_scores[pos] = pick_scores[s];
         }
+        if (p.syn_k || p.syn_v) {  // the fused gather: one 16-B chunk per item, 4 loads in flight per thread
+            __syncthreads();       // the sorted rows are in out_rows
+            constexpr int CH = D / 4;
+            const int per = p.take * CH, items = per * ((p.syn_k ? 1 : 0) + (p.syn_v ? 1 : 0));
+            for (int i0 = tid; i0 < items; i0 += 4 * NT) {
+                float4 v[4];
+                float4* dst[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int it = i0 + u * NT;
+                    dst[u] = nullptr;
+                    if (it < items) {
+                        const int kv = it / per, sc = (it % per) / CH, c = it % CH;
+                        const bool isv = !p.syn_k || kv == 1;
+                        const float* src = (isv ? p.V : p.X) + g * p.gstride + out_rows[sc] * p.rstride;
+                        v[u] = __ldg(reinterpret_cast<const float4*>(src) + c);
+                        dst[u] = reinterpret_cast<float4*>((isv ? p.syn_v : p.syn_k) + g * p.syn_gs + (int64_t)sc * D) + c;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (dst[u]) *dst[u] = v[u];
+            }
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (CL) cg::this_cluster().sync();  // no CTA exits while a peer may still push into it
@@ -1207,7 +1237,9 @@ size_t select_tc_scratch(int G) {
 
 bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, const double* cen, int take,
                       double lambda, unsigned flags, int64_t* pick_rows, double* pick_scores, int64_t* rows,
-                      double* scores, double* gaps, void* scratch, cudaStream_t s) {
+                      double* scores, double* gaps, void* scratch, cudaStream_t s, const SynGather* gat,
+                      bool* gathered) {
+    if (gathered) *gathered = false;
     if (g.dim != D || (g.rstride & 3) != 0 || (g.gstride & 3) != 0 || (reinterpret_cast<uintptr_t>(g.X) & 15) != 0 ||
         g.L < 1)
         return false;
@@ -1233,6 +1265,23 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
     prm.x2h = nullptr;
     prm.x2c = nullptr;
     prm.cnt = nullptr;
+    prm.V = nullptr;
+    prm.syn_k = nullptr;
+    prm.syn_v = nullptr;
+    prm.syn_gs = 0;
+    {  // the gather goes into the kernel when every access is a 16-B chunk
+        auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+        if (gat && (gat->syn_k || (gat->syn_v && gat->values)) && (gat->syn_gs & 3) == 0 &&
+            (!gat->syn_k || a16(gat->syn_k)) && (!gat->syn_v || !gat->values || (a16(gat->syn_v) && a16(gat->values)))) {
+            prm.syn_k = gat->syn_k;
+            if (gat->syn_v && gat->values) {
+                prm.V = gat->values;
+                prm.syn_v = gat->syn_v;
+            }
+            prm.syn_gs = gat->syn_gs;
+            if (gathered) *gathered = true;
+        }
+    }
 #ifdef CX_EXPERIMENTS
     const char* tr = getenv("CX_SEL_TRACE");
     if (tr && tr[0] == '1') CX_CUDA(cudaMallocManaged(&prm.trace, sizeof(long long) * 16 * 4096));
@@ -1280,6 +1329,9 @@ bool select_tc_launch(const GroupView& g, const Options& o, const double* attn, 
             pw.out_rows = rows + (int64_t)g0 * take;
             pw.out_scores = scores + (int64_t)g0 * take;
             pw.gaps = gaps ? gaps + g0 : nullptr;
+            if (pw.V) pw.V += (int64_t)g0 * g.gstride;
+            if (pw.syn_k) pw.syn_k += (int64_t)g0 * pw.syn_gs;
+            if (pw.syn_v) pw.syn_v += (int64_t)g0 * pw.syn_gs;
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3((unsigned)cfg.C, (unsigned)ng, 1);
             lc.blockDim = dim3(NT, 1, 1);

@@ -934,10 +934,11 @@ void centroid_launch(const GroupView& g, double* cen, cudaStream_t s) {
     }
 }
 
-void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
-                    unsigned flags, int64_t* rows, double* scores, cudaStream_t s, const double* cen_in) {
+bool select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, double lambda,
+                    unsigned flags, int64_t* rows, double* scores, cudaStream_t s, const double* cen_in,
+                    const SynGather* gat) {
     const int take = (int)std::min<int64_t>(k, g.L);
-    if (take <= 0 || g.G <= 0) return;
+    if (take <= 0 || g.G <= 0) return true;  // nothing to gather either
     double* cen = ctx->arena.take<double>((size_t)g.G * g.dim);
     int64_t* pr = ctx->arena.take<int64_t>((size_t)g.G * take);
     double* ps = ctx->arena.take<double>((size_t)g.G * take);
@@ -958,15 +959,17 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     }
     ctx->gaps_n = g.G;
     const int impl = ctx->opt.select_impl;
+    bool gathered = false;
     if (!(flags & CX_SELECT_GENERIC) && impl != CX_SELECT_IMPL_CUDA_CORE &&
-        select_tc_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, tc_scratch, s))
-        return;
+        select_tc_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, tc_scratch, s,
+                         gat, &gathered))
+        return gathered;
     if (impl == CX_SELECT_IMPL_TC && !(flags & CX_SELECT_GENERIC))
         fail(CX_PRECONDITION_ERROR, "select: the pinned tensor-core selection does not apply to this shape");
     if (!(flags & CX_SELECT_GENERIC) &&
         (select64_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s) ||
          select128_launch(g, ctx->opt, attn, cen, take, lambda, flags, pr, ps, rows, scores, ctx->gaps, grec, s)))
-        return;
+        return false;
     // the generic kernel does not monitor: NaN (all-ones bits) = not measured
     CX_CUDA(cudaMemsetAsync(ctx->gaps, 0xFF, sizeof(double) * (size_t)g.G, s));
 
@@ -1000,6 +1003,7 @@ void select_grouped(cx_ctx* ctx, const GroupView& g, const double* attn, int k, 
     cfg.numAttrs = 1;
     CX_CUDA(cudaLaunchKernelEx(&cfg, select_kernel, prm));
     count_launch();
+    return false;
 }
 
 void gather_rows(const GroupView& g, const float* src, const int64_t* rows, int take, float* dst,
