@@ -12,6 +12,8 @@ from paper_2601_01298_b200 import device as cxd  # noqa: E402
 
 G, L, D, K, LAM, QPG = 48, 8192, 64, 164, 0.5, 7
 torch.cuda.set_device(0)
+for kv in filter(None, os.environ.get("OPTS", "").split(",")):  # e.g. OPTS=attn_impl=1
+    cxd.set_option(kv.split("=")[0], int(kv.split("=")[1]))
 dev = torch.device("cuda", 0)
 gen = torch.Generator(device=dev).manual_seed(1234)
 keys = torch.randn(G, L, D, device=dev, generator=gen)
@@ -51,5 +53,14 @@ e1.record()
 torch.cuda.synchronize()
 e2e = e0.elapsed_time(e1) / 10
 ok_h = all(torch.equal(a.cpu(), b) for a, b in zip(out, h_out))
-print(f"{os.environ.get('TAG', '')}: device {statistics.mean(times):.4f} ms (min {min(times):.4f}), "
+a_t = []
+for _ in range(10):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    cxd.attention_grouped(keys, queries)
+    e1.record()
+    torch.cuda.synchronize()
+    a_t.append(e0.elapsed_time(e1))
+print(f"{os.environ.get('TAG', '')}: attention {statistics.mean(a_t) * 1e3:.1f} us, device {statistics.mean(times):.4f} ms (min {min(times):.4f}), "
       f"e2e {e2e:.4f} ms, gather ok {ok}, host == device {ok_h}", flush=True)
