@@ -62,5 +62,15 @@ for _ in range(10):
     e1.record()
     torch.cuda.synchronize()
     a_t.append(e0.elapsed_time(e1))
-print(f"{os.environ.get('TAG', '')}: attention {statistics.mean(a_t) * 1e3:.1f} us, device {statistics.mean(times):.4f} ms (min {min(times):.4f}), "
+attn = cxd.attention_grouped(keys, queries)
+s_t = []
+for _ in range(10):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    cxd.select_grouped(keys, attn, K, LAM)
+    e1.record()
+    torch.cuda.synchronize()
+    s_t.append(e0.elapsed_time(e1))
+print(f"{os.environ.get('TAG', '')}: centroid+selection {statistics.mean(s_t):.4f} ms, attention {statistics.mean(a_t) * 1e3:.1f} us, device {statistics.mean(times):.4f} ms (min {min(times):.4f}), "
       f"e2e {e2e:.4f} ms, gather ok {ok}, host == device {ok_h}", flush=True)
