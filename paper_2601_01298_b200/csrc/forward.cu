@@ -200,7 +200,20 @@ __device__ __forceinline__ void stage_tile(float (*tile)[65], const float* src, 
 // of the (agent, head) to finish combines every chunk (no second launch).
 __global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch P, int l, int n_heads, int d_k,
                                                  const float* q, double* part, unsigned* counters, int n_chunks,
-                                                 float* att) {
+                                                 float* att, const char* pf, size_t pf_bytes) {
+    // the weights the next launches read (this layer's Wo / W_in / W_out, the next layer's
+    // Wq / Wk / Wv: contiguous) -> L2 while the cache rows stream: the matvecs that follow then
+    // start from L2 hits instead of HBM round trips.  Read-only data, so no ordering with the
+    // predecessor is needed.
+    if (threadIdx.x == 0 && pf_bytes) {
+        const size_t ncta = (size_t)gridDim.x * gridDim.y * gridDim.z;
+        const size_t cid = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const size_t share = ((pf_bytes + ncta - 1) / ncta + 255) & ~(size_t)255;
+        for (size_t o = cid * share; o < min(pf_bytes, (cid + 1) * share); o += 16384) {
+            const uint32_t n = (uint32_t)min((size_t)16384, min(pf_bytes, (cid + 1) * share) - o);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf + o), "r"(n) : "memory");
+        }
+    }
     pdl_enter();
     const int ch = blockIdx.x, h = blockIdx.y, b = blockIdx.z, t = threadIdx.x;
     const FwAgent& a = P.a[b];
@@ -495,8 +508,13 @@ void forward_batch(cx_ctx* c, const cx_weights* w, int nb, cx_kvcache* const* ca
         launch_pdl(fw_qkv_rope, dim3((unsigned)((pairs + 7) / 8)), dim3(256), s, true, P, l, W + w->wq(l), w->n_heads,
                    w->d_k, w->rope_base, (const float*)x, W + w->attn_norm(l), 1e-5, qb,
                    l == L - 1 ? final_query : nullptr);
+        // L2 prefetch of [Wo(l), Wv(l + 1) end): this layer's output / MLP weights and the next
+        // layer's q / k / v weights (the last layer: up to the end of its block)
+        const size_t pf0 = w->wo(l), pf1 = l + 1 < L ? w->wo(l + 1) : w->attn_norm(l) + w->per_layer;
         launch_pdl(fw_attend, dim3((unsigned)n_chunks, (unsigned)w->n_heads, (unsigned)nb), dim3(256), s, true, P, l,
-                   w->n_heads, w->d_k, (const float*)qb, part, c->fw_counters, n_chunks, att);
+                   w->n_heads, w->d_k, (const float*)qb, part, c->fw_counters, n_chunks, att,
+                   reinterpret_cast<const char*>(W + pf0),
+                   (reinterpret_cast<uintptr_t>(W + pf0) & 15) ? 0 : ((pf1 - pf0) * sizeof(float) & ~(size_t)15));
         matvec_launch(W + w->wo(l), d, d, att, nb, x, 2, s, nullptr, 1e-5, true);                // x += Wo att
         matvec_launch(W + w->w_in(l), dff, d, x, nb, ff, 1, s, W + w->mlp_norm(l), 1e-5, true);  // relu(W_in rmsnorm(x))
         matvec_launch(W + w->w_out(l), d, dff, ff, nb, x, 2, s, nullptr, 1e-5, true);            // x += W_out ff
