@@ -186,6 +186,11 @@ extern "C" cx_status cx_ctx_destroy(cx_ctx* c) {
         cudaStreamSynchronize(c->side);
         if (c->arena.base) cudaFree(c->arena.base);
         if (c->fw_counters) cudaFree(c->fw_counters);
+        for (auto& fg : c->fw_graphs) cudaGraphExecDestroy(fg.exec);
+        for (cudaEvent_t e : c->fw_ev)
+            if (e) cudaEventDestroy(e);
+        if (c->fw_dev) cudaFree(c->fw_dev);
+        if (c->fw_host) cudaFreeHost(c->fw_host);
         if (c->d_flag) cudaFree(c->d_flag);
         if (c->gaps) cudaFree(c->gaps);
         cudaEventDestroy(c->ev_fork);

@@ -147,6 +147,21 @@ struct cx_ctx {
     int num_sms = 0;
     unsigned* fw_counters = nullptr;  // forward_step attention: per (agent, head) chunk counters (kept zero)
     int fw_counters_n = 0;
+    // forward_step: the agents' batch lives in device memory (one H2D copy per step from a pinned
+    // staging ring), so a step's launch sequence is the same for every token and replays as a
+    // captured CUDA graph, keyed by everything the launches bake in
+    static constexpr int kFwRing = 16;
+    void* fw_dev = nullptr;                   // the batch (device)
+    void* fw_host = nullptr;                  // [kFwRing] batches (pinned)
+    cudaEvent_t fw_ev[kFwRing] = {};          // staging slot i is reusable once fw_ev[i] has fired
+    int fw_slot = 0;
+    struct FwGraph {
+        const void* key[8];
+        int nb, n_chunks;
+        cudaGraphExec_t exec;
+        uint64_t launches;
+    };
+    std::vector<FwGraph> fw_graphs;
     cx::Options opt;                // cx_ctx_set_option
     std::mutex mu;
 };

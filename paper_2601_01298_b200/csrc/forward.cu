@@ -15,7 +15,10 @@
 // once per launch and shared through L1/L2).  Attention splits every (agent, head)
 // over 128-entry chunks (partial max / sum / P.V in fp64, then a combine), so a
 // river with an 8192-row cache spreads over many CTAs.
+#include <algorithm>
 #include <cmath>
+#include <cstddef>
+#include <cstring>
 #include <memory>
 #include <vector>
 
@@ -41,8 +44,9 @@ struct FwAgent {
     int64_t position;
     int token;
 };
-// the batch travels as a kernel parameter: no host->device copy, so a forward step
-// never synchronizes its stream (a pageable cudaMemcpyAsync would)
+// the batch is copied to device memory once per step from a pinned staging slot (a pageable
+// cudaMemcpyAsync would synchronise the stream), so the kernels' parameters do not change from
+// token to token and the step replays as one CUDA graph
 struct FwBatch {
     int B;
     FwAgent a[FW_MAX_B];
@@ -62,7 +66,8 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-__global__ void fw_embed(const __grid_constant__ FwBatch P, const float* emb, int d, float* x) {
+__global__ void fw_embed(const FwBatch* __restrict__ Pd, const float* emb, int d, float* x) {
+    const FwBatch& P = *Pd;
     const int b = blockIdx.x;
     if (b >= P.B) return;
     for (int i = threadIdx.x; i < d; i += blockDim.x) x[(size_t)b * d + i] = emb[(size_t)P.a[b].token * d + i];
@@ -124,9 +129,10 @@ __global__ void fw_matvec(const float* W, int n_out, int n_in, const float* X, i
 // q, k, v = W{q,k,v} rmsnorm(x) for one rotation pair (2e, 2e+1) per warp, then RoPE on q and
 // k (kernels.cpp:49-62) and the new entry's K / V into the agent's cache at layer l
 // (model.cpp:142-152 write_layer); q (rotated) -> qbuf, and final_q at the last layer.
-__global__ void fw_qkv_rope(const __grid_constant__ FwBatch P, int l, const float* Wq, int n_heads, int d_k,
+__global__ void fw_qkv_rope(const FwBatch* __restrict__ Pd, int l, const float* Wq, int n_heads, int d_k,
                             double base, const float* x, const float* gain, double eps, float* qbuf, float* final_q) {
     pdl_enter();
+    const FwBatch& P = *Pd;
     const int d = n_heads * d_k;
     const int wpb = blockDim.x / 32, lane = threadIdx.x & 31;
     const long long item = (long long)blockIdx.x * wpb + threadIdx.x / 32;
@@ -198,7 +204,7 @@ __device__ __forceinline__ void stage_tile(float (*tile)[65], const float* src, 
 // [0, row + 1): K / V tiles staged through shared memory with coalesced loads; the chunk's
 // partial (max m, sum l of e^{s-m}, sum e^{s-m} v, all fp64) goes to `part`, and the last CTA
 // of the (agent, head) to finish combines every chunk (no second launch).
-__global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch P, int l, int n_heads, int d_k,
+__global__ void __launch_bounds__(256) fw_attend(const FwBatch* __restrict__ Pd, int l, int n_heads, int d_k,
                                                  const float* q, double* part, unsigned* counters, int n_chunks,
                                                  float* att, const char* pf, size_t pf_bytes) {
     // the weights the next launches read (this layer's Wo / W_in / W_out, the next layer's
@@ -215,6 +221,7 @@ __global__ void __launch_bounds__(256) fw_attend(const __grid_constant__ FwBatch
         }
     }
     pdl_enter();
+    const FwBatch& P = *Pd;
     const int ch = blockIdx.x, h = blockIdx.y, b = blockIdx.z, t = threadIdx.x;
     const FwAgent& a = P.a[b];
     const int64_t n = a.row + 1;
@@ -499,30 +506,94 @@ void forward_batch(cx_ctx* c, const cx_weights* w, int nb, cx_kvcache* const* ca
     float* ff = c->arena.take<float>((size_t)nb * dff);
     double* part = c->arena.take<double>((size_t)nb * w->n_heads * n_chunks * (2 + w->d_k));
     const float* W = w->buf;
-    fw_embed<<<nb, 128, 0, s>>>(P, W + w->emb, d, x);
-    check_launch("fw_embed");
-    const long long pairs = (long long)(d / 2) * nb;
-    for (int l = 0; l < L; ++l) {
-        // rmsnorm + q/k/v + RoPE + the cache append, one launch
-        // every launch after fw_embed is a programmatic dependent of the previous one
-        launch_pdl(fw_qkv_rope, dim3((unsigned)((pairs + 7) / 8)), dim3(256), s, true, P, l, W + w->wq(l), w->n_heads,
-                   w->d_k, w->rope_base, (const float*)x, W + w->attn_norm(l), 1e-5, qb,
-                   l == L - 1 ? final_query : nullptr);
-        // L2 prefetch of [Wo(l), Wv(l + 1) end): this layer's output / MLP weights and the next
-        // layer's q / k / v weights (the last layer: up to the end of its block)
-        const size_t pf0 = w->wo(l), pf1 = l + 1 < L ? w->wo(l + 1) : w->attn_norm(l) + w->per_layer;
-        launch_pdl(fw_attend, dim3((unsigned)n_chunks, (unsigned)w->n_heads, (unsigned)nb), dim3(256), s, true, P, l,
-                   w->n_heads, w->d_k, (const float*)qb, part, c->fw_counters, n_chunks, att,
-                   reinterpret_cast<const char*>(W + pf0),
-                   (reinterpret_cast<uintptr_t>(W + pf0) & 15) ? 0 : ((pf1 - pf0) * sizeof(float) & ~(size_t)15));
-        matvec_launch(W + w->wo(l), d, d, att, nb, x, 2, s, nullptr, 1e-5, true);                // x += Wo att
-        matvec_launch(W + w->w_in(l), dff, d, x, nb, ff, 1, s, W + w->mlp_norm(l), 1e-5, true);  // relu(W_in rmsnorm(x))
-        matvec_launch(W + w->w_out(l), d, dff, ff, nb, x, 2, s, nullptr, 1e-5, true);            // x += W_out ff
+    // the batch -> device memory (a pinned staging slot whose previous copy has long completed)
+    if (!c->fw_dev) {
+        CX_CUDA(cudaMalloc(&c->fw_dev, sizeof(FwBatch)));
+        CX_CUDA(cudaMallocHost(&c->fw_host, sizeof(FwBatch) * cx_ctx::kFwRing));
+        for (cudaEvent_t& e : c->fw_ev) CX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    {
+        const int slot = c->fw_slot;
+        c->fw_slot = (slot + 1) % cx_ctx::kFwRing;
+        CX_CUDA(cudaEventSynchronize(c->fw_ev[slot]));
+        FwBatch* hp = static_cast<FwBatch*>(c->fw_host) + slot;
+        const size_t bytes = offsetof(FwBatch, a) + sizeof(FwAgent) * (size_t)nb;
+        std::memcpy(hp, &P, bytes);
+        CX_CUDA(cudaMemcpyAsync(c->fw_dev, hp, bytes, cudaMemcpyHostToDevice, s));
+        CX_CUDA(cudaEventRecord(c->fw_ev[slot], s));
+    }
+    const FwBatch* Pd = static_cast<const FwBatch*>(c->fw_dev);
     float* hid = hidden ? hidden : hs;
-    launch_pdl(fw_rmsnorm, dim3((unsigned)((nb + 7) / 8)), dim3(256), s, true, (const float*)x, W + w->final_norm, d,
-               nb, hid, 1e-5);
-    if (logits) matvec_launch(W + w->unemb, w->vocab, d, hid, nb, logits, 0, s, nullptr, 1e-5, true);
+    auto issue = [&]() {
+        fw_embed<<<nb, 128, 0, s>>>(Pd, W + w->emb, d, x);
+        check_launch("fw_embed");
+        const long long pairs = (long long)(d / 2) * nb;
+        for (int l = 0; l < L; ++l) {
+            // rmsnorm + q/k/v + RoPE + the cache append, one launch
+            // every launch after fw_embed is a programmatic dependent of the previous one
+            launch_pdl(fw_qkv_rope, dim3((unsigned)((pairs + 7) / 8)), dim3(256), s, true, Pd, l, W + w->wq(l),
+                       w->n_heads, w->d_k, w->rope_base, (const float*)x, W + w->attn_norm(l), 1e-5, qb,
+                       l == L - 1 ? final_query : nullptr);
+            // L2 prefetch of [Wo(l), Wv(l + 1) end): this layer's output / MLP weights and the next
+            // layer's q / k / v weights (the last layer: up to the end of its block)
+            const size_t pf0 = w->wo(l), pf1 = l + 1 < L ? w->wo(l + 1) : w->attn_norm(l) + w->per_layer;
+            launch_pdl(fw_attend, dim3((unsigned)n_chunks, (unsigned)w->n_heads, (unsigned)nb), dim3(256), s, true, Pd,
+                       l, w->n_heads, w->d_k, (const float*)qb, part, c->fw_counters, n_chunks, att,
+                       reinterpret_cast<const char*>(W + pf0),
+                       (reinterpret_cast<uintptr_t>(W + pf0) & 15) ? 0 : ((pf1 - pf0) * sizeof(float) & ~(size_t)15));
+            matvec_launch(W + w->wo(l), d, d, att, nb, x, 2, s, nullptr, 1e-5, true);                // x += Wo att
+            matvec_launch(W + w->w_in(l), dff, d, x, nb, ff, 1, s, W + w->mlp_norm(l), 1e-5, true);  // relu(W_in rmsnorm(x))
+            matvec_launch(W + w->w_out(l), d, dff, ff, nb, x, 2, s, nullptr, 1e-5, true);            // x += W_out ff
+        }
+        launch_pdl(fw_rmsnorm, dim3((unsigned)((nb + 7) / 8)), dim3(256), s, true, (const float*)x, W + w->final_norm,
+                   d, nb, hid, 1e-5);
+        if (logits) matvec_launch(W + w->unemb, w->vocab, d, hid, nb, logits, 0, s, nullptr, 1e-5, true);
+    };
+    // replay the captured sequence (a named stream that is not already being captured)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    const bool named = s != nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread;
+    if (named) CX_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (!named || cs != cudaStreamCaptureStatusNone) {
+        issue();
+    } else {
+        const void* key[8] = {w, x, part, logits, hidden, final_query, c->fw_counters, c->fw_dev};
+        cx_ctx::FwGraph* hit = nullptr;
+        for (auto& fg : c->fw_graphs)
+            if (fg.nb == nb && fg.n_chunks == n_chunks && std::equal(key, key + 8, fg.key)) hit = &fg;
+        if (!hit) {
+            // the launches issue() makes (counted per replay, not at capture)
+            const uint64_t n = 2 + 5 * (uint64_t)L + (logits ? 1 : 0);
+            CX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            cudaGraph_t graph = nullptr;
+            try {
+                issue();
+            } catch (...) {
+                cudaStreamEndCapture(s, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            CX_CUDA(cudaStreamEndCapture(s, &graph));
+            count_launch(0 - n);  // captured, not launched: counted at each replay
+            cudaGraphExec_t exec = nullptr;
+            const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ie != cudaSuccess) fail(CX_DEVICE_ERROR, std::string("forward_step graph: ") + cudaGetErrorString(ie));
+            if (c->fw_graphs.size() >= 16) {  // oldest out
+                cudaGraphExecDestroy(c->fw_graphs.front().exec);
+                c->fw_graphs.erase(c->fw_graphs.begin());
+            }
+            cx_ctx::FwGraph fg{};
+            std::copy(key, key + 8, fg.key);
+            fg.nb = nb;
+            fg.n_chunks = n_chunks;
+            fg.exec = exec;
+            fg.launches = n;
+            c->fw_graphs.push_back(fg);
+            hit = &c->fw_graphs.back();
+        }
+        CX_CUDA(cudaGraphLaunch(hit->exec, s));
+        count_launch(hit->launches);
+    }
     // the entry is complete at every layer (end_entry)
     for (int b = 0; b < nb; ++b) {
         cx_kvcache* kc = caches[b];

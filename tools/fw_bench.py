@@ -1,6 +1,8 @@
 """forward_step cost on the cfg5 river (24 layers x d_model 128, L context rows):
 device time per token (CUDA events) and host issue time.  Usage:
-python tools/fw_bench.py [L] [n_tokens]"""
+python tools/fw_bench.py [L] [n_tokens]   (STREAM=1: on a created stream, where the step
+replays as a captured CUDA graph; the default stream issues the launches directly)"""
+import os
 import sys
 import time
 
@@ -21,6 +23,8 @@ torch.cuda.synchronize()
 river.append_context_dev(pk.data_ptr(), pv.data_ptr(), 0, L)
 torch.cuda.synchronize()
 logits = torch.empty(256, device="cuda")
+stream = torch.cuda.Stream() if os.environ.get("STREAM") == "1" else torch.cuda.current_stream()
+torch.cuda.set_stream(stream)
 for i in range(5):
     rt.forward_step_dev(w, [river], [i], [L + i], logits=logits)
 torch.cuda.synchronize()
