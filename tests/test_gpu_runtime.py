@@ -265,3 +265,44 @@ def test_cortex_gate_decides_before_injection(theta):
         assert 0 < ref_inj < len(ref_log) - 1, "the median threshold should split the thoughts"
     assert torch.equal(logits, ref_logits), "river logits differ from the gated replay"
     cx.close()
+
+
+def test_forward_step_graph_replay_matches_direct_launches():
+    """forward_step on a created stream replays a captured CUDA graph (the batch is read from
+    device memory); on the default stream it issues its launches directly.  Both must give
+    the same bits, token after token, across a chunk-count change (every 128 rows: a new
+    graph), a cache regrow (new K / V pointers inside the same graph) and a batch of two."""
+    from paper_2601_01298_b200 import runtime as rt
+    from paper_2601_01298_b200.model import KvCache, ModelConfig
+    cfg = ModelConfig(n_layers=3, n_heads=2, d_model=128, d_k=64, vocab_size=97, max_positions=4096)
+    w = rt.Weights(cfg, rt.random_flat_weights(cfg, 11))
+    L0, n = 100, 70  # rows 100 .. 170: crosses 128; capacity 130 forces a regrow
+    g = torch.Generator(device="cuda").manual_seed(4)
+    pk = torch.randn(3, L0, 128, device="cuda", generator=g)
+    pv = torch.randn(3, L0, 128, device="cuda", generator=g)
+
+    def run(stream):
+        caches = [KvCache(cfg, capacity=130), KvCache(cfg, capacity=130)]
+        torch.cuda.synchronize()
+        for c in caches:
+            c.append_context_dev(pk.data_ptr(), pv.data_ptr(), 0, L0)
+        torch.cuda.synchronize()
+        logits = torch.empty(n, 2, 97, device="cuda")
+        fq = torch.empty(n, 2, 128, device="cuda")
+        with torch.cuda.stream(stream):
+            for t in range(n):
+                batch = caches if t % 3 else caches[:1]  # batches of 2 and of 1 interleaved
+                rt.forward_step_dev(w, batch, [(7 * t + b) % 97 for b in range(len(batch))],
+                                    [L0 + t] * len(batch), logits=logits[t, :len(batch)],
+                                    final_query=fq[t, :len(batch)])
+        torch.cuda.synchronize()
+        for t in range(n):
+            if t % 3 == 0:
+                logits[t, 1] = 0.0
+                fq[t, 1] = 0.0
+        return logits.cpu(), fq.cpu()
+
+    direct = run(torch.cuda.default_stream())
+    graph = run(torch.cuda.Stream())
+    assert torch.isfinite(direct[0]).all()
+    assert torch.equal(direct[0], graph[0]) and torch.equal(direct[1], graph[1])
