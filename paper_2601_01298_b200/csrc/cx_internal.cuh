@@ -156,7 +156,7 @@ struct cx_ctx {
     cudaEvent_t fw_ev[kFwRing] = {};          // staging slot i is reusable once fw_ev[i] has fired
     int fw_slot = 0;
     struct FwGraph {
-        const void* key[8];
+        const void* key[10];
         int nb, n_chunks;
         cudaGraphExec_t exec;
         uint64_t launches;

@@ -556,10 +556,14 @@ void forward_batch(cx_ctx* c, const cx_weights* w, int nb, cx_kvcache* const* ca
     if (!named || cs != cudaStreamCaptureStatusNone) {
         issue();
     } else {
-        const void* key[8] = {w, x, part, logits, hidden, final_query, c->fw_counters, c->fw_dev};
+        // everything the captured launches bake in: the weights' device buffer and shape (a
+        // destroyed cx_weights' address may come back with other contents), scratch and outputs
+        const uintptr_t shape = (uintptr_t)L | (uintptr_t)d << 8 | (uintptr_t)w->vocab << 24 | (uintptr_t)w->n_heads << 48;
+        const void* key[10] = {w, w->buf, reinterpret_cast<const void*>(shape), x, part, logits, hidden,
+                               final_query, c->fw_counters, c->fw_dev};
         cx_ctx::FwGraph* hit = nullptr;
         for (auto& fg : c->fw_graphs)
-            if (fg.nb == nb && fg.n_chunks == n_chunks && std::equal(key, key + 8, fg.key)) hit = &fg;
+            if (fg.nb == nb && fg.n_chunks == n_chunks && std::equal(key, key + 10, fg.key)) hit = &fg;
         if (!hit) {
             // the launches issue() makes (counted per replay, not at capture)
             const uint64_t n = 2 + 5 * (uint64_t)L + (logits ? 1 : 0);
@@ -583,7 +587,7 @@ void forward_batch(cx_ctx* c, const cx_weights* w, int nb, cx_kvcache* const* ca
                 c->fw_graphs.erase(c->fw_graphs.begin());
             }
             cx_ctx::FwGraph fg{};
-            std::copy(key, key + 8, fg.key);
+            std::copy(key, key + 10, fg.key);
             fg.nb = nb;
             fg.n_chunks = n_chunks;
             fg.exec = exec;
