@@ -423,7 +423,12 @@ cx_status cx_weights_destroy(cx_weights* w);
  * Every agent is checked (token range, open entry, position bounds, strictly
  * increasing context positions) before any device work, with the reference's
  * error categories.  Projections, RMSNorm, RoPE and attention accumulate in fp64
- * (the reference's rounding points), so logits agree to ~1e-12 relative. */
+ * (the reference's rounding points), so logits agree to ~1e-12 relative.
+ * On a created stream the step's launch sequence is captured once per (weights,
+ * batch size, 128-row chunk count, scratch) and replayed as a CUDA graph (the
+ * agents' cache pointers / rows / positions / tokens go to device memory first);
+ * on the default stream, or a stream the caller is capturing, the launches are
+ * issued directly.  Both give the same bits. */
 cx_status cx_forward_step_dev(cx_ctx* ctx, const cx_weights* w, int n_agents, cx_kvcache* const* caches,
                               const int* tokens, const int64_t* positions, float* logits,
                               float* hidden, float* final_query, void* stream);
