@@ -700,17 +700,17 @@ void compress_impl(cx_ctx* c, const cx_groups* gr, const float* values, int k, d
         // fork: the centroids (A2, a latency-bound serial sum per coordinate)
         // run on the side stream while the attention mass (A3) runs on `s`
 #ifdef CX_EXPERIMENTS
-        // timing only (results invalid): 1 = skip the centroids, 2 = skip the attention mass
+        // timing only (results invalid): 1 = skip the centroids, 2 = skip the attention mass, 3 = both
         const int skip_pro = getenv("CX_EXP_PROLOGUE") ? atoi(getenv("CX_EXP_PROLOGUE")) : 0;
 #else
         const int skip_pro = 0;
 #endif
         CX_CUDA(cudaEventRecord(c->ev_fork, s));
         CX_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-        if (skip_pro != 1) centroid_launch(g, cen, c->side);
+        if (skip_pro != 1 && skip_pro != 3) centroid_launch(g, cen, c->side);
         CX_CUDA(cudaEventRecord(c->ev_join, c->side));
         const size_t mark = c->arena.used;
-        if (skip_pro != 2) attention_grouped(c, g, attn, s);
+        if (skip_pro != 2 && skip_pro != 3) attention_grouped(c, g, attn, s);
         c->arena.used = mark;  // attention scratch is dead once `attn` is written (stream-ordered)
         CX_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
         const int64_t gs = syn_gstride > 0 ? syn_gstride : (int64_t)take * g.dim;
