@@ -623,3 +623,44 @@ def test_group_shards_match_the_full_cfg2_compression(dev, world):
         torch.cuda.synchronize()
         for x, y in zip(full, part):
             assert torch.equal(x[b:e], y), f"rank {r} of {world}: groups {b}..{e} differ"
+
+
+@pytest.mark.parametrize("which", ["keys_only", "values_only", "no_values", "strided", "unaligned"])
+def test_compress_partial_synapse_outputs(dev, which):
+    """cx_compress_grouped_dev with one synapse output NULL, no values, a strided synapse
+    layout, or an output the fused in-kernel gather cannot take (not 16-B aligned: the
+    separate gather launch runs): the rows are the same and every requested synapse block
+    equals the selected source rows."""
+    import ctypes as C
+    import torch
+    G, L, D, k = 4, 3000, 64, 37
+    g = torch.Generator(device="cuda").manual_seed(21)
+    kt = torch.randn(G, L, D, device="cuda", generator=g)
+    vt = torch.randn(G, L, D, device="cuda", generator=g)
+    qt = torch.randn(G, 7, D, device="cuda", generator=g)
+    ref_rows = dev.compress_grouped(kt, vt, qt, k, 0.5)[0]
+    rows = torch.empty(G, k, dtype=torch.int64, device="cuda")
+    scores = torch.empty(G, k, dtype=torch.float64, device="cuda")
+    gs = k * D + (64 if which == "strided" else 0)  # floats between synapse blocks
+    off = 1 if which == "unaligned" else 0
+    sk = torch.full((G * gs + off,), float("nan"), device="cuda")
+    sv = torch.full((G * gs + off,), float("nan"), device="cuda")
+    kp = None if which == "values_only" else sk.data_ptr() + 4 * off
+    vp = None if which in ("keys_only", "no_values") else sv.data_ptr() + 4 * off
+    vals = None if which == "no_values" else vt.data_ptr()
+    grp = dev._groups(kt, qt, "gqa")
+    st = dev.lib.cx_compress_grouped_strided_dev(dev.ctx(0), C.byref(grp), vals, k, C.c_double(0.5), 0,
+                                                  rows.data_ptr(), scores.data_ptr(), kp, vp, gs, None)
+    assert st == 0, dev.lib.cx_last_error()
+    torch.cuda.synchronize()
+    assert torch.equal(rows, ref_rows)
+    idx = rows.unsqueeze(-1).expand(G, k, D)
+    blk = lambda t: t[off:].view(G, gs)[:, :k * D].view(G, k, D)  # noqa: E731
+    if kp is not None:
+        assert torch.equal(blk(sk), torch.gather(kt, 1, idx))
+    else:
+        assert torch.isnan(sk).all()
+    if vp is not None:
+        assert torch.equal(blk(sv), torch.gather(vt, 1, idx))
+    else:
+        assert torch.isnan(sv).all()
