@@ -428,13 +428,14 @@ def finish_b200(args, rank, world, dev, ms, sel_ms, value, launches, clk, keys, 
         print(json.dumps(line), flush=True)
 
 
-def ncu_traffic(kernel_substr):
+def ncu_traffic(kernel_substr, capture="full"):
     """dram__bytes_read.sum + dram__bytes_write.sum (bytes, one launch) of a kernel
-    from the newest committed `ncu --set full` summary (profiles/r<N>_ncu_full_summary.json,
-    made by tools/ncu_summary.py from `ncu ... python tools/prof_step.py`), or None."""
+    from the newest committed `ncu --set full` summary (profiles/r<N>_ncu_<capture>_summary.json,
+    made by tools/ncu_summary.py from `ncu ... python tools/prof_step.py`), or None.
+    capture "full": one compression + one N=1000 decode step; "dec100": one N=100 decode step."""
     prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
-    path = next((os.path.join(prof, f"{t}_ncu_full_summary.json") for t in ("r2", "r1")
-                 if os.path.exists(os.path.join(prof, f"{t}_ncu_full_summary.json"))), "")
+    path = next((os.path.join(prof, f"{t}_ncu_{capture}_summary.json") for t in ("r2", "r1")
+                 if os.path.exists(os.path.join(prof, f"{t}_ncu_{capture}_summary.json"))), "")
     try:
         with open(path) as f:
             rows = json.load(f)
@@ -525,7 +526,8 @@ def run_decode(args, dev, rank=0, world=1):
                               "kernel": "decode_tc_kernel (tcgen05 synapse + CUDA-core private rows)",
                               "roofline": {"bound": "hbm", "achieved": b / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                                            "frac": b / (ms * 1e-3) / 1e9 / hbm, "bytes": b,
-                                           "traffic": ncu_traffic("decode_tc_kernel") if n == 1000 else None}}
+                                           "traffic": ncu_traffic("decode_tc_kernel", {1000: "full", 100: "dec100"}[n])
+                                           if n in (100, 1000) else None}}
     return out
 
 

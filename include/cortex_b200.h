@@ -180,6 +180,9 @@ cx_status cx_select_grouped_dev(cx_ctx* ctx, const cx_groups* g, const double* a
                                        (DSMEM), 2 cooperative launch (global-memory exchanges),
                                        3 split: co-resident clusters + a cooperative launch for the
                                        remaining groups on the free SMs, side by side in one wave */
+#define CX_OPT_HOST_STAGE_OUTPUTS 8 /* 1 = host path stages the synapse K/V on the device and copies
+                                       it back even when the caller's buffers are pinned (default 0:
+                                       the landmark gather writes them straight into pinned memory) */
 #define CX_DECODE_AUTO 0            /* tcgen05, then v2, then the generic kernel */
 #define CX_DECODE_TC 1              /* pinned: an error if the shape does not apply */
 #define CX_DECODE_V2 2
@@ -231,7 +234,9 @@ cx_status cx_compress_grouped_strided_dev(cx_ctx* ctx, const cx_groups* g, const
  * stream so the upload of chunk i+1 overlaps the compression of chunk i (true
  * overlap needs pinned host memory).  When `values` is pinned (device-accessible),
  * only the selected value rows cross PCIe (zero-copy gather); otherwise all of
- * it is uploaded.  Synchronous: returns with outputs written.
+ * it is uploaded.  When syn_keys and syn_values are both pinned, the landmark
+ * gather writes them in place over PCIe (no device copy, no D2H; see
+ * CX_OPT_HOST_STAGE_OUTPUTS).  Synchronous: returns with outputs written.
  * Same checks, in the same order, as cx_compress_grouped_dev. */
 cx_status cx_compress_grouped_host(cx_ctx* ctx, int n_groups, int64_t count, int dim,
                                    const float* keys, const float* values, const float* queries,

@@ -619,6 +619,7 @@ extern "C" cx_status cx_ctx_set_option(cx_ctx* c, int option, int64_t value) {
             case CX_OPT_DECODE_IMPL: c->opt.decode_impl = in(CX_DECODE_AUTO, CX_DECODE_V1); break;
             case CX_OPT_DECODE_CTAS_PER_LH: c->opt.decode_ctas_per_lh = in(0, 1 << 16); break;
             case CX_OPT_HOST_UPLOAD_VALUES: c->opt.host_upload_values = in(0, 1); break;
+            case CX_OPT_HOST_STAGE_OUTPUTS: c->opt.host_stage_outputs = in(0, 1); break;
             case CX_OPT_SELECT_IMPL: c->opt.select_impl = in(CX_SELECT_IMPL_AUTO, CX_SELECT_IMPL_CUDA_CORE); break;
             case CX_OPT_SELECT_EXCHANGE: c->opt.select_exchange = in(0, 3); break;
             default: fail(CX_INVALID_ARGUMENT, "ctx_set_option: unknown option");
@@ -636,6 +637,7 @@ extern "C" cx_status cx_ctx_get_option(cx_ctx* c, int option, int64_t* value) {
             case CX_OPT_DECODE_IMPL: *value = c->opt.decode_impl; break;
             case CX_OPT_DECODE_CTAS_PER_LH: *value = c->opt.decode_ctas_per_lh; break;
             case CX_OPT_HOST_UPLOAD_VALUES: *value = c->opt.host_upload_values; break;
+            case CX_OPT_HOST_STAGE_OUTPUTS: *value = c->opt.host_stage_outputs; break;
             case CX_OPT_SELECT_IMPL: *value = c->opt.select_impl; break;
             case CX_OPT_SELECT_EXCHANGE: *value = c->opt.select_exchange; break;
             default: fail(CX_INVALID_ARGUMENT, "ctx_get_option: unknown option");
@@ -796,6 +798,21 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
                 vdev = reinterpret_cast<const float*>(pa.devicePointer);
             cudaGetLastError();
         }
+        // Likewise the synapse K/V: when both output buffers are pinned, the landmark gather
+        // writes the rows straight into them (posted PCIe writes, overlapping the gather's
+        // reads) instead of a device copy plus a 4 MB D2H after the selection.
+        float* hsk = nullptr;
+        float* hsv = nullptr;
+        if (syn_keys && syn_values && !c->opt.host_stage_outputs) {
+            cudaPointerAttributes ka{}, va{};
+            if (cudaPointerGetAttributes(&ka, syn_keys) == cudaSuccess && ka.type == cudaMemoryTypeHost &&
+                ka.devicePointer != nullptr && cudaPointerGetAttributes(&va, syn_values) == cudaSuccess &&
+                va.type == cudaMemoryTypeHost && va.devicePointer != nullptr) {
+                hsk = reinterpret_cast<float*>(ka.devicePointer);
+                hsv = reinterpret_cast<float*>(va.devicePointer);
+            }
+            cudaGetLastError();
+        }
         // device staging: keys | values | queries | rows | scores | syn_k | syn_v (256-B aligned slices)
         auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
         const size_t b_k = al(sizeof(float) * in_g * n_groups), b_q = al(sizeof(float) * q_g * n_groups);
@@ -821,6 +838,10 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         double* ds = reinterpret_cast<double*>(p); p += b_s;
         float* dsk = reinterpret_cast<float*>(p); p += b_o;
         float* dsv = reinterpret_cast<float*>(p); p += b_o;
+        if (hsk) {  // gather destinations: the caller's pinned buffers
+            dsk = hsk;
+            dsv = hsv;
+        }
         double* dattn = reinterpret_cast<double*>(p); p += b_a;
         double* dcen = reinterpret_cast<double*>(p);
         // Chunks of groups, one selection wave each (the cost model's co-resident clusters:
@@ -949,9 +970,9 @@ extern "C" cx_status cx_compress_grouped_host(cx_ctx* c, int n_groups, int64_t c
         }
         CX_CUDA(cudaMemcpyAsync(out_rows, dr, sizeof(int64_t) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));
         CX_CUDA(cudaMemcpyAsync(out_scores, ds, sizeof(double) * take * n_groups, cudaMemcpyDeviceToHost, c->stream));
-        if (syn_keys)
+        if (syn_keys && !hsk)
             CX_CUDA(cudaMemcpyAsync(syn_keys, dsk, sizeof(float) * o_g * n_groups, cudaMemcpyDeviceToHost, c->stream));
-        if (syn_values)
+        if (syn_values && !hsk)
             CX_CUDA(cudaMemcpyAsync(syn_values, dsv, sizeof(float) * o_g * n_groups, cudaMemcpyDeviceToHost, c->stream));
         check_flag_and_sync(x);  // non-finite attention input -> precondition_error (kernels.cpp:70)
         check_flag_and_sync(c);

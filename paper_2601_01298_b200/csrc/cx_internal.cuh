@@ -60,6 +60,7 @@ struct Options {
     int decode_impl = 0;         // CX_OPT_DECODE_IMPL: CX_DECODE_{AUTO,TC,V2,V1}
     int decode_ctas_per_lh = 0;  // CX_OPT_DECODE_CTAS_PER_LH: tcgen05 decode CTAs per (layer, KV head) (0 = auto)
     int host_upload_values = 0;  // CX_OPT_HOST_UPLOAD_VALUES: host path uploads all values even when pinned
+    int host_stage_outputs = 0;  // CX_OPT_HOST_STAGE_OUTPUTS: host path copies the synapse back even when pinned
 };
 
 // One NVTX range per C-ABI call (named after the entry point) and per runtime phase: an

@@ -236,7 +236,8 @@ def gate_decide(h: torch.Tensor, t: torch.Tensor, theta: float):
 
 
 OPTIONS = {"select_cluster": 1, "select_no_sketch": 2, "decode_impl": 3, "decode_ctas_per_lh": 4,
-           "host_upload_values": 5, "select_impl": 6, "select_exchange": 7}
+           "host_upload_values": 5, "select_impl": 6, "select_exchange": 7,
+           "host_stage_outputs": 8}
 DECODE_IMPLS = {"auto": 0, "tc": 1, "v2": 2, "v1": 3}
 SELECT_IMPLS = {"auto": 0, "tc": 1, "cuda_core": 2}
 

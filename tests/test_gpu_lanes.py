@@ -216,3 +216,35 @@ def test_decode_tail_len_out_of_range_is_flagged(cx_option, impl):
         assert torch.equal(tk[a][:, :, keep], tk0[a][:, :, keep])
     device.decode_step(sk, sv, tk, tv, tl, q, out)  # no append: tail_len == t_cap would be valid
     assert device.device_errors() == 0
+
+
+@pytest.mark.parametrize("G,L,k", [(48, 8192, 164), (13, 1500, 60)])
+def test_compress_grouped_host_pinned_outputs(cx, G, L, k):
+    """Pinned synapse outputs are written in place by the landmark gather (zero-copy);
+    staged (CX_OPT_HOST_STAGE_OUTPUTS = 1) and mixed pinned / pageable outputs take the
+    device copy + D2H.  All three give the same bits, equal to the selected host rows."""
+    import torch
+    from paper_2601_01298_b200 import device
+    gen = torch.Generator().manual_seed(5 + G)
+    hk = torch.randn(G, L, 64, generator=gen).pin_memory()
+    hv = torch.randn(G, L, 64, generator=gen).pin_memory()
+    hq = torch.randn(G, 7, 64, generator=gen).pin_memory()
+
+    def outs(pin_k, pin_v):
+        return (torch.empty(G, k, dtype=torch.int64).pin_memory(), torch.empty(G, k, dtype=torch.float64).pin_memory(),
+                torch.full((G, k, 64), float("nan"), pin_memory=pin_k),
+                torch.full((G, k, 64), float("nan"), pin_memory=pin_v))
+
+    zero_copy = device.compress_grouped_host(hk, hv, hq, k, 0.5, out=outs(True, True))
+    mixed = device.compress_grouped_host(hk, hv, hq, k, 0.5, out=outs(True, False))
+    old = device.set_option("host_stage_outputs", 1)
+    try:
+        staged = device.compress_grouped_host(hk, hv, hq, k, 0.5, out=outs(True, True))
+    finally:
+        device.set_option("host_stage_outputs", old)
+    for other in (mixed, staged):
+        for a, b in zip(zero_copy, other):
+            assert torch.equal(a, b)
+    gi = torch.arange(G)[:, None]
+    rows = zero_copy[0]
+    assert torch.equal(zero_copy[2], hk[gi, rows]) and torch.equal(zero_copy[3], hv[gi, rows])
